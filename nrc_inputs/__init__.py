@@ -1,0 +1,103 @@
+"""Seeded synthetic inputs shared (as DATA, not code) by the oracle tests, the
+CUDA parity tests and bench.py.
+
+This module holds none of the method's arithmetic: it draws cache records
+shaped like the paper's workload and evaluates a fixed analytic radiance
+field used as training targets.  Record layout (16 fp32 = 64 B, the shape of
+a cache query, Table 1):
+
+    pos[3] dir[3] normal[3] roughness diffuse[3] specular[3]
+
+Distribution ("input recipe"):
+  * pos ~ U[0,1)^3 (AABB = unit cube),
+  * dir, normal = normalised N(0, I3), rejecting |y| < 1e-7 (avoids the
+    signed-zero seam of atan2 at phi = +-pi),
+  * roughness ~ Exp(mean 0.5),
+  * diffuse ~ U[0,0.6)^3, specular ~ U[0,0.4)^3 (alpha + beta <= 1).
+
+Seeds: queries 0x1080, training frame f -> 0x7EA1 + f,
+convergence step j -> 0xC3 + j, weights seed 1.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+REC_FLOATS = 16
+SEED_QUERY = 0x1080
+SEED_TRAIN = 0x7EA1
+SEED_C3 = 0xC3
+SEED_WEIGHTS = 1
+
+# C2 / C5 workload sizes
+N_1080P = 1920 * 1080
+N_4K = 3840 * 2160
+TRAIN_S = 4
+TRAIN_L = 16384
+
+
+def _unit_vectors(rng: np.random.Generator, n: int) -> np.ndarray:
+    out = np.empty((n, 3), np.float32)
+    filled = 0
+    while filled < n:
+        k = n - filled
+        v = rng.standard_normal((k + 16, 3))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        v = v.astype(np.float32)
+        ok = (np.abs(v[:, 1]) >= 1e-7) & np.all(np.isfinite(v), axis=1)
+        v = v[ok][:k]
+        out[filled:filled + v.shape[0]] = v
+        filled += v.shape[0]
+    return out
+
+
+def records(n: int, seed: int = SEED_QUERY) -> np.ndarray:
+    """n synthetic cache records, float32 [n, 16]."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    r = np.empty((n, REC_FLOATS), np.float32)
+    r[:, 0:3] = rng.random((n, 3), dtype=np.float32)
+    r[:, 3:6] = _unit_vectors(rng, n)
+    r[:, 6:9] = _unit_vectors(rng, n)
+    r[:, 9] = rng.exponential(0.5, n).astype(np.float32)
+    r[:, 10:13] = (rng.random((n, 3)) * 0.6).astype(np.float32)
+    r[:, 13:16] = (rng.random((n, 3)) * 0.4).astype(np.float32)
+    return r
+
+
+_F = np.array([[3.0, 1.0, 2.0], [1.0, 4.0, 2.0], [2.0, 2.0, 5.0]])
+
+
+def radiance_field(recs: np.ndarray) -> np.ndarray:
+    """Analytic stand-in for the scattered radiance L_s (Eq. 1):
+    (alpha+beta) * (0.5 + 0.4 sin(2 pi F p + (0,1,2)) + 2 max(0, w.n)^(1/(0.05 + 1 - e^-r)) (1, .8, .6)).
+    Smooth in position, glossy lobe in direction; fp64 evaluation -> fp32."""
+    p = recs[:, 0:3].astype(np.float64)
+    w = recs[:, 3:6].astype(np.float64)
+    nrm = recs[:, 6:9].astype(np.float64)
+    r = recs[:, 9].astype(np.float64)
+    refl = recs[:, 10:13].astype(np.float64) + recs[:, 13:16].astype(np.float64)
+    base = 0.5 + 0.4 * np.sin(2 * np.pi * p @ _F.T + np.array([0.0, 1.0, 2.0]))
+    cosw = np.clip(np.sum(w * nrm, axis=1), 0.0, None)
+    expo = 1.0 / (0.05 + 1.0 - np.exp(-np.maximum(r, 0.0)))
+    lobe = 2.0 * cosw[:, None] ** expo[:, None] * np.array([1.0, 0.8, 0.6])
+    return (refl * (base + lobe)).astype(np.float32)
+
+
+def targets(recs: np.ndarray, noise: float = 0.0, seed: int = 0) -> np.ndarray:
+    """Training targets: the analytic field, optionally with unbiased
+    log-normal multiplicative noise exp(N(0, noise^2)) / E[.] (the noisy
+    regime the relative loss targets)."""
+    t = radiance_field(recs).astype(np.float64)
+    if noise > 0:
+        rng = np.random.Generator(np.random.PCG64(seed ^ 0x5EED))
+        t *= np.exp(rng.normal(0.0, noise, t.shape) - 0.5 * noise * noise)
+    return t.astype(np.float32)
+
+
+def train_frame(frame: int = 0, n: int = TRAIN_S * TRAIN_L, noise: float = 0.0):
+    """One frame's training records + targets (65,536 by default)."""
+    rec = records(n, SEED_TRAIN + frame)
+    return rec, targets(rec, noise, SEED_TRAIN + frame)
+
+
+def query_batch(n: int = N_1080P, seed: int = SEED_QUERY) -> np.ndarray:
+    return records(n, seed)

@@ -1,0 +1,464 @@
+/*
+ * nrc_oracle.c -- plain, slow, fp64 CPU ORACLE for the Neural Radiance Caching
+ * hot path (Mueller, Rousselle, Novak, Keller, "Real-time Neural Radiance
+ * Caching for Path Tracing", arXiv 2106.12372).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2106_12372_b200/, libnrc.so) never links, imports
+ * or calls anything in oracle/; the two share no code, headers, tables or
+ * constant generators.  Inputs reach both sides only through nrc_inputs/
+ * (seeded generators, no method arithmetic).
+ *
+ * Citations: "P:L<n>" = /root/reference/PAPER.md line n; "S:L<n>" = SPEC.md
+ * line n; numbered readings (R1..R20) are listed in DESIGN.md section 3.
+ *
+ * Every function is the plain definition written out, in the paper's order
+ * and notation: no blocking, fusion or reordering.  fp64 throughout, except
+ * the position normalisation step (R3), which both sides fix to fp32 so the
+ * integer floor parts of the triangle wave are bit-identical.
+ *
+ * Parity status of each function (pins live in tests/test_oracle_*.py):
+ *   orc_tri, orc_quartic, orc_one_blob, orc_sph, orc_freq ... pinned (closed
+ *       forms, SPEC worked examples, periodicity, integral of quartic = 1)
+ *   orc_encode ............................................. pinned (golden
+ *       vector tests/golden/encode_c0.txt, structural invariants)
+ *   orc_forward / orc_query ................................ pinned (zero net,
+ *       constant net via pad channel, linear chain, homogeneity, permutation)
+ *   orc_loss ............................................... pinned (S:L193-195
+ *       values 0.2493766 and 33.333, FD with frozen luminance)
+ *   orc_backward / orc_grad_batch .......................... pinned (central
+ *       finite differences, zero-gradient, 1-layer outer product)
+ *   orc_adam ............................................... pinned (zero grad,
+ *       first-step |dw| = lr|g|/(|g|+eps), monotonicity)
+ *   orc_ema ................................................ pinned (t=1,
+ *       constant stream 1e4 steps, a=0, linearity, printed-form 0.5124*C)
+ *   orc_lcg_* .............................................. pinned (S:L274
+ *       example [3,0,1,2], bijection for many n)
+ *   orc_init_weights ....................................... pinned (Glorot
+ *       bound, moments of the uniform distribution)
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+/* ---- architecture (reading R1: 6 weight matrices) ------------ */
+#define ORC_IN 64     /* 62 encoded dims padded to 64            */
+#define ORC_HID 64    /* "five hidden layers have 64 neurons each"  */
+#define ORC_OUT 3     /* "reduces the 64 dimensions to three RGB values"     */
+#define ORC_NMAT 6
+/* logical parameter layout: W0..W4 (64x64), W5 (3x64), row-major [out][in] */
+#define ORC_NPARAM (5 * 64 * 64 + 3 * 64)
+
+static const int64_t orc_mat_off[ORC_NMAT + 1] = {0, 4096, 8192, 12288, 16384, 20480, 20672};
+static const int orc_mat_rows[ORC_NMAT] = {64, 64, 64, 64, 64, 3};
+
+int64_t orc_param_count(void) { return ORC_NPARAM; }
+
+/* ---- cheap primitives, fig:cheap_primitives ------------------ */
+
+/* tri(x) := 2 | x mod 2 - 1 | - 1 with floored modulo. */
+double orc_tri(double x)
+{
+    double m = x - 2.0 * floor(x / 2.0); /* x mod 2 in [0, 2) */
+    return 2.0 * fabs(m - 1.0) - 1.0;
+}
+
+/* quartic(x) := 15/16 (1 - x^2)^2 on |x| <= 1, else 0. */
+double orc_quartic(double x)
+{
+    if (fabs(x) > 1.0) return 0.0;
+    double t = 1.0 - x * x;
+    return 15.0 / 16.0 * t * t;
+}
+
+/* One-blob encoding with k evenly spaced kernels (k=4 P:L588).
+ * Reading R6: centres (i+1/2)/k, width 1/k, input clamped to [0,1]. */
+void orc_one_blob(double s, int k, double* out)
+{
+    if (s < 0.0) s = 0.0;
+    if (s > 1.0) s = 1.0;
+    for (int i = 0; i < k; ++i) {
+        double c = (i + 0.5) / k;
+        out[i] = orc_quartic((s - c) * k);
+    }
+}
+
+/* sph(u): conversion to spherical coordinates normalised to [0,1]^2
+ * (Table 1 caption).  Reading R7: theta' = acos(z)/pi,
+ * phi' = (atan2(y,x)+pi)/(2 pi), order (theta', phi'); zero vector -> (0,0,1).
+ * Returns 1 if the input was the zero vector (counted by callers). */
+int orc_sph(const double* u_in, double* out)
+{
+    double x = u_in[0], y = u_in[1], z = u_in[2];
+    double len = sqrt(x * x + y * y + z * z);
+    int degenerate = 0;
+    if (!(len > 0.0)) {
+        x = 0.0; y = 0.0; z = 1.0;
+        degenerate = 1;
+    } else {
+        x /= len; y /= len; z /= len;
+    }
+    if (z > 1.0) z = 1.0;
+    if (z < -1.0) z = -1.0;
+    out[0] = acos(z) / M_PI;
+    out[1] = (atan2(y, x) + M_PI) / (2.0 * M_PI);
+    return degenerate;
+}
+
+/* Frequency encoding with 12 triangle waves of frequency 2^d, d = 0..11,
+ * cosine terms omitted (tri replaces sin).
+ * Reading R4: entry d = tri(2^d v). */
+void orc_freq(double v, double* out12)
+{
+    for (int d = 0; d < 12; ++d) out12[d] = orc_tri(ldexp(v, d));
+}
+
+/* Position normalisation (reading R3): v = fp32(fp32(p - lo) * inv),
+ * inv = fp32(1 / fp32(hi - lo)), no clamp, no FMA contraction. */
+float orc_normalize_pos(float p, float lo, float hi)
+{
+    volatile float ext = hi - lo;
+    volatile float inv = 1.0f / ext;
+    volatile float d = p - lo;
+    volatile float v = d * inv;
+    return v;
+}
+
+/* Input encoding, Table 1 + padding.
+ * record layout (nrc_inputs, 16 floats): pos[3] dir[3] normal[3] roughness
+ * diffuse[3] specular[3].  Output e[64] (readings R4-R6, R19):
+ *   e[12a+d]  = tri(2^d v_a)           a = x,y,z; d = 0..11   (36)
+ *   e[36..39] = ob(theta'(omega)), e[40..43] = ob(phi'(omega))   (8)
+ *   e[44..47] = ob(theta'(n)),     e[48..51] = ob(phi'(n))       (8)
+ *   e[52..55] = ob(1 - exp(-r))                                  (4)
+ *   e[56..58] = alpha, e[59..61] = beta (identity)       (6)
+ *   e[62] = e[63] = 1 (pad with a value of 1)            (2)
+ * Returns the number of degenerate (zero) direction vectors. */
+int orc_encode(const float* rec, const float* aabb_lo, const float* aabb_hi, double* e)
+{
+    int degenerate = 0;
+    for (int a = 0; a < 3; ++a) {
+        float v = orc_normalize_pos(rec[a], aabb_lo[a], aabb_hi[a]);
+        orc_freq((double)v, e + 12 * a);
+    }
+    double u[3], sp[2];
+    u[0] = rec[3]; u[1] = rec[4]; u[2] = rec[5];
+    degenerate += orc_sph(u, sp);
+    orc_one_blob(sp[0], 4, e + 36);
+    orc_one_blob(sp[1], 4, e + 40);
+    u[0] = rec[6]; u[1] = rec[7]; u[2] = rec[8];
+    degenerate += orc_sph(u, sp);
+    orc_one_blob(sp[0], 4, e + 44);
+    orc_one_blob(sp[1], 4, e + 48);
+    double r = rec[9];
+    if (r < 0.0) r = 0.0;
+    orc_one_blob(1.0 - exp(-r), 4, e + 52); /* ob(1 - e^{-r}) */
+    for (int c = 0; c < 3; ++c) e[56 + c] = rec[10 + c];
+    for (int c = 0; c < 3; ++c) e[59 + c] = rec[13 + c];
+    e[62] = 1.0;
+    e[63] = 1.0;
+    return degenerate;
+}
+
+void orc_encode_batch(const float* recs, int64_t n, const float* lo, const float* hi, double* E)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) orc_encode(recs + 16 * i, lo, hi, E + 64 * i);
+}
+
+/* ---- network (fig:fully-fused-illustration (a) P:L545) -------
+ * H[0] = e; H[i+1] = ReLU(W_i H[i]), i = 0..4; y = W_5 H[5] (linear output,
+ * reading R2).  W in the logical layout (row-major [out][in]). */
+void orc_forward(const double* W, const double* e, double* H /* 6*64 */, double* y /* 3 */)
+{
+    for (int k = 0; k < ORC_IN; ++k) H[k] = e[k];
+    for (int i = 0; i < 5; ++i) {
+        const double* Wi = W + orc_mat_off[i];
+        const double* hin = H + 64 * i;
+        double* hout = H + 64 * (i + 1);
+        for (int o = 0; o < 64; ++o) {
+            double acc = 0.0;
+            for (int k = 0; k < 64; ++k) acc += Wi[64 * o + k] * hin[k];
+            hout[o] = acc > 0.0 ? acc : 0.0;
+        }
+    }
+    const double* W5 = W + orc_mat_off[5];
+    for (int o = 0; o < 3; ++o) {
+        double acc = 0.0;
+        for (int k = 0; k < 64; ++k) acc += W5[64 * o + k] * H[64 * 5 + k];
+        y[o] = acc;
+    }
+}
+
+/* flags shared in meaning (not in code) with include/nrc.h */
+#define ORC_FACTORIZE 1u
+#define ORC_CLAMP_QUERY 2u
+
+/* Cache query (P:L874-878 reflectance factorisation; clamp reading R2):
+ * q = max(0, y * (alpha + beta)).  W is the set being evaluated (EMA weights
+ * for queries, P:L355 -- the caller chooses). */
+void orc_query_batch(const double* W, const float* recs, int64_t n, const float* lo, const float* hi,
+                     unsigned flags, double* q)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double e[64], H[6 * 64], y[3];
+        const float* rec = recs + 16 * i;
+        orc_encode(rec, lo, hi, e);
+        orc_forward(W, e, H, y);
+        for (int c = 0; c < 3; ++c) {
+            double v = y[c];
+            if (flags & ORC_FACTORIZE) v *= (double)rec[10 + c] + (double)rec[13 + c];
+            if ((flags & ORC_CLAMP_QUERY) && v < 0.0) v = 0.0;
+            q[3 * i + c] = v;
+        }
+    }
+}
+
+/* ---- relative L2 loss, Eq.(5) ---------------------------------
+ * l = (1/3) sum_c (yhat_c - t_c)^2 / (sg(lambda)^2 + eps), where lambda is the
+ * Rec.709 luminance of the prediction (readings R8, R9, R10).
+ * dl/dyhat_c = 2 (yhat_c - t_c) / (3 (lambda^2 + eps)), lambda held constant
+ * (stop-gradient sg).  Returns l; writes dl/dyhat if dyhat != NULL. */
+double orc_loss(const double* yhat, const double* t, double eps, double* dyhat)
+{
+    double lam = 0.2126 * yhat[0] + 0.7152 * yhat[1] + 0.0722 * yhat[2];
+    double den = lam * lam + eps;
+    double l = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        double r = yhat[c] - t[c];
+        l += r * r / den;
+        if (dyhat) dyhat[c] = 2.0 * r / (3.0 * den);
+    }
+    return l / 3.0;
+}
+
+/* Same loss with an externally frozen denominator luminance (used by the
+ * finite-difference pin, which needs sg(.) held at the base point). */
+double orc_loss_frozen(const double* yhat, const double* t, double eps, double lam)
+{
+    double den = lam * lam + eps;
+    double l = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        double r = yhat[c] - t[c];
+        l += r * r / den;
+    }
+    return l / 3.0;
+}
+
+/* ---- backward pass: reverse-mode through the 6 layers --------
+ * dy = dl/dy (3).  G += outer products:  G5 += dy h5^T;  delta5 = W5^T dy;
+ * for i = 4..0: g = delta_{i+1} * 1[h_{i+1} > 0] (ReLU'(0) = 0, reading R17);
+ * G_i += g h_i^T;  delta_i = W_i^T g. */
+void orc_backward(const double* W, const double* H, const double* dy, double* G)
+{
+    double delta[64], g[64];
+    const double* W5 = W + orc_mat_off[5];
+    double* G5 = G + orc_mat_off[5];
+    for (int o = 0; o < 3; ++o)
+        for (int k = 0; k < 64; ++k) G5[64 * o + k] += dy[o] * H[64 * 5 + k];
+    for (int k = 0; k < 64; ++k) {
+        double acc = 0.0;
+        for (int o = 0; o < 3; ++o) acc += W5[64 * o + k] * dy[o];
+        delta[k] = acc;
+    }
+    for (int i = 4; i >= 0; --i) {
+        const double* Wi = W + orc_mat_off[i];
+        double* Gi = G + orc_mat_off[i];
+        const double* hout = H + 64 * (i + 1);
+        const double* hin = H + 64 * i;
+        for (int o = 0; o < 64; ++o) g[o] = hout[o] > 0.0 ? delta[o] : 0.0;
+        for (int o = 0; o < 64; ++o)
+            for (int k = 0; k < 64; ++k) Gi[64 * o + k] += g[o] * hin[k];
+        if (i > 0) {
+            for (int k = 0; k < 64; ++k) {
+                double acc = 0.0;
+                for (int o = 0; o < 64; ++o) acc += Wi[64 * o + k] * g[o];
+                delta[k] = acc;
+            }
+        }
+    }
+}
+
+/* Per-record loss and gradient over a batch: writes the UN-normalised sums
+ * G = sum_records dl/dW (the 1/N of the batch mean is applied by the caller;
+ * reading R13) and loss_sum = sum_records l.  The loss sees the factored,
+ * unclamped prediction yhat = y * (alpha + beta) (readings R2, R9).  Records
+ * with a non-finite target are masked (no loss, no gradient) and counted
+ * (S:L262).  Deterministic for any thread count: the batch is cut into a
+ * fixed number of contiguous chunks, each summed in index order, and the
+ * chunk sums are added in chunk order. */
+#define ORC_CHUNKS 64
+void orc_grad_batch(const double* W, const float* recs, const float* tgts, int64_t n, const float* lo,
+                    const float* hi, double eps, unsigned flags, double* G, double* loss_sum,
+                    int64_t* n_bad_targets)
+{
+    double* Gc = (double*)calloc((size_t)ORC_CHUNKS * ORC_NPARAM, sizeof(double));
+    double lc[ORC_CHUNKS];
+    int64_t bc[ORC_CHUNKS];
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int ch = 0; ch < ORC_CHUNKS; ++ch) {
+        int64_t i0 = n * ch / ORC_CHUNKS, i1 = n * (ch + 1) / ORC_CHUNKS;
+        double* Gk = Gc + (size_t)ch * ORC_NPARAM;
+        double lsum = 0.0;
+        int64_t nbad = 0;
+        for (int64_t i = i0; i < i1; ++i) {
+            const float* rec = recs + 16 * i;
+            const float* tg = tgts + 3 * i;
+            if (!(isfinite(tg[0]) && isfinite(tg[1]) && isfinite(tg[2]))) {
+                ++nbad;
+                continue;
+            }
+            double e[64], H[6 * 64], y[3], yhat[3], t[3], dyhat[3], dy[3];
+            orc_encode(rec, lo, hi, e);
+            orc_forward(W, e, H, y);
+            for (int c = 0; c < 3; ++c) {
+                double f = (flags & ORC_FACTORIZE) ? (double)rec[10 + c] + (double)rec[13 + c] : 1.0;
+                yhat[c] = y[c] * f;
+                t[c] = tg[c];
+            }
+            lsum += orc_loss(yhat, t, eps, dyhat);
+            for (int c = 0; c < 3; ++c) {
+                double f = (flags & ORC_FACTORIZE) ? (double)rec[10 + c] + (double)rec[13 + c] : 1.0;
+                dy[c] = dyhat[c] * f; /* chain rule through yhat = y * (alpha+beta) */
+            }
+            orc_backward(W, H, dy, Gk);
+        }
+        lc[ch] = lsum;
+        bc[ch] = nbad;
+    }
+    memset(G, 0, sizeof(double) * ORC_NPARAM);
+    double lsum = 0.0;
+    int64_t nbad = 0;
+    for (int ch = 0; ch < ORC_CHUNKS; ++ch) {
+        const double* Gk = Gc + (size_t)ch * ORC_NPARAM;
+        for (int64_t j = 0; j < ORC_NPARAM; ++j) G[j] += Gk[j];
+        lsum += lc[ch];
+        nbad += bc[ch];
+    }
+    free(Gc);
+    if (loss_sum) *loss_sum = lsum;
+    if (n_bad_targets) *n_bad_targets = nbad;
+}
+
+/* ---- Adam (reading R11: lr, beta1, beta2, eps outside sqrt,
+ * standard bias correction, t starting at 1).  Non-finite gradient entries
+ * are zeroed and counted. Returns the count. */
+int64_t orc_adam(double* w, double* m, double* v, const double* g_in, int64_t P, int64_t t, double lr,
+                 double b1, double b2, double eps)
+{
+    int64_t bad = 0;
+    double bc1 = 1.0 - pow(b1, (double)t);
+    double bc2 = 1.0 - pow(b2, (double)t);
+    for (int64_t j = 0; j < P; ++j) {
+        double g = g_in[j];
+        if (!isfinite(g)) {
+            g = 0.0;
+            ++bad;
+        }
+        m[j] = b1 * m[j] + (1.0 - b1) * g;
+        v[j] = b2 * v[j] + (1.0 - b2) * g * g;
+        double mhat = m[j] / bc1;
+        double vhat = v[j] / bc2;
+        w[j] -= lr * mhat / (sqrt(vhat) + eps);
+    }
+    return bad;
+}
+
+/* ---- EMA of the weights, Eq.(2) --------------------------------
+ * eta_t = 1 - a^t.  Reading R12 (constant-preserving form):
+ *   Wbar_t = [(1-a) W_t + a eta_{t-1} Wbar_{t-1}] / eta_t.
+ * printed_form != 0 evaluates Eq.(2) exactly as printed:
+ *   Wbar_t = (1-a)/eta_t W_t + a eta_{t-1} Wbar_{t-1}. */
+void orc_ema(double* wbar, const double* w, int64_t P, int64_t t, double a, int printed_form)
+{
+    double eta_t = 1.0 - pow(a, (double)t);
+    double eta_p = 1.0 - pow(a, (double)(t - 1));
+    for (int64_t j = 0; j < P; ++j) {
+        if (printed_form)
+            wbar[j] = (1.0 - a) / eta_t * w[j] + a * eta_p * wbar[j];
+        else
+            wbar[j] = ((1.0 - a) * w[j] + a * eta_p * wbar[j]) / eta_t;
+    }
+}
+
+/* ---- LCG shuffle into s batches of l records ------------------
+ * Reading R15.  splitmix64 stream of the shuffle seed gives (a, c);
+ * m = 2^ceil(log2 n); f(i) = (a i + c) mod m; perm(i) = f iterated until < n. */
+static uint64_t orc_splitmix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+void orc_lcg_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* c, uint64_t* m)
+{
+    uint64_t mm = 1;
+    while (mm < n) mm <<= 1;
+    uint64_t x0 = orc_splitmix64(seed);
+    uint64_t x1 = orc_splitmix64(seed + 0x9E3779B97F4A7C15ull);
+    uint64_t aa = ((x0 & (mm - 1)) & ~(uint64_t)3) | 1;
+    if (mm >= 8 && aa == 1) aa = 5;
+    *a = aa;
+    *c = (x1 & (mm - 1)) | 1;
+    *m = mm;
+}
+
+uint64_t orc_lcg_perm(uint64_t i, uint64_t n, uint64_t a, uint64_t c, uint64_t m)
+{
+    uint64_t x = i;
+    do {
+        x = (a * x + c) & (m - 1);
+    } while (x >= n);
+    return x;
+}
+
+void orc_lcg_permute(uint64_t n, uint64_t a, uint64_t c, uint64_t m, uint64_t* out)
+{
+    for (uint64_t i = 0; i < n; ++i) out[i] = orc_lcg_perm(i, n, a, c, m);
+}
+
+/* ---- initialisation (reading R16): Glorot-uniform from a
+ * counter-based splitmix64 stream: u = (splitmix64(seed ^ (i<<32 | r*in+c))
+ * >> 11) * 2^-53;  w = fp32((2u - 1) sqrt(6 / (fan_in + fan_out))). */
+void orc_init_weights(uint64_t seed, float* W32)
+{
+    for (int i = 0; i < ORC_NMAT; ++i) {
+        int rows = orc_mat_rows[i];
+        double bound = sqrt(6.0 / (64.0 + (double)rows));
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < 64; ++c) {
+                uint64_t ctr = ((uint64_t)i << 32) | (uint64_t)(r * 64 + c);
+                double u = (double)(orc_splitmix64(seed ^ ctr) >> 11) * (1.0 / 9007199254740992.0);
+                W32[orc_mat_off[i] + 64 * r + c] = (float)((2.0 * u - 1.0) * bound);
+            }
+    }
+}
+
+/* ---- one optimisation step: gradient of the batch mean
+ * loss, Adam, EMA.  w, m, v, wbar are fp64 arrays of ORC_NPARAM.  Returns the
+ * batch-mean loss. */
+double orc_train_step(double* w, double* m, double* v, double* wbar, int64_t t, const float* recs,
+                      const float* tgts, int64_t n, const float* lo, const float* hi, double loss_eps,
+                      unsigned flags, double lr, double b1, double b2, double adam_eps, double ema_a,
+                      int ema_printed, double* G_out, int64_t* bad_grads, int64_t* bad_targets)
+{
+    double G[ORC_NPARAM];
+    double lsum = 0.0;
+    if (n <= 0) return 0.0; /* empty batch: no-op */
+    orc_grad_batch(w, recs, tgts, n, lo, hi, loss_eps, flags, G, &lsum, bad_targets);
+    for (int64_t j = 0; j < ORC_NPARAM; ++j) G[j] /= (double)n; /* batch mean (R10, R13) */
+    if (G_out) memcpy(G_out, G, sizeof(G));
+    int64_t bad = orc_adam(w, m, v, G, ORC_NPARAM, t, lr, b1, b2, adam_eps);
+    if (bad_grads) *bad_grads = bad;
+    orc_ema(wbar, w, ORC_NPARAM, t, ema_a, ema_printed);
+    return lsum / (double)n;
+}
