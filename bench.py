@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""bench.py -- NRC frame benchmark (BASELINE.json metric).
+
+One step = one 1080p frame of the paper's hot path (tab:timings
+P:L1241-1309): a cache query of 2,073,600 records (one per pixel)
+with the EMA weights, plus the frame's training -- 65,536 records LCG-
+shuffled into s = 4 batches of l = 16,384, each a fused
+forward / relative-L2 / backward step followed by Adam + EMA.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nrc|reference]
+
+N > 1 (launched with torch.distributed.run, one rank per GPU, NCCL): the same
+1080p frame is split across ranks -- query rows sharded with no
+communication, training data-parallel (each rank takes l/N rows of every
+batch, one NCCL all-reduce of the 20,672-float gradient per step, identical
+Adam on every rank) -- strong scaling, max-over-ranks device time.
+
+--impl reference: the fp64 CPU oracle (oracle/, as it stands) on the host
+cores, timed on a bounded sample of the same frame and scaled to the frame.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+N_QUERY = 1920 * 1080
+TRAIN_S, TRAIN_L = 4, 16384
+N_TRAIN = TRAIN_S * TRAIN_L
+FLOP_QUERY = 2 * (64 * 64 + 4 * 64 * 64 + 64 * 3)            # 41,344
+FLOP_TRAIN = FLOP_QUERY + 2 * (4 * 4096 + 192) + FLOP_QUERY  # 115,840
+BYTES_QUERY = 64 + 12                                        # record in + RGB out
+METRIC = "NRC frame ms (1080p: 2.07M queries + 4×16384 train); queries/s, records/s"
+CONFIG_NAME = "1080p frame: 2,073,600 queries + 4x16384 train, width 64, 5 hidden layers"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ============================================================================ reference arm (oracle)
+def oracle_frame_estimate(q_sample: int, t_sample: int, reps: int = 1):
+    """Times the fp64 oracle on q_sample queries and one train step of
+    t_sample records; scales to one 1080p frame.  Returns (ms_frame, detail)."""
+    import nrc_inputs
+    import oracle
+    oracle.build()
+    recs_q = nrc_inputs.records(q_sample, seed=nrc_inputs.SEED_QUERY)
+    recs_t, tg = nrc_inputs.train_frame(0, n=t_sample)
+    oc = oracle.OracleCache()
+    tq = tt = 0.0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oc.query(recs_q)
+        t1 = time.perf_counter()
+        oc.train_step(recs_t, tg)
+        t2 = time.perf_counter()
+        tq += t1 - t0
+        tt += t2 - t1
+    tq /= reps
+    tt /= reps
+    ms = 1e3 * (tq / q_sample * N_QUERY + tt / t_sample * N_TRAIN)
+    sample = (f"{q_sample} queries + one {t_sample}-record train step per rep, scaled to 2,073,600 queries + "
+              f"65,536 train records")
+    return ms, sample, tq, tt
+
+
+def omp_threads():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    q_sample, t_sample = 32768, 4096
+    oracle_frame_estimate(1024, 256)  # warm-up (build, page-in)
+    times = []
+    for _ in range(args.warmup):
+        oracle_frame_estimate(q_sample, t_sample)
+    for _ in range(args.steps):
+        ms, sample, _, _ = oracle_frame_estimate(q_sample, t_sample)
+        times.append(ms)
+    ms = float(np.mean(times))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (nrc_inputs seeded records)",
+        "config": {"workload": CONFIG_NAME + " (oracle, sampled)"},
+        "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": omp_threads(), "kind": "oracle", "sample": sample},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ============================================================================ CUDA arm
+def run_nrc(args):
+    import torch
+    import torch.distributed as dist
+
+    import nrc_inputs
+    import paper_2106_12372_b200 as nrc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- inputs (synthetic, resident in HBM before timing)
+    q0 = rank * N_QUERY // world
+    q1 = (rank + 1) * N_QUERY // world
+    recs_q_all = nrc_inputs.records(N_QUERY, seed=nrc_inputs.SEED_QUERY)
+    recs_q = torch.from_numpy(recs_q_all[q0:q1].copy()).to(dev)
+    nq_local = q1 - q0
+    frames = []
+    for f in range(2):
+        r, t = nrc_inputs.train_frame(f, n=N_TRAIN, noise=0.3)
+        frames.append((torch.from_numpy(r).to(dev), torch.from_numpy(t).to(dev), r, t))
+    rgb = torch.empty((nq_local, 3), dtype=torch.float32, device=dev)
+    cache = nrc.RadianceCache(nrc.Config(max_batch=max(N_QUERY, N_TRAIN)), device=local)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    # data-parallel pieces for world > 1
+    grad = torch.zeros(nrc.NPARAM, dtype=torch.float32, device=dev)
+    loss_sum = torch.zeros(1, dtype=torch.float32, device=dev)
+    row_lo, row_hi = rank * TRAIN_L // world, (rank + 1) * TRAIN_L // world
+
+    q_start = torch.cuda.Event(enable_timing=True)
+    q_end = torch.cuda.Event(enable_timing=True)
+
+    def frame(fi, timed_query=False):
+        """One 1080p frame: query (EMA weights of the previous frame) + training."""
+        d_r, d_t, _, _ = frames[fi % 2]
+        launches = 0
+        if timed_query:
+            q_start.record(stream)
+        cache.query(recs_q, rgb)
+        if timed_query:
+            q_end.record(stream)
+        launches += cache.last_launch_count
+        if world == 1:
+            cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
+            launches += cache.last_launch_count
+        else:
+            for j in range(TRAIN_S):
+                # this rank's rows of shuffled batch j, gathered in-kernel
+                cache.train_frame_backward(d_r, d_t, TRAIN_L, 1000 + fi % 2, j, row_lo, row_hi, grad, loss_sum)
+                launches += cache.last_launch_count
+                dist.all_reduce(grad)
+                cache.train_apply(grad, TRAIN_L)
+                launches += cache.last_launch_count
+        return launches
+
+    for i in range(args.warmup):
+        frame(i)
+    torch.cuda.synchronize()
+    barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    qt = []
+    launches = 0
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the timed events)
+            ev[i][0].record(stream)
+            launches += frame(i, timed_query=True)
+            ev[i][1].record(stream)
+            torch.cuda.synchronize()
+            qt.append(q_start.elapsed_time(q_end))
+        torch.cuda.synchronize()
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    ms = float(np.mean(step_ms))
+    q_ms = float(np.mean(qt))
+    if world > 1:
+        t = torch.tensor([ms, q_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, q_ms = float(t[0]), float(t[1])
+
+    # ---- end to end through the C ABI with host buffers (N = 1 path; for N > 1 rank-local)
+    e2e = None
+    if world == 1:
+        hq = torch.from_numpy(recs_q_all).pin_memory()
+        ht = torch.from_numpy(frames[0][2]).pin_memory()
+        htg = torch.from_numpy(frames[0][3]).pin_memory()
+        hrgb = torch.empty((N_QUERY, 3), dtype=torch.float32).pin_memory()
+        hloss = torch.empty(64, dtype=torch.float32).pin_memory()
+        scratch = torch.empty(cache.frame_scratch_bytes(N_QUERY, N_TRAIN) + 256, dtype=torch.uint8, device=dev)
+        off = (-scratch.data_ptr()) % 256
+        scratch = scratch[off:]
+        hq_np, ht_np, htg_np, hrgb_np, hl_np = hq.numpy(), ht.numpy(), htg.numpy(), hrgb.numpy(), hloss.numpy()
+        for _ in range(2):
+            cache.frame_host(hq_np, hrgb_np, ht_np, htg_np, TRAIN_S, TRAIN_L, 7, hl_np, scratch)
+        torch.cuda.synchronize()
+        e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
+        for i in range(args.steps):
+            e_ev[i][0].record(stream)
+            cache.frame_host(hq_np, hrgb_np, ht_np, htg_np, TRAIN_S, TRAIN_L, 7, hl_np, scratch)
+            e_ev[i][1].record(stream)
+            torch.cuda.synchronize()
+        e_ms = float(np.mean([s.elapsed_time(e) for s, e in e_ev]))
+        e2e = {"value": e_ms, "unit": "ms", "h2d_bytes_per_step": N_QUERY * 64 + N_TRAIN * (64 + 12),
+               "d2h_bytes_per_step": N_QUERY * 12 + TRAIN_S * 4,
+               "note": "nrc_frame_host: pinned host records -> device, query + 4 train steps, RGB + losses -> host"}
+
+    peak_tf, peak_bw, peak_src = peaks()
+    q_flops = FLOP_QUERY * nq_local
+    achieved = q_flops / (q_ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 Adam/EMA)", "data": "synthetic (nrc_inputs)",
+        "config": {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
+        "query_ms": q_ms, "train_ms": ms - q_ms,
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "kernel": "nrc_query_kernel", "achieved": achieved, "peak": peak_tf,
+                     "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": None,
+                     "peak_source": f"{peak_src} bf16 dense burst (fp16 same rate)",
+                     "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_local} queries"},
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_cpu_baseline:
+        cms, sample, _, _ = oracle_frame_estimate(16384, 2048)
+        line["cpu_baseline"] = {"value": cms, "unit": "ms", "cores": omp_threads(), "kind": "oracle",
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["nrc", "reference"], default="nrc")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_nrc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

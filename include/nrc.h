@@ -1,0 +1,224 @@
+/*
+ * nrc.h -- C ABI of libnrc, a B200-native (sm_100a) implementation of the
+ * data-parallel hot path of Neural Radiance Caching (Mueller, Rousselle,
+ * Novak, Keller, "Real-time Neural Radiance Caching for Path Tracing",
+ * SIGGRAPH 2021, arXiv 2106.12372).
+ *
+ * Citations: "P:L<n>" = line n of the paper source; "S:L<n>" =
+ * line n of SPEC.md; "R<k>" = reading k in DESIGN.md section 3.
+ *
+ * The calls follow the paper's statement of the problem: a radiance cache
+ * that maps cache-query records (Table 1) to scattered radiance
+ * (Eq. 1) through a fully fused 64-wide MLP (P:L602-628,
+ * P:L692-698), trained online every frame from (record, target) pairs with
+ * the relative L2 loss (Eq. 5) and Adam, with
+ * EMA-averaged weights for queries (Eq. 2), on s batches of l
+ * LCG-shuffled records.
+ *
+ * Conventions
+ *  - All functions have C linkage, never throw and never exit.  They return
+ *    nrc_status; on failure nrc_last_error(handle) holds a message.
+ *  - Pointers named d_* are CUDA device pointers (e.g. torch tensors'
+ *    data_ptr()); h_* are host pointers.  The caller owns every buffer,
+ *    including the state arena passed to nrc_init.  The library never calls
+ *    cudaMalloc/cudaFree.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Device-side calls are stream-ordered and asynchronous: results
+ *    are valid once the stream has been synchronised.  nrc_get_params,
+ *    nrc_set_params and nrc_get_stats are synchronous (device-wide sync).
+ *  - Validation failures (NULL or misaligned pointers, n > max_batch, bad
+ *    config) return NRC_ERR_INVALID_ARGUMENT / NRC_ERR_UNSUPPORTED and
+ *    enqueue nothing.  n == 0 is a valid no-op.
+ *  - Data-dependent problems never fail a call: non-finite gradient entries
+ *    are zeroed and counted; records with a non-finite target are
+ *    masked out of loss and gradient and counted.
+ *  - A handle is not thread-safe.  Train calls on one handle must not
+ *    overlap each other; queries may run concurrently with training only on
+ *    another stream and only if the caller orders them against the EMA
+ *    update (they read the fp16 EMA image that train steps rewrite).
+ */
+#ifndef NRC_H_
+#define NRC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NRC_ABI_VERSION 1u
+
+/* One cache query (Table 1): 16 fp32 = 64 bytes.
+ * Arrays of records must be 16-byte aligned.  dir and normal need not be
+ * unit length (they are renormalised; a zero vector reads as (0,0,1)). */
+typedef struct nrc_record {
+    float pos[3];      /* x in world space; normalised by the config AABB (R3) */
+    float dir[3];      /* scattered direction omega                              */
+    float normal[3];   /* surface normal n(x)                                    */
+    float roughness;   /* r(x, omega) >= 0 (negative values read as 0)           */
+    float diffuse[3];  /* diffuse reflectance alpha                              */
+    float specular[3]; /* specular reflectance beta                              */
+} nrc_record;
+
+typedef enum nrc_status {
+    NRC_OK = 0,
+    NRC_ERR_INVALID_ARGUMENT = 1,
+    NRC_ERR_UNSUPPORTED = 2,
+    NRC_ERR_OUT_OF_MEMORY = 3, /* state arena too small */
+    NRC_ERR_CUDA = 4,          /* a CUDA call failed; see nrc_last_error */
+    NRC_ERR_NCCL = 5,          /* reserved for the fused collective path */
+    NRC_ERR_STATE = 6          /* handle not initialised / wrong device  */
+} nrc_status;
+
+/* Parameter sets readable/writable through nrc_get_params/nrc_set_params. */
+typedef enum nrc_param_set {
+    NRC_PARAMS_TRAIN = 0, /* fp32 master weights W_t             */
+    NRC_PARAMS_EMA = 1,   /* EMA weights W-bar_t used by queries */
+    NRC_ADAM_M = 2,       /* Adam first moment                            */
+    NRC_ADAM_V = 3        /* Adam second moment                           */
+} nrc_param_set;
+
+/* nrc_config.flags */
+enum {
+    NRC_FACTORIZE = 1u,         /* multiply the output by alpha+beta       */
+    NRC_CLAMP_QUERY = 2u,       /* clamp query radiance at 0 (R2)                        */
+    NRC_EMA_PRINTED_FORM = 4u,  /* Eq.(2) exactly as printed instead of R12's form      */
+    NRC_QUERY_RAW_WEIGHTS = 8u  /* queries read W_t instead of W-bar_t                  */
+};
+
+typedef struct nrc_config {
+    uint32_t abi_version;      /* must equal NRC_ABI_VERSION                          */
+    uint32_t hidden_width;     /* 64 ("five hidden layers have 64 neurons")   */
+    uint32_t n_hidden_layers;  /* 5; fixed in ABI v1                         */
+    uint32_t max_batch;        /* largest n accepted by query/train calls             */
+    float aabb_min[3];         /* position normalisation domain (R3)           */
+    float aabb_max[3];
+    float learning_rate;       /* 1e-2 (R11; paper: "high learning-rate")     */
+    float adam_beta1;          /* 0.9  (R11)                                          */
+    float adam_beta2;          /* 0.99 (R11)                                          */
+    float adam_eps;            /* 1e-8 (R11), added outside the square root           */
+    float loss_eps;            /* 0.01 (Eq. 5)                                */
+    float ema_alpha;           /* 0.99; 0 => W-bar == W                      */
+    uint32_t flags;            /* default NRC_FACTORIZE | NRC_CLAMP_QUERY             */
+    uint64_t seed;             /* Glorot-uniform init stream (R16)                    */
+    int32_t device;            /* CUDA device ordinal the state lives on              */
+} nrc_config;
+
+typedef struct nrc_handle nrc_handle;
+
+/* Fills *cfg with the paper's defaults (width 64, 5 hidden layers, unit-cube
+ * AABB, lr 1e-2, betas 0.9/0.99, eps 1e-8, loss eps 0.01, EMA 0.99, seed 1,
+ * max_batch 8,294,400 = one 4K frame, device 0). */
+void nrc_default_config(nrc_config* cfg);
+
+/* Bytes of device memory the caller must provide to nrc_init (weights,
+ * Adam state, EMA, fp16 weight images, gradient partials, counters).
+ * Returns 0 for an invalid config. */
+size_t nrc_state_bytes(const nrc_config* cfg);
+
+/* Validates cfg, carves the state out of d_state (device memory of at least
+ * nrc_state_bytes(cfg) bytes, 256-byte aligned, owned by the caller and kept
+ * alive until nrc_destroy), writes the seeded Glorot-uniform weights (R16),
+ * W-bar = W, m = v = 0, step = 0.  Synchronous.  *out receives a host-side
+ * handle (freed by nrc_destroy). */
+nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nrc_handle** out);
+
+nrc_status nrc_destroy(nrc_handle* h);
+
+/* Cache query: d_rgb[3i+c] = max(0, y_c(e(rec_i)) *
+ * (alpha_c + beta_c)) with the EMA weights, for i < n.  d_rec: n
+ * records (16-byte aligned); d_rgb: 3n fp32 (4-byte aligned).  One fused
+ * kernel: encode -> 6 tcgen05 layers -> factorisation epilogue. */
+nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* d_rgb, void* stream);
+
+/* One optimisation step on a batch: forward, relative
+ * L2 loss (Eq. 5) of the factored prediction, backward, Adam on the batch-
+ * mean gradient, EMA update.  d_rec: n records; d_tgt: 3n fp32 targets;
+ * d_loss (optional, 1 fp32): the batch-mean loss.  n <= max_batch. */
+nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n, float* d_loss,
+                          void* stream);
+
+/* Multi-GPU split of nrc_train_step.  nrc_train_backward writes the UN-
+ * normalised gradient sum over the n_local records into d_grad
+ * (nrc_param_count() fp32, logical layout: W0..W4 64x64 then W5 3x64, row-
+ * major [out][in]) and, if d_loss_sum != NULL, the loss sum (1 fp32).  The
+ * caller all-reduces (SUM) d_grad across ranks, then nrc_train_apply runs
+ * Adam + EMA with g = d_grad_sum / n_global.  Deterministic: equal inputs
+ * give bitwise-equal replicas on every rank. */
+nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_local,
+                              float* d_grad, float* d_loss_sum, void* stream);
+nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, void* stream);
+
+/* A frame's training: records are shuffled by the LCG
+ * permutation of nrc_lcg_params(n_total, shuffle_seed) (R15) and split into
+ * s disjoint batches of l records (P:L350 footnote); batch j is records
+ * perm(j*l + k), k < l, gathered inside the kernel (nothing materialised).
+ * If s*l > n_total, l shrinks to n_total / s.  d_losses: s fp32
+ * (optional).  Equivalent to s nrc_train_step calls on the gathered batches. */
+nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s,
+                           uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream);
+
+/* Data-parallel shard of batch j of a frame (multi-GPU nrc_train_frame): the
+ * un-normalised gradient sum and loss sum over records perm(j*l + k) for
+ * row_begin <= k < row_end, with perm the LCG permutation of
+ * nrc_lcg_params(n_total, shuffle_seed), gathered in-kernel.  Rank r of P
+ * takes k in [r*l/P, (r+1)*l/P); all-reduce d_grad, then nrc_train_apply
+ * with n_global = l.  d_grad / d_loss_sum as in nrc_train_backward. */
+nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
+                                    uint32_t l, uint64_t shuffle_seed, uint32_t j, uint32_t row_begin,
+                                    uint32_t row_end, float* d_grad, float* d_loss_sum, void* stream);
+
+/* Host helper: the LCG constants of reading R15 (m = 2^ceil(log2 n), a = 1
+ * mod 4, c odd, from the splitmix64 stream of seed). */
+nrc_status nrc_lcg_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* c, uint64_t* m);
+
+/* The input encoding alone (Table 1 + padding):
+ * d_out[64 i + j] = fp16 bits of feature j of record i (row-major, logical
+ * order).  Same device function the fused kernels use. */
+nrc_status nrc_encode(nrc_handle* h, const nrc_record* d_rec, uint64_t n, uint16_t* d_out, void* stream);
+
+/* Parameter I/O in the logical layout (nrc_param_count() fp32 host floats).
+ * nrc_set_params(NRC_PARAMS_TRAIN) also refreshes the fp16 image of W;
+ * nrc_set_params(NRC_PARAMS_EMA) refreshes the fp16 image of W-bar.
+ * Synchronous. */
+nrc_status nrc_get_params(nrc_handle* h, nrc_param_set which, float* h_out, size_t n);
+nrc_status nrc_set_params(nrc_handle* h, nrc_param_set which, const float* h_in, size_t n);
+
+/* Adam step count t and the non-finite counters.  Synchronous. */
+nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets);
+
+/* 20,672 at width 64 (5*64*64 + 3*64; reading R1). */
+size_t nrc_param_count(const nrc_handle* h);
+
+const char* nrc_status_string(nrc_status s);
+const char* nrc_last_error(const nrc_handle* h);
+
+/* End-to-end frame with HOST buffers (for pinned host memory): copies the
+ * query records and the training records/targets into d_scratch (at least
+ * nrc_frame_scratch_bytes(n_query, n_train) bytes of device memory), runs
+ * nrc_query (EMA weights from before this frame's training) and
+ * nrc_train_frame, and copies the radiance (3 n_query fp32) and the s losses
+ * back.  Asynchronous on `stream`; the caller synchronises. */
+size_t nrc_frame_scratch_bytes(uint64_t n_query, uint32_t n_train);
+nrc_status nrc_frame_host(nrc_handle* h, const nrc_record* h_query, uint64_t n_query, float* h_rgb,
+                          const nrc_record* h_train, const float* h_tgt, uint32_t n_train, uint32_t s, uint32_t l,
+                          uint64_t shuffle_seed, float* h_losses, void* d_scratch, size_t scratch_bytes,
+                          void* stream);
+
+/* Diagnostic: one tcgen05 tile product in each operand layout the kernels
+ * use, on plain row-major fp16 inputs (mode 0: D[128x64] = A[128x64] B[64x64]^T;
+ * mode 1: D[128x64] = A[128x64] B[64x64]; mode 2: D[64x64] = A[128x64]^T
+ * B[128x64]; mode 3: D[128x16] = A[128x64] B[16x64]^T).  D is fp32
+ * row-major.  Synchronous. */
+nrc_status nrc_selftest_umma(int mode, const uint16_t* d_a, const uint16_t* d_b, float* d_d);
+
+/* Number of kernel launches the most recent call on this handle enqueued
+ * (used by bench.py to report gpu_launches). */
+uint32_t nrc_last_launch_count(const nrc_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NRC_H_ */

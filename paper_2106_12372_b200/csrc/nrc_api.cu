@@ -1,0 +1,643 @@
+// nrc_api.cu -- host side of libnrc: the C ABI declared in include/nrc.h.
+// Argument validation, state-arena layout, launch configuration.  All
+// arithmetic of the method runs in the kernels of nrc_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nrc.h"
+#include "nrc_kernels.cuh"
+
+using namespace nrc;
+
+namespace {
+
+constexpr int kQueryGroups = 4;   // 4-warp groups per query CTA
+constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
+
+struct StateLayout {
+    size_t w, m, v, ema, wimg, eimg, partials, loss_part, counters, total;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+StateLayout layout() {
+    StateLayout L{};
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o = align_up(o + bytes, 256);
+        return at;
+    };
+    const size_t pf = sizeof(float) * kParamPadded;
+    L.w = take(pf);
+    L.m = take(pf);
+    L.v = take(pf);
+    L.ema = take(pf);
+    L.wimg = take(kImgBytes);
+    L.eimg = take(kImgBytes);
+    L.partials = take(pf * kMaxPartials);
+    L.loss_part = take(sizeof(float) * kMaxPartials);
+    L.counters = take(sizeof(unsigned long long) * 4);
+    L.total = o;
+    return L;
+}
+
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+}  // namespace
+
+struct nrc_handle {
+    nrc_config cfg;
+    uint8_t* state;
+    StateLayout L;
+    int num_sms;
+    uint64_t step;
+    EncodeParams ep;
+    std::string err;
+    uint32_t launches;
+    float* d_w() { return reinterpret_cast<float*>(state + L.w); }
+    float* d_m() { return reinterpret_cast<float*>(state + L.m); }
+    float* d_v() { return reinterpret_cast<float*>(state + L.v); }
+    float* d_ema() { return reinterpret_cast<float*>(state + L.ema); }
+    uint8_t* d_wimg() { return state + L.wimg; }
+    uint8_t* d_eimg() { return state + L.eimg; }
+    float* d_partials() { return reinterpret_cast<float*>(state + L.partials); }
+    float* d_loss_part() { return reinterpret_cast<float*>(state + L.loss_part); }
+    unsigned long long* d_counters() { return reinterpret_cast<unsigned long long*>(state + L.counters); }
+};
+
+static nrc_status fail(nrc_handle* h, nrc_status s, const std::string& msg) {
+    if (h) h->err = msg;
+    return s;
+}
+static nrc_status cuda_check(nrc_handle* h, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return NRC_OK;
+    return fail(h, NRC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define NRC_CUDA(h, call)                                          \
+    do {                                                           \
+        nrc_status _s = cuda_check((h), (call), #call);            \
+        if (_s != NRC_OK) return _s;                               \
+    } while (0)
+#define NRC_LAUNCHED(h, what)                                      \
+    do {                                                           \
+        nrc_status _s = cuda_check((h), cudaGetLastError(), what); \
+        if (_s != NRC_OK) return _s;                               \
+        ++(h)->launches;                                           \
+    } while (0)
+
+static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+extern "C" {
+
+void nrc_default_config(nrc_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    c->abi_version = NRC_ABI_VERSION;
+    c->hidden_width = 64;
+    c->n_hidden_layers = 5;
+    c->max_batch = 3840u * 2160u;
+    for (int i = 0; i < 3; ++i) {
+        c->aabb_min[i] = 0.0f;
+        c->aabb_max[i] = 1.0f;
+    }
+    c->learning_rate = 1e-2f;
+    c->adam_beta1 = 0.9f;
+    c->adam_beta2 = 0.99f;
+    c->adam_eps = 1e-8f;
+    c->loss_eps = 0.01f;
+    c->ema_alpha = 0.99f;
+    c->flags = NRC_FACTORIZE | NRC_CLAMP_QUERY;
+    c->seed = 1;
+    c->device = 0;
+}
+
+static nrc_status validate_config(const nrc_config* c, std::string* why) {
+    if (!c) {
+        *why = "config is NULL";
+        return NRC_ERR_INVALID_ARGUMENT;
+    }
+    if (c->abi_version != NRC_ABI_VERSION) {
+        *why = "ABI version mismatch";
+        return NRC_ERR_UNSUPPORTED;
+    }
+    if (c->hidden_width != 64 || c->n_hidden_layers != 5) {
+        *why = "only hidden_width 64 with 5 hidden layers is built (P:L694)";
+        return NRC_ERR_UNSUPPORTED;
+    }
+    if (c->max_batch == 0) {
+        *why = "max_batch must be > 0";
+        return NRC_ERR_INVALID_ARGUMENT;
+    }
+    for (int i = 0; i < 3; ++i) {
+        const float ext = c->aabb_max[i] - c->aabb_min[i];
+        if (!(ext > 0.0f) || !std::isfinite(ext)) {
+            *why = "degenerate AABB";
+            return NRC_ERR_INVALID_ARGUMENT;
+        }
+    }
+    if (!(c->learning_rate > 0.0f) || !(c->adam_beta1 >= 0.0f && c->adam_beta1 < 1.0f) ||
+        !(c->adam_beta2 >= 0.0f && c->adam_beta2 < 1.0f) || !(c->adam_eps >= 0.0f) || !(c->loss_eps > 0.0f) ||
+        !(c->ema_alpha >= 0.0f && c->ema_alpha < 1.0f)) {
+        *why = "optimiser hyper-parameter out of range";
+        return NRC_ERR_INVALID_ARGUMENT;
+    }
+    return NRC_OK;
+}
+
+size_t nrc_state_bytes(const nrc_config* cfg) {
+    std::string why;
+    if (validate_config(cfg, &why) != NRC_OK) return 0;
+    return layout().total;
+}
+
+const char* nrc_status_string(nrc_status s) {
+    switch (s) {
+        case NRC_OK: return "NRC_OK";
+        case NRC_ERR_INVALID_ARGUMENT: return "NRC_ERR_INVALID_ARGUMENT";
+        case NRC_ERR_UNSUPPORTED: return "NRC_ERR_UNSUPPORTED";
+        case NRC_ERR_OUT_OF_MEMORY: return "NRC_ERR_OUT_OF_MEMORY";
+        case NRC_ERR_CUDA: return "NRC_ERR_CUDA";
+        case NRC_ERR_NCCL: return "NRC_ERR_NCCL";
+        case NRC_ERR_STATE: return "NRC_ERR_STATE";
+    }
+    return "NRC_ERR_UNKNOWN";
+}
+
+const char* nrc_last_error(const nrc_handle* h) { return h ? h->err.c_str() : "NULL handle"; }
+uint32_t nrc_last_launch_count(const nrc_handle* h) { return h ? h->launches : 0; }
+size_t nrc_param_count(const nrc_handle*) { return kParamLogical; }
+
+nrc_status nrc_lcg_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* c, uint64_t* m) {
+    if (!a || !c || !m || n == 0) return NRC_ERR_INVALID_ARGUMENT;
+    uint64_t mm = 1;
+    while (mm < n) mm <<= 1;
+    const uint64_t x0 = splitmix64(seed), x1 = splitmix64(seed + 0x9E3779B97F4A7C15ull);
+    uint64_t aa = ((x0 & (mm - 1)) & ~uint64_t(3)) | 1u;
+    if (mm >= 8 && aa == 1) aa = 5;
+    *a = aa;
+    *c = (x1 & (mm - 1)) | 1u;
+    *m = mm;
+    return NRC_OK;
+}
+
+static nrc_status refresh_images(nrc_handle* h, cudaStream_t st) {
+    const int blocks = (kParamPadded + 255) / 256;
+    nrc_image_kernel<<<blocks, 256, 0, st>>>(h->d_w(), h->d_wimg());
+    NRC_LAUNCHED(h, "nrc_image_kernel");
+    nrc_image_kernel<<<blocks, 256, 0, st>>>(h->d_ema(), h->d_eimg());
+    NRC_LAUNCHED(h, "nrc_image_kernel");
+    return NRC_OK;
+}
+
+nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nrc_handle** out) {
+    std::string why;
+    if (!out) return NRC_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    nrc_status s = validate_config(cfg, &why);
+    if (s != NRC_OK) {
+        std::fprintf(stderr, "nrc_init: %s\n", why.c_str());
+        return s;
+    }
+    const StateLayout L = layout();
+    if (!d_state || !aligned(d_state, 256)) return NRC_ERR_INVALID_ARGUMENT;
+    if (state_bytes < L.total) return NRC_ERR_OUT_OF_MEMORY;
+
+    nrc_handle* h = new nrc_handle();
+    h->cfg = *cfg;
+    h->state = static_cast<uint8_t*>(d_state);
+    h->L = L;
+    h->step = 0;
+    h->launches = 0;
+    for (int i = 0; i < 3; ++i) {
+        // reading R3: inv = fp32(1 / fp32(hi - lo))
+        volatile float ext = cfg->aabb_max[i] - cfg->aabb_min[i];
+        volatile float inv = 1.0f / ext;
+        h->ep.lo[i] = cfg->aabb_min[i];
+        h->ep.inv[i] = inv;
+    }
+    auto bail = [&](nrc_status st) {
+        std::fprintf(stderr, "nrc_init: %s\n", h->err.c_str());
+        delete h;
+        return st;
+    };
+    if ((s = cuda_check(h, cudaSetDevice(cfg->device), "cudaSetDevice")) != NRC_OK) return bail(s);
+    if ((s = cuda_check(h, cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, cfg->device),
+                        "cudaDeviceGetAttribute")) != NRC_OK)
+        return bail(s);
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cfg->device);
+    if (major != 10) {
+        h->err = "libnrc is built for sm_100a (B200); device compute capability major = " + std::to_string(major);
+        return bail(NRC_ERR_UNSUPPORTED);
+    }
+    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_query_kernel<kQueryGroups>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                query_smem_bytes<kQueryGroups>()),
+                        "cudaFuncSetAttribute(query)")) != NRC_OK)
+        return bail(s);
+    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kTrainSmemBytes),
+                        "cudaFuncSetAttribute(train)")) != NRC_OK)
+        return bail(s);
+
+    // Glorot-uniform init from the counter-based splitmix64 stream (R16).
+    std::vector<float> w(kParamPadded, 0.0f);
+    const int rows_of[6] = {64, 64, 64, 64, 64, 3};
+    for (int i = 0; i < 6; ++i) {
+        const double bound = std::sqrt(6.0 / (64.0 + double(rows_of[i])));
+        for (int r = 0; r < rows_of[i]; ++r)
+            for (int c = 0; c < 64; ++c) {
+                const uint64_t ctr = (uint64_t(i) << 32) | uint64_t(r * 64 + c);
+                const double u = double(splitmix64(cfg->seed ^ ctr) >> 11) * (1.0 / 9007199254740992.0);
+                w[layer_off(i) + r * 64 + c] = float((2.0 * u - 1.0) * bound);
+            }
+    }
+    const size_t pf = sizeof(float) * kParamPadded;
+    if ((s = cuda_check(h, cudaMemset(h->state, 0, L.total), "cudaMemset(state)")) != NRC_OK) return bail(s);
+    if ((s = cuda_check(h, cudaMemcpy(h->d_w(), w.data(), pf, cudaMemcpyHostToDevice), "cudaMemcpy(w)")) != NRC_OK)
+        return bail(s);
+    if ((s = cuda_check(h, cudaMemcpy(h->d_ema(), w.data(), pf, cudaMemcpyHostToDevice), "cudaMemcpy(ema)")) != NRC_OK)
+        return bail(s);
+    if ((s = refresh_images(h, 0)) != NRC_OK) return bail(s);
+    if ((s = cuda_check(h, cudaDeviceSynchronize(), "nrc_init sync")) != NRC_OK) return bail(s);
+    *out = h;
+    return NRC_OK;
+}
+
+nrc_status nrc_destroy(nrc_handle* h) {
+    delete h;
+    return NRC_OK;
+}
+
+static nrc_status check_handle(nrc_handle* h) {
+    if (!h || !h->state) return NRC_ERR_STATE;
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != h->cfg.device) return cuda_check(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+    return NRC_OK;
+}
+
+nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* d_rgb, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n == 0) return NRC_OK;
+    if (!d_rec || !d_rgb || !aligned(d_rec, 16) || !aligned(d_rgb, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query: NULL or misaligned pointer");
+    if (n > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query: n > max_batch");
+    QueryArgs qa;
+    qa.rec = reinterpret_cast<const float*>(d_rec);
+    qa.out = d_rgb;
+    qa.n = n;
+    const bool raw = (h->cfg.flags & NRC_QUERY_RAW_WEIGHTS) || h->cfg.ema_alpha == 0.0f;
+    qa.wimg = raw ? h->d_wimg() : h->d_eimg();
+    qa.ep = h->ep;
+    qa.flags = h->cfg.flags & (NRC_FACTORIZE | NRC_CLAMP_QUERY);
+    const uint64_t ntiles = (n + kTile - 1) / kTile;
+    const uint64_t ctas_needed = (ntiles + kQueryGroups - 1) / kQueryGroups;
+    const int grid = int(ctas_needed < uint64_t(h->num_sms) ? ctas_needed : uint64_t(h->num_sms));
+    nrc_query_kernel<kQueryGroups><<<grid, 128 * kQueryGroups, query_smem_bytes<kQueryGroups>(),
+                                     static_cast<cudaStream_t>(stream)>>>(qa);
+    NRC_LAUNCHED(h, "nrc_query_kernel");
+    return NRC_OK;
+}
+
+struct Gather {
+    bool on;
+    uint64_t a, c, m, n, offset;
+};
+
+// fused forward/backward over n rows -> per-CTA partials; returns #partials
+static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                               const Gather& gth, cudaStream_t st, int* nparts) {
+    TrainArgs ta;
+    ta.rec = reinterpret_cast<const float*>(d_rec);
+    ta.tgt = d_tgt;
+    ta.n = n;
+    ta.gather = gth.on ? 1u : 0u;
+    ta.lcg_a = gth.a;
+    ta.lcg_c = gth.c;
+    ta.lcg_m = gth.m;
+    ta.lcg_n = gth.n;
+    ta.offset = gth.offset;
+    ta.wimg = h->d_wimg();
+    ta.ep = h->ep;
+    ta.flags = h->cfg.flags & NRC_FACTORIZE;
+    ta.loss_eps = h->cfg.loss_eps;
+    ta.partials = h->d_partials();
+    ta.loss_part = h->d_loss_part();
+    ta.bad_targets = h->d_counters() + 1;
+    const uint32_t ntiles = (n + kTile - 1) / kTile;
+    int grid = int(ntiles);
+    const int cap = h->num_sms < kMaxPartials ? h->num_sms : kMaxPartials;
+    if (grid > cap) grid = cap;
+    nrc_train_kernel<<<grid, 128, kTrainSmemBytes, st>>>(ta);
+    NRC_LAUNCHED(h, "nrc_train_kernel");
+    *nparts = grid;
+    return NRC_OK;
+}
+
+static AdamArgs adam_args(nrc_handle* h) {
+    AdamArgs aa{};
+    const nrc_config& c = h->cfg;
+    const uint64_t t = h->step;  // already incremented
+    aa.w = h->d_w();
+    aa.m = h->d_m();
+    aa.v = h->d_v();
+    aa.ema = h->d_ema();
+    aa.wimg = h->d_wimg();
+    aa.eimg = h->d_eimg();
+    aa.lr = c.learning_rate;
+    aa.b1 = c.adam_beta1;
+    aa.b2 = c.adam_beta2;
+    aa.eps = c.adam_eps;
+    aa.inv_bc1 = float(1.0 / (1.0 - std::pow(double(c.adam_beta1), double(t))));
+    aa.inv_bc2 = float(1.0 / (1.0 - std::pow(double(c.adam_beta2), double(t))));
+    // Eq.(2): eta_t = 1 - a^t.  R12: W-bar = [(1-a) W + a eta_{t-1} W-bar] / eta_t
+    const double al = c.ema_alpha;
+    const double eta_t = 1.0 - std::pow(al, double(t));
+    const double eta_p = 1.0 - std::pow(al, double(t - 1));
+    if (al == 0.0) {
+        aa.ema_c1 = 1.0f;
+        aa.ema_c2 = 0.0f;
+    } else if (c.flags & NRC_EMA_PRINTED_FORM) {
+        aa.ema_c1 = float((1.0 - al) / eta_t);
+        aa.ema_c2 = float(al * eta_p);
+    } else {
+        aa.ema_c1 = float((1.0 - al) / eta_t);
+        aa.ema_c2 = float(al * eta_p / eta_t);
+    }
+    aa.bad_grads = h->d_counters() + 0;
+    return aa;
+}
+
+static nrc_status train_step_impl(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                                  const Gather& gth, float* d_loss, cudaStream_t st) {
+    int np = 0;
+    nrc_status s = launch_train(h, d_rec, d_tgt, n, gth, st, &np);
+    if (s != NRC_OK) return s;
+    h->step += 1;
+    AdamArgs aa = adam_args(h);
+    aa.src = h->d_partials();
+    aa.nsrc = np;
+    aa.src_logical = 0;
+    aa.inv_n = float(1.0 / double(n));
+    aa.loss_part = h->d_loss_part();
+    aa.nloss = np;
+    aa.loss_scale = float(1.0 / double(n));
+    aa.loss_out = d_loss;
+    nrc_adam_kernel<<<(kParamPadded + 255) / 256, 256, 0, st>>>(aa);
+    NRC_LAUNCHED(h, "nrc_adam_kernel");
+    return NRC_OK;
+}
+
+static nrc_status check_train_args(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint64_t n,
+                                   const char* who) {
+    if (!d_rec || !d_tgt || !aligned(d_rec, 16) || !aligned(d_tgt, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, std::string(who) + ": NULL or misaligned pointer");
+    if (n > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, std::string(who) + ": n > max_batch");
+    return NRC_OK;
+}
+
+nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n, float* d_loss,
+                          void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n == 0) return NRC_OK;
+    if ((s = check_train_args(h, d_rec, d_tgt, n, "nrc_train_step")) != NRC_OK) return s;
+    if (d_loss && !aligned(d_loss, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "misaligned d_loss");
+    Gather g{false, 0, 0, 0, 0, 0};
+    return train_step_impl(h, d_rec, d_tgt, n, g, d_loss, static_cast<cudaStream_t>(stream));
+}
+
+nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_local,
+                              float* d_grad, float* d_loss_sum, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (!d_grad || !aligned(d_grad, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_backward: bad d_grad");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n_local == 0) {  // contributes a zero gradient to the all-reduce
+        NRC_CUDA(h, cudaMemsetAsync(d_grad, 0, sizeof(float) * kParamLogical, st));
+        if (d_loss_sum) NRC_CUDA(h, cudaMemsetAsync(d_loss_sum, 0, sizeof(float), st));
+        return NRC_OK;
+    }
+    if ((s = check_train_args(h, d_rec, d_tgt, n_local, "nrc_train_backward")) != NRC_OK) return s;
+    int np = 0;
+    Gather g{false, 0, 0, 0, 0, 0};
+    if ((s = launch_train(h, d_rec, d_tgt, n_local, g, st, &np)) != NRC_OK) return s;
+    nrc_reduce_kernel<<<(kParamPadded + 255) / 256, 256, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
+                                                                  d_loss_sum);
+    NRC_LAUNCHED(h, "nrc_reduce_kernel");
+    return NRC_OK;
+}
+
+nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
+                                    uint32_t l, uint64_t shuffle_seed, uint32_t j, uint32_t row_begin,
+                                    uint32_t row_end, float* d_grad, float* d_loss_sum, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (!d_grad || !aligned(d_grad, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_backward: bad d_grad");
+    if (row_begin > row_end || row_end > l || uint64_t(j + 1) * l > n_total)
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_backward: rows outside batch j");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint32_t n = row_end - row_begin;
+    if (n == 0) {
+        NRC_CUDA(h, cudaMemsetAsync(d_grad, 0, sizeof(float) * kParamLogical, st));
+        if (d_loss_sum) NRC_CUDA(h, cudaMemsetAsync(d_loss_sum, 0, sizeof(float), st));
+        return NRC_OK;
+    }
+    if ((s = check_train_args(h, d_rec, d_tgt, n, "nrc_train_frame_backward")) != NRC_OK) return s;
+    Gather g{true, 0, 0, 0, n_total, uint64_t(j) * l + row_begin};
+    nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
+    int np = 0;
+    if ((s = launch_train(h, d_rec, d_tgt, n, g, st, &np)) != NRC_OK) return s;
+    nrc_reduce_kernel<<<(kParamPadded + 255) / 256, 256, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
+                                                                  d_loss_sum);
+    NRC_LAUNCHED(h, "nrc_reduce_kernel");
+    return NRC_OK;
+}
+
+nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n_global == 0) return NRC_OK;
+    if (!d_grad_sum || !aligned(d_grad_sum, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply: bad grad");
+    h->step += 1;
+    AdamArgs aa = adam_args(h);
+    aa.src = d_grad_sum;
+    aa.nsrc = 1;
+    aa.src_logical = 1;
+    aa.inv_n = float(1.0 / double(n_global));
+    aa.loss_out = nullptr;
+    nrc_adam_kernel<<<(kParamPadded + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(aa);
+    NRC_LAUNCHED(h, "nrc_adam_kernel");
+    return NRC_OK;
+}
+
+nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s_,
+                           uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
+    if (!d_rec || !d_tgt || !aligned(d_rec, 16) || !aligned(d_tgt, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: NULL or misaligned pointer");
+    if (uint64_t(s_) * l > n_total) l = n_total / s_;  // batches shrink proportionally
+    if (l == 0) return NRC_OK;
+    if (l > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: l > max_batch");
+    Gather g{true, 0, 0, 0, n_total, 0};
+    nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t total = 0;
+    for (uint32_t j = 0; j < s_; ++j) {
+        g.offset = uint64_t(j) * l;
+        if ((s = train_step_impl(h, d_rec, d_tgt, l, g, d_losses ? d_losses + j : nullptr, st)) != NRC_OK) return s;
+        total += h->launches;
+        h->launches = 0;
+    }
+    h->launches = total;
+    return NRC_OK;
+}
+
+nrc_status nrc_encode(nrc_handle* h, const nrc_record* d_rec, uint64_t n, uint16_t* d_out, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n == 0) return NRC_OK;
+    if (!d_rec || !d_out || !aligned(d_rec, 16) || !aligned(d_out, 16))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_encode: NULL or misaligned pointer");
+    const unsigned blocks = unsigned((n + 127) / 128);
+    nrc_encode_kernel<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const float*>(d_rec), n,
+                                                                              h->ep, reinterpret_cast<uint4*>(d_out));
+    NRC_LAUNCHED(h, "nrc_encode_kernel");
+    return NRC_OK;
+}
+
+static float* param_ptr(nrc_handle* h, nrc_param_set which) {
+    switch (which) {
+        case NRC_PARAMS_TRAIN: return h->d_w();
+        case NRC_PARAMS_EMA: return h->d_ema();
+        case NRC_ADAM_M: return h->d_m();
+        case NRC_ADAM_V: return h->d_v();
+    }
+    return nullptr;
+}
+
+// logical (20,672) <-> padded (21,504): only W5's rows 3..15 are padding
+static void logical_to_padded(const float* lg, float* pd) {
+    std::memset(pd, 0, sizeof(float) * kParamPadded);
+    std::memcpy(pd, lg, sizeof(float) * 20480);
+    std::memcpy(pd + 20480, lg + 20480, sizeof(float) * 192);
+}
+static void padded_to_logical(const float* pd, float* lg) {
+    std::memcpy(lg, pd, sizeof(float) * 20480);
+    std::memcpy(lg + 20480, pd + 20480, sizeof(float) * 192);
+}
+
+nrc_status nrc_get_params(nrc_handle* h, nrc_param_set which, float* h_out, size_t n) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    float* src = param_ptr(h, which);
+    if (!src || !h_out || n < size_t(kParamLogical)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_get_params");
+    std::vector<float> pd(kParamPadded);
+    NRC_CUDA(h, cudaDeviceSynchronize());
+    NRC_CUDA(h, cudaMemcpy(pd.data(), src, sizeof(float) * kParamPadded, cudaMemcpyDeviceToHost));
+    padded_to_logical(pd.data(), h_out);
+    return NRC_OK;
+}
+
+nrc_status nrc_set_params(nrc_handle* h, nrc_param_set which, const float* h_in, size_t n) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    float* dst = param_ptr(h, which);
+    if (!dst || !h_in || n < size_t(kParamLogical)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_set_params");
+    std::vector<float> pd(kParamPadded);
+    logical_to_padded(h_in, pd.data());
+    NRC_CUDA(h, cudaDeviceSynchronize());
+    NRC_CUDA(h, cudaMemcpy(dst, pd.data(), sizeof(float) * kParamPadded, cudaMemcpyHostToDevice));
+    h->launches = 0;
+    if ((s = refresh_images(h, 0)) != NRC_OK) return s;
+    NRC_CUDA(h, cudaDeviceSynchronize());
+    return NRC_OK;
+}
+
+nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    unsigned long long c[4] = {0, 0, 0, 0};
+    NRC_CUDA(h, cudaDeviceSynchronize());
+    NRC_CUDA(h, cudaMemcpy(c, h->d_counters(), sizeof(c), cudaMemcpyDeviceToHost));
+    if (step) *step = h->step;
+    if (nonfinite_grads) *nonfinite_grads = c[0];
+    if (nonfinite_targets) *nonfinite_targets = c[1];
+    return NRC_OK;
+}
+
+size_t nrc_frame_scratch_bytes(uint64_t n_query, uint32_t n_train) {
+    return align_up(n_query * sizeof(nrc_record), 256) + align_up(n_query * 3 * sizeof(float), 256) +
+           align_up(size_t(n_train) * sizeof(nrc_record), 256) + align_up(size_t(n_train) * 3 * sizeof(float), 256) +
+           256;
+}
+
+nrc_status nrc_frame_host(nrc_handle* h, const nrc_record* h_query, uint64_t n_query, float* h_rgb,
+                          const nrc_record* h_train, const float* h_tgt, uint32_t n_train, uint32_t s_, uint32_t l,
+                          uint64_t shuffle_seed, float* h_losses, void* d_scratch, size_t scratch_bytes,
+                          void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if (!d_scratch || !aligned(d_scratch, 256) || scratch_bytes < nrc_frame_scratch_bytes(n_query, n_train))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_frame_host: scratch too small or misaligned");
+    if ((n_query && (!h_query || !h_rgb)) || (n_train && (!h_train || !h_tgt)))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_frame_host: NULL host buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* p = static_cast<uint8_t*>(d_scratch);
+    nrc_record* dq = reinterpret_cast<nrc_record*>(p);
+    p += align_up(n_query * sizeof(nrc_record), 256);
+    float* drgb = reinterpret_cast<float*>(p);
+    p += align_up(n_query * 3 * sizeof(float), 256);
+    nrc_record* dt = reinterpret_cast<nrc_record*>(p);
+    p += align_up(size_t(n_train) * sizeof(nrc_record), 256);
+    float* dtg = reinterpret_cast<float*>(p);
+    p += align_up(size_t(n_train) * 3 * sizeof(float), 256);
+    float* dloss = reinterpret_cast<float*>(p);  // up to 64 losses
+    if (s_ > 64) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_frame_host: s > 64");
+    uint32_t launches = 0;
+    if (n_query) NRC_CUDA(h, cudaMemcpyAsync(dq, h_query, n_query * sizeof(nrc_record), cudaMemcpyHostToDevice, st));
+    if (n_train) {
+        NRC_CUDA(h, cudaMemcpyAsync(dt, h_train, size_t(n_train) * sizeof(nrc_record), cudaMemcpyHostToDevice, st));
+        NRC_CUDA(h, cudaMemcpyAsync(dtg, h_tgt, size_t(n_train) * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+    }
+    if ((s = nrc_query(h, dq, n_query, drgb, stream)) != NRC_OK) return s;
+    launches += h->launches;
+    if ((s = nrc_train_frame(h, dt, dtg, n_train, s_, l, shuffle_seed, dloss, stream)) != NRC_OK) return s;
+    launches += h->launches;
+    if (n_query) NRC_CUDA(h, cudaMemcpyAsync(h_rgb, drgb, n_query * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (h_losses && s_) NRC_CUDA(h, cudaMemcpyAsync(h_losses, dloss, s_ * sizeof(float), cudaMemcpyDeviceToHost, st));
+    h->launches = launches;
+    return NRC_OK;
+}
+
+nrc_status nrc_selftest_umma(int mode, const uint16_t* d_a, const uint16_t* d_b, float* d_d) {
+    if (mode < 0 || mode > 3 || !d_a || !d_b || !d_d || !aligned(d_a, 16) || !aligned(d_b, 16))
+        return NRC_ERR_INVALID_ARGUMENT;
+    nrc_selftest_kernel<<<1, 128>>>(mode, d_a, d_b, d_d);
+    if (cudaGetLastError() != cudaSuccess) return NRC_ERR_CUDA;
+    if (cudaDeviceSynchronize() != cudaSuccess) return NRC_ERR_CUDA;
+    return NRC_OK;
+}
+
+}  // extern "C"

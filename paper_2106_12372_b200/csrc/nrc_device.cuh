@@ -1,0 +1,286 @@
+// nrc_device.cuh -- sm_100a device primitives for libnrc: PTX wrappers for
+// mbarriers, 1-D TMA bulk copies, tcgen05 (UMMA, TMEM alloc/ld, commit), the
+// 128B-swizzled operand layout, and the input encoding (Table 1).
+//
+// Operand layout: every 64-wide fp16 tile (activations,
+// gradients, weights) is stored as 128-byte lines, line r holding 64 fp16
+// values whose 16-byte chunk c sits at chunk position c ^ (r & 7) -- the
+// SWIZZLE_128B atom (8 lines x 128 B, 1024-B aligned).  The same bytes are a
+// K-major operand when a line is an M/N row and an MN-major operand when a
+// line is a K row, so one stored tile serves forward, dgrad and wgrad.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace nrc {
+
+// ----------------------------------------------------------------- constants
+constexpr int kW = 64;                    // hidden width
+constexpr int kTile = 128;                // rows per tile (one TMEM lane per row)
+constexpr int kNumLayers = 6;             // W0..W5 (reading R1)
+constexpr int kOutPad = 16;               // W5 padded to 16 rows (UMMA N granularity)
+constexpr int kParamLogical = 5 * 64 * 64 + 3 * 64;   // 20,672
+constexpr int kParamPadded = 5 * 64 * 64 + 16 * 64;   // 21,504
+constexpr int kParamPaddedEnd = kParamPadded;
+// start of layer i in the padded parameter layout (i = 6: end)
+__host__ __device__ constexpr int layer_off(int i) { return i < 6 ? i * 4096 : kParamPaddedEnd; }
+constexpr int kImgBytes = kParamPadded * 2;           // 43,008 B fp16 image
+constexpr int kTileBytes = kTile * 128;               // 16 KB per 128x64 fp16 tile
+constexpr int kRecFloats = 16;                        // 64-B record
+
+// ----------------------------------------------------------------- misc PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "NRC_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra NRC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// Generic-proxy smem writes -> visible to the async proxy (tensor core reads).
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ----------------------------------------------------------------- tcgen05
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish() {
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem], kind::f16 (fp16 in, fp32 accumulate).
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Arrive on an mbarrier once all previously issued tcgen05 ops of this thread
+// have completed (implies tcgen05.fence::before_thread_sync).
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B fp16, majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn_major, int b_mn_major) {
+    return (1u << 4) | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) | (uint32_t(N >> 3) << 17) |
+           (uint32_t(M >> 4) << 24);
+}
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version field = 1.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFFu);
+    d |= uint64_t((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+// K-major operand (line = M/N row, 64 K values per line); K step of 16 = +32 B.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t tile_saddr, int kstep) {
+    return make_sdesc(tile_saddr + 32u * kstep, 16u, 1024u);
+}
+// MN-major operand (line = K row, 64 M/N values per line); K step of 16 = +2048 B.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile_saddr, int kstep) {
+    return make_sdesc(tile_saddr + 2048u * kstep, 8192u, 1024u);
+}
+
+// 32 lanes x 32 bit, 32 / 16 / 4 consecutive columns.  The wait takes the
+// registers as in/out operands so no use can be scheduled before it.
+#define NRC_R8(o) "=r"(r[o + 0]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3]), "=r"(r[o + 4]), "=r"(r[o + 5]), \
+                  "=r"(r[o + 6]), "=r"(r[o + 7])
+#define NRC_W8(o) "+r"(r[o + 0]), "+r"(r[o + 1]), "+r"(r[o + 2]), "+r"(r[o + 3]), "+r"(r[o + 4]), "+r"(r[o + 5]), \
+                  "+r"(r[o + 6]), "+r"(r[o + 7])
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : NRC_R8(0), NRC_R8(8), NRC_R8(16), NRC_R8(24)
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : NRC_W8(0), NRC_W8(8), NRC_W8(16), NRC_W8(24)::"memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : NRC_R8(0), NRC_R8(8)
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : NRC_W8(0), NRC_W8(8)::"memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3])::"memory");
+}
+#undef NRC_R8
+#undef NRC_W8
+
+// ----------------------------------------------------------------- fp16 packing
+// (lo, hi) -> f16x2 with round-to-nearest-even (cvt puts its FIRST source in
+// the upper half).
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+    uint32_t d;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    return d;
+}
+// Same with ReLU fused into the conversion (cvt.rn.relu).
+__device__ __forceinline__ uint32_t pack_h2_relu(float lo, float hi) {
+    uint32_t d;
+    asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    return d;
+}
+// Byte offset of 16-B chunk c of line r inside a SWIZZLE_128B tile.
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
+
+__device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t saddr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(saddr)
+                 : "memory");
+    return v;
+}
+
+// ----------------------------------------------------------------- encoding
+// Position normalisation constants: v = fp32(fp32(p - lo) * inv) (reading R3).
+struct EncodeParams {
+    float lo[3];
+    float inv[3];
+};
+
+// tri(x) = 2 |x mod 2 - 1| - 1, floored mod.  x = 2^d v is exact in
+// fp32, so floor(x/2) and x - 2 floor(x/2) are exact.
+__device__ __forceinline__ float tri_f(float x) {
+    float m = x - 2.0f * floorf(x * 0.5f);
+    return 2.0f * fabsf(m - 1.0f) - 1.0f;
+}
+// quartic(x) = 15/16 (1 - x^2)^2 on |x| <= 1, branchless.
+__device__ __forceinline__ float quartic_f(float x) {
+    float t = fmaf(-x, x, 1.0f);
+    float q = 0.9375f * t * t;
+    return fabsf(x) <= 1.0f ? q : 0.0f;
+}
+// One-blob, k = 4, centres (i + 1/2)/4, width 1/4, clamp to [0,1] (R6).
+__device__ __forceinline__ void one_blob4(float s, float* o) {
+    s = fminf(fmaxf(s, 0.0f), 1.0f);
+    float x = 4.0f * s;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = quartic_f(x - (float(i) + 0.5f));
+}
+// sph (Table 1 caption; reading R7): (acos(z)/pi, (atan2(y,x)+pi)/(2 pi))
+__device__ __forceinline__ void sph_f(float x, float y, float z, float& th, float& ph) {
+    float l2 = x * x + y * y + z * z;
+    if (!(l2 > 0.0f)) {
+        x = 0.0f;
+        y = 0.0f;
+        z = 1.0f;
+    } else {
+        float il = 1.0f / sqrtf(l2);
+        x *= il;
+        y *= il;
+        z *= il;
+    }
+    z = fminf(fmaxf(z, -1.0f), 1.0f);
+    th = acosf(z) * 0.318309886183790672f;                      // 1/pi
+    ph = (atan2f(y, x) + 3.14159265358979323846f) * 0.159154943091895336f;  // 1/(2 pi)
+}
+
+// Encodes one record into 64 fp16 features packed as 32 f16x2 words, in the
+// order of reading R5 / Table 1: freq(x) 36 | ob(sph(w)) 8 | ob(sph(n)) 8 |
+// ob(1-e^-r) 4 | alpha 3 | beta 3 | 1, 1.
+__device__ __forceinline__ void encode_record(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
+    float e[64];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float v = __fmul_rn(__fsub_rn(rec[a], ep.lo[a]), ep.inv[a]);
+#pragma unroll
+        for (int d = 0; d < 12; ++d) e[12 * a + d] = tri_f(v * float(1 << d));
+    }
+    float th, ph;
+    sph_f(rec[3], rec[4], rec[5], th, ph);
+    one_blob4(th, e + 36);
+    one_blob4(ph, e + 40);
+    sph_f(rec[6], rec[7], rec[8], th, ph);
+    one_blob4(th, e + 44);
+    one_blob4(ph, e + 48);
+    one_blob4(1.0f - expf(-fmaxf(rec[9], 0.0f)), e + 52);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) e[56 + c] = rec[10 + c];
+    e[62] = 1.0f;
+    e[63] = 1.0f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) h[j] = pack_h2(e[2 * j], e[2 * j + 1]);
+}
+
+// Writes a packed 64-feature row into line `row` of a SWIZZLE_128B tile.
+__device__ __forceinline__ void store_row_swz(uint32_t tile_saddr, uint32_t row, const uint32_t (&h)[32]) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        st_shared_v4(tile_saddr + swz(row, c), h[4 * c + 0], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+}
+
+// Fetch 16 floats of a record (64 B, 16-B aligned) from global memory.
+__device__ __forceinline__ void load_record_global(const float* __restrict__ src, float* rec) {
+    const float4* s = reinterpret_cast<const float4*>(src);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float4 v = __ldg(s + i);
+        rec[4 * i + 0] = v.x;
+        rec[4 * i + 1] = v.y;
+        rec[4 * i + 2] = v.z;
+        rec[4 * i + 3] = v.w;
+    }
+}
+
+// LCG permutation of reading R15: f(i) = (a i + c) mod m, iterated
+// until < n (cycle walking).
+__device__ __forceinline__ uint64_t lcg_perm(uint64_t i, uint64_t n, uint64_t a, uint64_t c, uint64_t m) {
+    uint64_t x = i;
+    do {
+        x = (a * x + c) & (m - 1);
+    } while (x >= n);
+    return x;
+}
+
+}  // namespace nrc

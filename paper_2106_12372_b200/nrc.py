@@ -1,0 +1,272 @@
+"""Thin Python binding over libnrc's C ABI (include/nrc.h).
+
+Argument marshalling only: every step of the hot path (encoding, fused MLP
+query, fused forward/backward/wgrad, Adam, EMA, LCG gather) runs in the CUDA
+kernels behind the C ABI.  PyTorch supplies device memory and streams; there
+is no CPU fallback -- constructing a RadianceCache without a B200 raises.
+
+Paper: Mueller et al., "Real-time Neural Radiance Caching for Path Tracing"
+(arXiv 2106.12372).  API names follow the paper's problem statement: a cache
+queried with records (Table 1) and trained online from
+(record, target) pairs.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+NPARAM = 5 * 64 * 64 + 3 * 64  # 20,672 (reading R1)
+REC_FLOATS = 16
+
+FACTORIZE = 1
+CLAMP_QUERY = 2
+EMA_PRINTED_FORM = 4
+QUERY_RAW_WEIGHTS = 8
+
+PARAMS_TRAIN, PARAMS_EMA, ADAM_M, ADAM_V = 0, 1, 2, 3
+_PARAM_SETS = {"train": PARAMS_TRAIN, "ema": PARAMS_EMA, "adam_m": ADAM_M, "adam_v": ADAM_V}
+
+
+class NRCError(RuntimeError):
+    pass
+
+
+@dataclass
+class Config:
+    """Mirror of nrc_config; defaults are the paper's constants (see nrc.h)."""
+    hidden_width: int = 64
+    n_hidden_layers: int = 5
+    max_batch: int = 3840 * 2160
+    aabb_min: Sequence[float] = (0.0, 0.0, 0.0)
+    aabb_max: Sequence[float] = (1.0, 1.0, 1.0)
+    learning_rate: float = 1e-2
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.99
+    adam_eps: float = 1e-8
+    loss_eps: float = 0.01
+    ema_alpha: float = 0.99
+    flags: int = FACTORIZE | CLAMP_QUERY
+    seed: int = 1
+
+    def to_c(self, device: int) -> _lib.NrcConfig:
+        c = _lib.NrcConfig()
+        _lib.load().nrc_default_config(ctypes.byref(c))
+        c.hidden_width = self.hidden_width
+        c.n_hidden_layers = self.n_hidden_layers
+        c.max_batch = self.max_batch
+        for i in range(3):
+            c.aabb_min[i] = self.aabb_min[i]
+            c.aabb_max[i] = self.aabb_max[i]
+        c.learning_rate = self.learning_rate
+        c.adam_beta1 = self.adam_beta1
+        c.adam_beta2 = self.adam_beta2
+        c.adam_eps = self.adam_eps
+        c.loss_eps = self.loss_eps
+        c.ema_alpha = self.ema_alpha
+        c.flags = self.flags
+        c.seed = self.seed & (2 ** 64 - 1)
+        c.device = device
+        return c
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def lcg_params(n: int, seed: int):
+    """LCG constants (a, c, m) of reading R15, from the C ABI."""
+    L = _lib.load()
+    a, c, m = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    st = L.nrc_lcg_params(int(n), int(seed) & (2 ** 64 - 1), ctypes.byref(a), ctypes.byref(c), ctypes.byref(m))
+    if st != 0:
+        raise NRCError(f"nrc_lcg_params: {L.nrc_status_string(st).decode()}")
+    return a.value, c.value, m.value
+
+
+class RadianceCache:
+    """The neural radiance cache on one GPU (state in a torch-owned arena)."""
+
+    def __init__(self, config: Optional[Config] = None, device: int = 0):
+        if not torch.cuda.is_available():
+            raise NRCError("RadianceCache needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        self.L = _lib.load()
+        self.config = config or Config()
+        self.device = torch.device("cuda", device)
+        self._cfg = self.config.to_c(device)
+        nbytes = self.L.nrc_state_bytes(ctypes.byref(self._cfg))
+        if nbytes == 0:
+            raise NRCError("invalid config")
+        self.state = torch.zeros(nbytes + 256, dtype=torch.uint8, device=self.device)
+        off = (-self.state.data_ptr()) % 256
+        self._state_ptr = self.state.data_ptr() + off
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            st = self.L.nrc_init(ctypes.byref(self._cfg), ctypes.c_void_p(self._state_ptr), nbytes, ctypes.byref(h))
+        if st != 0:
+            raise NRCError(f"nrc_init failed: {self.L.nrc_status_string(st).decode()}")
+        self.h = h
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st: int, what: str):
+        if st != 0:
+            msg = self.L.nrc_last_error(self.h)
+            raise NRCError(f"{what}: {self.L.nrc_status_string(st).decode()}: {msg.decode() if msg else ''}")
+
+    def _rec(self, records: torch.Tensor) -> torch.Tensor:
+        if records.device != self.device or records.dtype != torch.float32 or records.dim() != 2 \
+                or records.shape[1] != REC_FLOATS or not records.is_contiguous():
+            raise NRCError("records must be a contiguous float32 [n, 16] tensor on the cache's device")
+        return records
+
+    def _f32(self, t: torch.Tensor, shape, name: str) -> torch.Tensor:
+        if t.device != self.device or t.dtype != torch.float32 or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+            raise NRCError(f"{name} must be a contiguous float32 {tuple(shape)} tensor on the cache's device")
+        return t
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self.L.nrc_last_launch_count(self.h))
+
+    # ------------------------------------------------------------------ API
+    def query(self, records: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Radiance for each record with the EMA weights."""
+        records = self._rec(records)
+        n = records.shape[0]
+        if out is None:
+            out = torch.empty((n, 3), dtype=torch.float32, device=self.device)
+        self._f32(out, (n, 3), "out")
+        self._check(self.L.nrc_query(self.h, _ptr(records), n, _ptr(out), _stream(stream)), "nrc_query")
+        return out
+
+    def train_step(self, records: torch.Tensor, targets: torch.Tensor, loss: Optional[torch.Tensor] = None,
+                   stream=None) -> torch.Tensor:
+        """One Adam + EMA step on the batch; returns the device loss."""
+        records = self._rec(records)
+        n = records.shape[0]
+        self._f32(targets, (n, 3), "targets")
+        if loss is None:
+            loss = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self._check(self.L.nrc_train_step(self.h, _ptr(records), _ptr(targets), n, _ptr(loss), _stream(stream)),
+                    "nrc_train_step")
+        return loss
+
+    def train_backward(self, records: torch.Tensor, targets: torch.Tensor, grad: Optional[torch.Tensor] = None,
+                       loss_sum: Optional[torch.Tensor] = None, stream=None):
+        """Un-normalised gradient sum (logical layout) and loss sum over the records."""
+        records = self._rec(records)
+        n = records.shape[0]
+        self._f32(targets, (n, 3), "targets")
+        if grad is None:
+            grad = torch.empty(NPARAM, dtype=torch.float32, device=self.device)
+        if loss_sum is None:
+            loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self._check(self.L.nrc_train_backward(self.h, _ptr(records), _ptr(targets), n, _ptr(grad), _ptr(loss_sum),
+                                              _stream(stream)), "nrc_train_backward")
+        return grad, loss_sum
+
+    def train_apply(self, grad_sum: torch.Tensor, n_global: int, stream=None):
+        """Adam + EMA with g = grad_sum / n_global (after an all-reduce)."""
+        self._f32(grad_sum, (NPARAM,), "grad_sum")
+        self._check(self.L.nrc_train_apply(self.h, _ptr(grad_sum), int(n_global), _stream(stream)), "nrc_train_apply")
+
+    def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int = 4, l: int = 16384,
+                    shuffle_seed: int = 0, losses: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """A frame's training: LCG shuffle into s batches of l records."""
+        records = self._rec(records)
+        n = records.shape[0]
+        self._f32(targets, (n, 3), "targets")
+        if losses is None:
+            losses = torch.zeros(max(int(s), 1), dtype=torch.float32, device=self.device)
+        self._check(self.L.nrc_train_frame(self.h, _ptr(records), _ptr(targets), n, int(s), int(l),
+                                           int(shuffle_seed) & (2 ** 64 - 1), _ptr(losses), _stream(stream)),
+                    "nrc_train_frame")
+        return losses
+
+    def train_frame_backward(self, records: torch.Tensor, targets: torch.Tensor, l: int, shuffle_seed: int, j: int,
+                             row_begin: int, row_end: int, grad: Optional[torch.Tensor] = None,
+                             loss_sum: Optional[torch.Tensor] = None, stream=None):
+        """Gradient/loss sums over rows [row_begin, row_end) of shuffled batch j
+        (the data-parallel shard of nrc_train_frame's step j)."""
+        records = self._rec(records)
+        n = records.shape[0]
+        self._f32(targets, (n, 3), "targets")
+        if grad is None:
+            grad = torch.empty(NPARAM, dtype=torch.float32, device=self.device)
+        if loss_sum is None:
+            loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self._check(self.L.nrc_train_frame_backward(self.h, _ptr(records), _ptr(targets), n, int(l),
+                                                    int(shuffle_seed) & (2 ** 64 - 1), int(j), int(row_begin),
+                                                    int(row_end), _ptr(grad), _ptr(loss_sum), _stream(stream)),
+                    "nrc_train_frame_backward")
+        return grad, loss_sum
+
+    def encode(self, records: torch.Tensor, stream=None) -> torch.Tensor:
+        """The 64-dim fp16 network input of each record (Table 1 + padding)."""
+        records = self._rec(records)
+        n = records.shape[0]
+        out = torch.empty((n, 64), dtype=torch.float16, device=self.device)
+        self._check(self.L.nrc_encode(self.h, _ptr(records), n, _ptr(out), _stream(stream)), "nrc_encode")
+        return out
+
+    def get_params(self, which: str = "train") -> np.ndarray:
+        out = np.zeros(NPARAM, np.float32)
+        self._check(self.L.nrc_get_params(self.h, _PARAM_SETS[which], out.ctypes.data, NPARAM), "nrc_get_params")
+        return out
+
+    def set_params(self, values, which: str = "train"):
+        v = np.ascontiguousarray(values, dtype=np.float32).reshape(-1)
+        if v.size != NPARAM:
+            raise NRCError(f"expected {NPARAM} parameters")
+        self._check(self.L.nrc_set_params(self.h, _PARAM_SETS[which], v.ctypes.data, NPARAM), "nrc_set_params")
+
+    def stats(self) -> dict:
+        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(self.L.nrc_get_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "nrc_get_stats")
+        return {"step": a.value, "nonfinite_grads": b.value, "nonfinite_targets": c.value}
+
+    def frame_host(self, query_rec: np.ndarray, rgb_out: np.ndarray, train_rec: np.ndarray, train_tgt: np.ndarray,
+                   s: int, l: int, shuffle_seed: int, losses_out: np.ndarray, scratch: torch.Tensor, stream=None):
+        """End-to-end frame from host buffers (pinned numpy views recommended)."""
+        nq, nt = query_rec.shape[0], train_rec.shape[0]
+        self._check(self.L.nrc_frame_host(self.h, query_rec.ctypes.data, nq, rgb_out.ctypes.data,
+                                          train_rec.ctypes.data, train_tgt.ctypes.data, nt, int(s), int(l),
+                                          int(shuffle_seed) & (2 ** 64 - 1), losses_out.ctypes.data,
+                                          _ptr(scratch), scratch.numel(), _stream(stream)), "nrc_frame_host")
+
+    def frame_scratch_bytes(self, n_query: int, n_train: int) -> int:
+        return int(self.L.nrc_frame_scratch_bytes(int(n_query), int(n_train)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.nrc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """Diagnostic tcgen05 tile product (nrc_selftest_umma) on fp16 inputs."""
+    L = _lib.load()
+    shape = {0: (128, 64), 1: (128, 64), 2: (64, 64), 3: (128, 16)}[mode]
+    d = torch.zeros(shape, dtype=torch.float32, device=a.device)
+    a = a.contiguous()
+    b = b.contiguous()
+    st = L.nrc_selftest_umma(mode, _ptr(a), _ptr(b), _ptr(d))
+    if st != 0:
+        raise NRCError(f"nrc_selftest_umma: {L.nrc_status_string(st).decode()}")
+    return d

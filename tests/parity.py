@@ -1,0 +1,54 @@
+"""Parity metrics of SURVEY 8(c) "Parity definitions".
+
+Radiance: per channel max_i |q_gpu - q_ref| / max_i |q_ref|          <= 1e-2
+Gradients: per matrix max |G_gpu - G_ref| / max |G_ref|              <= 3e-2
+Post-Adam: per matrix, over entries whose gradient signs agree,
+           max |w_gpu - w_ref| / max |w_ref|                         <= 3e-2
+           (sign-flipped entries: <= 1% and each |G_ref| <= 3e-2 max|G_ref|)
+The tolerances are north_star's (BASELINE.json)."""
+import numpy as np
+
+OFF = [0, 4096, 8192, 12288, 16384, 20480, 20672]
+TOL_RADIANCE = 1e-2
+TOL_GRAD = 3e-2
+TOL_PARAM = 3e-2
+
+
+def radiance_err(q_gpu, q_ref):
+    q_gpu = np.asarray(q_gpu, np.float64); q_ref = np.asarray(q_ref, np.float64)
+    return [float(np.max(np.abs(q_gpu[:, c] - q_ref[:, c])) / max(np.max(np.abs(q_ref[:, c])), 1e-30))
+            for c in range(3)]
+
+
+def per_matrix_err(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    out = []
+    for i in range(6):
+        x, y = a[OFF[i]:OFF[i + 1]], b[OFF[i]:OFF[i + 1]]
+        out.append(float(np.max(np.abs(x - y)) / max(np.max(np.abs(y)), 1e-30)))
+    return out
+
+
+def post_adam_err(w_gpu, w_ref, g_gpu, g_ref):
+    """Per-matrix post-Adam error over sign-agreeing entries, plus the sign-flip
+    statistics (fraction, and worst |G_ref| / max|G_ref| among the flips)."""
+    w_gpu = np.asarray(w_gpu, np.float64); w_ref = np.asarray(w_ref, np.float64)
+    g_gpu = np.asarray(g_gpu, np.float64); g_ref = np.asarray(g_ref, np.float64)
+    errs, flips, worst = [], 0, 0.0
+    for i in range(6):
+        s = slice(OFF[i], OFF[i + 1])
+        agree = np.sign(g_gpu[s]) == np.sign(g_ref[s])
+        flips += int((~agree).sum())
+        gmax = max(np.max(np.abs(g_ref[s])), 1e-30)
+        if (~agree).any():
+            worst = max(worst, float(np.max(np.abs(g_ref[s][~agree])) / gmax))
+        d = np.abs(w_gpu[s] - w_ref[s])[agree]
+        errs.append(float(d.max() / max(np.max(np.abs(w_ref[s])), 1e-30)) if d.size else 0.0)
+    return errs, flips / float(len(w_ref)), worst
+
+
+def fp16_ulp(x):
+    """ulp of the fp16 number nearest to x (subnormal spacing 2^-24)."""
+    x = np.abs(np.asarray(x, np.float64))
+    e = np.floor(np.log2(np.maximum(x, 2.0 ** -14)))
+    return 2.0 ** (e - 10)

@@ -1,0 +1,88 @@
+"""CPU-side checks of the C ABI boundary (no GPU compute): the library builds
+for sm_100a, loads, exports every symbol include/nrc.h declares, validates
+configs, and the host-only helpers agree with the paper readings."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "nrc.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(nrc_[a-z_0-9]+)\s*\(", src)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def libnrc():
+    from paper_2106_12372_b200 import _lib
+    return _lib.load()
+
+
+def test_library_exports_every_declared_symbol(libnrc):
+    from paper_2106_12372_b200 import _lib
+    decl = declared_functions()
+    assert len(decl) >= 20
+    assert set(decl) == set(_lib.SYMBOLS)
+    for name in decl:
+        assert hasattr(libnrc, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.lib_path()], capture_output=True, text=True).stdout
+    for name in decl:
+        assert re.search(r"\bT " + name + r"\b", out), f"{name} not exported with C linkage"
+
+
+def test_library_is_sm100a_tcgen05(libnrc):
+    from paper_2106_12372_b200 import _lib
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.lib_path()], capture_output=True, text=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", _lib.lib_path()], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass          # tcgen05.mma
+    assert "LDTM" in sass             # tcgen05.ld
+    assert "UBLKCP" in sass           # TMA bulk copy
+    assert "HMMA" not in re.sub(r"UTCHMMA", "", sass)  # no legacy mma.sync path
+
+
+def test_default_config_and_state_bytes(libnrc):
+    from paper_2106_12372_b200 import _lib
+    c = _lib.NrcConfig()
+    libnrc.nrc_default_config(ctypes.byref(c))
+    assert c.abi_version == 1 and c.hidden_width == 64 and c.n_hidden_layers == 5
+    assert c.loss_eps == pytest.approx(0.01) and c.ema_alpha == pytest.approx(0.99)
+    assert c.learning_rate == pytest.approx(1e-2) and c.flags == 3
+    nb = libnrc.nrc_state_bytes(ctypes.byref(c))
+    assert nb > 21504 * 4 * 4 + 2 * 43008
+    bad = _lib.NrcConfig(); libnrc.nrc_default_config(ctypes.byref(bad)); bad.hidden_width = 96
+    assert libnrc.nrc_state_bytes(ctypes.byref(bad)) == 0
+    bad.hidden_width = 64; bad.aabb_max[1] = bad.aabb_min[1]
+    assert libnrc.nrc_state_bytes(ctypes.byref(bad)) == 0
+    bad.aabb_max[1] = 1.0; bad.abi_version = 7
+    assert libnrc.nrc_state_bytes(ctypes.byref(bad)) == 0
+
+
+def test_init_rejects_bad_arguments_without_gpu(libnrc):
+    from paper_2106_12372_b200 import _lib
+    c = _lib.NrcConfig(); libnrc.nrc_default_config(ctypes.byref(c))
+    h = ctypes.c_void_p()
+    assert libnrc.nrc_init(ctypes.byref(c), None, 0, ctypes.byref(h)) == 1  # NULL state
+    assert libnrc.nrc_query(None, None, 0, None, None) == 6                 # NULL handle -> STATE
+    assert libnrc.nrc_status_string(0) == b"NRC_OK"
+    assert libnrc.nrc_param_count(None) == 20672
+
+
+def test_lcg_params_match_oracle(libnrc, orc):
+    # both sides implement reading R15 independently; the constants must agree
+    from paper_2106_12372_b200 import lcg_params
+    for n in (1, 2, 3, 1000, 16384, 65536, 65537, 2 ** 20):
+        for seed in (0, 7, 0xFFFFFFFFFFFF):
+            assert lcg_params(n, seed) == orc.lcg_params(n, seed)
+
+
+def test_frame_scratch_bytes(libnrc):
+    assert libnrc.nrc_frame_scratch_bytes(0, 0) >= 0
+    nb = libnrc.nrc_frame_scratch_bytes(2073600, 65536)
+    assert nb >= 2073600 * (64 + 12) + 65536 * 76
