@@ -396,7 +396,7 @@ static nrc_status train_step_impl(nrc_handle* h, const nrc_record* d_rec, const 
     aa.nloss = np;
     aa.loss_scale = float(1.0 / double(n));
     aa.loss_out = d_loss;
-    nrc_adam_kernel<<<(kParamPadded + 255) / 256, 256, 0, st>>>(aa);
+    nrc_adam_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(aa);
     NRC_LAUNCHED(h, "nrc_adam_kernel");
     return NRC_OK;
 }
@@ -437,7 +437,7 @@ nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const floa
     int np = 0;
     Gather g{false, 0, 0, 0, 0, 0};
     if ((s = launch_train(h, d_rec, d_tgt, n_local, g, st, &np)) != NRC_OK) return s;
-    nrc_reduce_kernel<<<(kParamPadded + 255) / 256, 256, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
+    nrc_reduce_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
                                                                   d_loss_sum);
     NRC_LAUNCHED(h, "nrc_reduce_kernel");
     return NRC_OK;
@@ -464,7 +464,7 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
     nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
     int np = 0;
     if ((s = launch_train(h, d_rec, d_tgt, n, g, st, &np)) != NRC_OK) return s;
-    nrc_reduce_kernel<<<(kParamPadded + 255) / 256, 256, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
+    nrc_reduce_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
                                                                   d_loss_sum);
     NRC_LAUNCHED(h, "nrc_reduce_kernel");
     return NRC_OK;
@@ -483,7 +483,7 @@ nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_gl
     aa.src_logical = 1;
     aa.inv_n = float(1.0 / double(n_global));
     aa.loss_out = nullptr;
-    nrc_adam_kernel<<<(kParamPadded + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(aa);
+    nrc_adam_kernel<<<kParamPadded / 32, kRedThreads, 0, static_cast<cudaStream_t>(stream)>>>(aa);
     NRC_LAUNCHED(h, "nrc_adam_kernel");
     return NRC_OK;
 }

@@ -11,183 +11,9 @@
 //   helpers            encode-only, partial reduction, image refresh, selftest
 #pragma once
 #include "nrc_device.cuh"
+#include "nrc_query.cuh"
 
 namespace nrc {
-
-__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
-}
-
-// ============================================================================ query
-struct QueryArgs {
-    const float* rec;    // n records x 16 fp32
-    float* out;          // n x 3 fp32
-    uint64_t n;
-    const uint8_t* wimg; // fp16 operand image (43,008 B), EMA or raw
-    EncodeParams ep;
-    uint32_t flags;      // NRC_FACTORIZE | NRC_CLAMP_QUERY
-};
-
-constexpr int kRecTileBytes = kTile * kRecFloats * 4;  // 8 KB of records per tile
-
-template <int G>
-__host__ __device__ constexpr int query_smem_bytes() {
-    return 1024 + kImgBytes + G * kTileBytes + G * 2 * kRecTileBytes + 8 * (1 + 3 * G) + 16;
-}
-template <int G>
-__host__ __device__ constexpr uint32_t query_tmem_cols() {
-    return (G * 64 <= 64) ? 64 : (G * 64 <= 128) ? 128 : (G * 64 <= 256) ? 256 : 512;
-}
-
-// One CTA per SM, G independent 4-warp groups sharing the weight image.  A
-// group owns one 128-row tile at a time: thread r of the group owns row r
-// (TMEM lane r), encodes it, and runs the per-layer epilogue for it; thread
-// 0 of the group issues the tcgen05.mma chain.  Groups interleave so the
-// tensor pipe works on one group's layer while others run epilogues/encode.
-template <int G>
-__global__ void __launch_bounds__(128 * G, 1) nrc_query_kernel(QueryArgs args) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = align1024(smem_raw);
-    const uint32_t tid = threadIdx.x;
-    const uint32_t g = tid >> 7, r = tid & 127, warp = tid >> 5, wq = warp & 3;
-    uint8_t* sW = smem;
-    uint8_t* sH = smem + kImgBytes + g * kTileBytes;
-    uint8_t* sRecBase = smem + kImgBytes + G * kTileBytes + g * 2 * kRecTileBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImgBytes + G * kTileBytes + G * 2 * kRecTileBytes);
-    uint64_t* wbar = &bars[0];
-    uint64_t* mma_bar = &bars[1 + 3 * g];
-    uint64_t* rec_bar = &bars[2 + 3 * g];  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + 3 * G);
-
-    if (tid == 0) {
-        mbar_init(wbar, 1);
-        for (int i = 0; i < G; ++i) {
-            mbar_init(&bars[1 + 3 * i], 1);
-            mbar_init(&bars[2 + 3 * i], 1);
-            mbar_init(&bars[3 + 3 * i], 1);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 0) {
-        tmem_alloc(tmem_slot, query_tmem_cols<G>());
-        tmem_relinquish();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    if (tid == 0) {
-        mbar_arrive_expect_tx(wbar, kImgBytes);
-        bulk_g2s(sW, args.wimg, kImgBytes, wbar);
-    }
-
-    const uint64_t n = args.n;
-    const uint64_t ntiles = (n + kTile - 1) / kTile;
-    const uint64_t stride = uint64_t(gridDim.x) * G;
-    uint64_t tile = uint64_t(blockIdx.x) * G + g;
-
-    auto issue_records = [&](uint64_t t, int b) {
-        const uint64_t row0 = t * kTile;
-        const uint64_t nv = (n - row0) < uint64_t(kTile) ? (n - row0) : uint64_t(kTile);
-        const uint32_t bytes = uint32_t(nv) * kRecFloats * 4;
-        mbar_arrive_expect_tx(&rec_bar[b], bytes);
-        bulk_g2s(sRecBase + b * kRecTileBytes, args.rec + row0 * kRecFloats, bytes, &rec_bar[b]);
-    };
-    if (r == 0 && tile < ntiles) issue_records(tile, 0);
-    mbar_wait(wbar, 0);
-
-    const uint32_t idesc64 = make_idesc(128, 64, 0, 0);
-    const uint32_t idesc16 = make_idesc(128, 16, 0, 0);
-    const uint32_t sW_a = smem_u32(sW), sH_a = smem_u32(sH);
-    const uint32_t t_acc = tmem_base + g * 64;
-    const uint32_t t_row = t_acc + ((wq * 32u) << 16);
-    uint32_t mma_phase = 0, rec_phase0 = 0, rec_phase1 = 0;
-    int buf = 0;
-
-#pragma unroll 1
-    for (; tile < ntiles; tile += stride) {
-        const uint64_t row = tile * kTile + r;
-        const bool valid = row < n;
-        if (buf == 0) {
-            mbar_wait(&rec_bar[0], rec_phase0);
-            rec_phase0 ^= 1;
-        } else {
-            mbar_wait(&rec_bar[1], rec_phase1);
-            rec_phase1 ^= 1;
-        }
-        float rec[16];
-        {
-            const float4* src = reinterpret_cast<const float4*>(sRecBase + buf * kRecTileBytes + r * 64);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float4 v = valid ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-                rec[4 * c + 0] = v.x;
-                rec[4 * c + 1] = v.y;
-                rec[4 * c + 2] = v.z;
-                rec[4 * c + 3] = v.w;
-            }
-        }
-        float fac[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) fac[c] = (args.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
-        {
-            uint32_t h[32];
-            encode_record(rec, args.ep, h);
-            store_row_swz(sH_a, r, h);
-        }
-        fence_async_smem();
-        named_bar_sync(1 + g, 128);
-        if (r == 0 && tile + stride < ntiles) issue_records(tile + stride, buf ^ 1);
-
-#pragma unroll 1
-        for (int L = 0; L < kNumLayers; ++L) {
-            if (r == 0) {
-                tc_fence_after();
-                const uint32_t wl = sW_a + layer_off(L) * 2;
-                const uint32_t idesc = (L < 5) ? idesc64 : idesc16;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) umma_f16(t_acc, desc_kmajor(sH_a, k), desc_kmajor(wl, k), idesc, k > 0);
-                umma_commit(mma_bar);
-            }
-            mbar_wait(mma_bar, mma_phase);
-            mma_phase ^= 1;
-            tc_fence_after();
-            if (L < 5) {
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    uint32_t v[32];
-                    tmem_ld32(t_row + 32 * half, v);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const float* f = reinterpret_cast<const float*>(v) + 8 * c;
-                        st_shared_v4(sH_a + swz(r, 4 * half + c), pack_h2_relu(f[0], f[1]), pack_h2_relu(f[2], f[3]),
-                                     pack_h2_relu(f[4], f[5]), pack_h2_relu(f[6], f[7]));
-                    }
-                }
-                tc_fence_before();
-                fence_async_smem();
-                named_bar_sync(1 + g, 128);
-            } else {
-                uint32_t v[4];
-                tmem_ld4(t_row, v);
-                tc_fence_before();
-                if (valid) {
-                    float* o = args.out + row * 3;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        float q = __uint_as_float(v[c]) * fac[c];
-                        if (args.flags & 2u) q = fmaxf(q, 0.0f);
-                        o[c] = q;
-                    }
-                }
-            }
-        }
-        buf ^= 1;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem_base, query_tmem_cols<G>());
-}
 
 // ============================================================================ train
 struct TrainArgs {
@@ -492,32 +318,50 @@ __device__ __forceinline__ int logical_index(int layer, int row, int col) {
     return row < 3 ? 20480 + row * 64 + col : -1;
 }
 
-__global__ void __launch_bounds__(256) nrc_adam_kernel(AdamArgs a) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (blockIdx.x == 0 && threadIdx.x < 32 && a.loss_out != nullptr) {
-        float s = 0.0f;
-        for (int p = threadIdx.x; p < a.nloss; p += 32) s += a.loss_part[p];
+// Block-level fixed-order sum of partials[p][j] over p < np for the 32
+// parameters j = 32*blockIdx.x + lane: warp w sums p = w, w+8, ... in
+// ascending order, then warp 0 adds the 8 warp sums in warp order.  The same
+// order in nrc_adam_kernel and nrc_reduce_kernel keeps nrc_train_step and
+// nrc_train_backward + nrc_train_apply bitwise identical.
+constexpr int kRedThreads = 256;
+constexpr int kRedWarps = kRedThreads / 32;
+__device__ __forceinline__ float block_partial_sum(const float* __restrict__ partials, int np, int j) {
+    __shared__ float sred[kRedWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float s = 0.0f;
+    const float* p0 = partials + j;
+#pragma unroll 4
+    for (int p = w; p < np; p += kRedWarps) s += __ldcg(p0 + size_t(p) * kParamPadded);
+    sred[w][lane] = s;
+    __syncthreads();
+    float t = 0.0f;
+    if (w == 0) {
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        for (int k = 0; k < kRedWarps; ++k) t += sred[k][lane];
+    }
+    return t;
+}
+__device__ __forceinline__ float warp_loss_sum(const float* __restrict__ part, int np) {
+    float s = 0.0f;
+    for (int p = threadIdx.x & 31; p < np; p += 32) s += part[p];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+}
+
+// grid = kParamPadded / 32 blocks of kRedThreads; warp 0 updates 32 parameters.
+__global__ void __launch_bounds__(kRedThreads) nrc_adam_kernel(AdamArgs a) {
+    const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+    float g = 0.0f;
+    if (!a.src_logical) g = block_partial_sum(a.src, a.nsrc, j);
+    if (threadIdx.x >= 32) return;
+    if (blockIdx.x == 0 && a.loss_out != nullptr) {
+        const float s = warp_loss_sum(a.loss_part, a.nloss);
         if (threadIdx.x == 0) *a.loss_out = s * a.loss_scale;
     }
-    if (j >= kParamPadded) return;
     int layer, row, col;
     padded_coords(j, layer, row, col);
-    float g = 0.0f;
-    if (!a.src_logical) {
-        const float* s = a.src + j;
-        int p = 0;
-        for (; p + 4 <= a.nsrc; p += 4) {
-            const float x0 = s[size_t(p) * kParamPadded], x1 = s[size_t(p + 1) * kParamPadded];
-            const float x2 = s[size_t(p + 2) * kParamPadded], x3 = s[size_t(p + 3) * kParamPadded];
-            g += x0;
-            g += x1;
-            g += x2;
-            g += x3;
-        }
-        for (; p < a.nsrc; ++p) g += s[size_t(p) * kParamPadded];
-    } else {
+    if (a.src_logical) {
         const int li = logical_index(layer, row, col);
         g = li >= 0 ? a.src[li] : 0.0f;
     }
@@ -551,34 +395,22 @@ __global__ void nrc_image_kernel(const float* __restrict__ w, uint8_t* __restric
 
 // Sum the per-CTA partials in fixed order into a logical-layout gradient
 // (nrc_train_backward), plus the loss sum.
-__global__ void nrc_reduce_kernel(const float* __restrict__ partials, int np, float* __restrict__ grad,
-                                  const float* __restrict__ loss_part, float* loss_sum) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (blockIdx.x == 0 && threadIdx.x < 32 && loss_sum != nullptr) {
-        float s = 0.0f;
-        for (int p = threadIdx.x; p < np; p += 32) s += loss_part[p];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+// grid = kParamPadded / 32 blocks of kRedThreads (same order as Adam's sum).
+__global__ void __launch_bounds__(kRedThreads) nrc_reduce_kernel(const float* __restrict__ partials, int np,
+                                                                 float* __restrict__ grad,
+                                                                 const float* __restrict__ loss_part,
+                                                                 float* loss_sum) {
+    const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+    const float g = block_partial_sum(partials, np, j);
+    if (threadIdx.x >= 32) return;
+    if (blockIdx.x == 0 && loss_sum != nullptr) {
+        const float s = warp_loss_sum(loss_part, np);
         if (threadIdx.x == 0) *loss_sum = s;
     }
-    if (j >= kParamPadded) return;
     int layer, row, col;
     padded_coords(j, layer, row, col);
     const int li = logical_index(layer, row, col);
-    if (li < 0) return;
-    float g = 0.0f;
-    const float* s = partials + j;
-    int p = 0;
-    for (; p + 4 <= np; p += 4) {
-        const float x0 = s[size_t(p) * kParamPadded], x1 = s[size_t(p + 1) * kParamPadded];
-        const float x2 = s[size_t(p + 2) * kParamPadded], x3 = s[size_t(p + 3) * kParamPadded];
-        g += x0;
-        g += x1;
-        g += x2;
-        g += x3;
-    }
-    for (; p < np; ++p) g += s[size_t(p) * kParamPadded];
-    grad[li] = g;
+    if (li >= 0) grad[li] = g;
 }
 
 // Encoding only (nrc_encode): one thread per record, logical feature order.
