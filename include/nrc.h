@@ -209,7 +209,8 @@ nrc_status nrc_frame_host(nrc_handle* h, const nrc_record* h_query, uint64_t n_q
 /* Diagnostic: one tcgen05 tile product in each operand layout the kernels
  * use, on plain row-major fp16 inputs (mode 0: D[128x64] = A[128x64] B[64x64]^T;
  * mode 1: D[128x64] = A[128x64] B[64x64]; mode 2: D[64x64] = A[128x64]^T
- * B[128x64]; mode 3: D[128x16] = A[128x64] B[16x64]^T).  D is fp32
+ * B[128x64]; mode 3: D[128x16] = A[128x64] B[16x64]^T; mode 4: as mode 0 with
+ * A read from tensor memory).  D is fp32
  * row-major.  Synchronous. */
 nrc_status nrc_selftest_umma(int mode, const uint16_t* d_a, const uint16_t* d_b, float* d_d);
 

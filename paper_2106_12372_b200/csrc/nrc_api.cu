@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -16,7 +17,28 @@ using namespace nrc;
 
 namespace {
 
-constexpr int kQueryGroups = 4;   // 4-warp groups per query CTA
+// Query-kernel configurations <tile groups per CTA, tiles in flight per group>
+// (DESIGN.md 5.2).  Entry 0 is the default; NRC_QUERY_CFG=i selects another
+// one (tuning runs only).
+struct QueryEntry {
+    cudaError_t (*set_smem)();
+    void (*launch)(int, const QueryArgs&, cudaStream_t);
+    int groups;
+};
+template <int G, int S>
+struct QueryLauncher {
+    static cudaError_t set_smem() {
+        return cudaFuncSetAttribute(nrc_query_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    query_smem_bytes<G, S>());
+    }
+    static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
+        nrc_query_kernel<G, S><<<grid, 128 * G, query_smem_bytes<G, S>(), st>>>(qa);
+    }
+};
+#define NRC_QCFG(G, S) {&QueryLauncher<G, S>::set_smem, &QueryLauncher<G, S>::launch, G}
+const QueryEntry kQueryCfgs[] = {NRC_QCFG(4, 2), NRC_QCFG(3, 2), NRC_QCFG(2, 4)};
+#undef NRC_QCFG
+constexpr int kNumQueryCfgs = int(sizeof(kQueryCfgs) / sizeof(kQueryCfgs[0]));
 constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
 
 struct StateLayout {
@@ -65,6 +87,7 @@ struct nrc_handle {
     EncodeParams ep;
     std::string err;
     uint32_t launches;
+    int query_cfg;
     float* d_w() { return reinterpret_cast<float*>(state + L.w); }
     float* d_m() { return reinterpret_cast<float*>(state + L.m); }
     float* d_v() { return reinterpret_cast<float*>(state + L.v); }
@@ -241,10 +264,11 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
         h->err = "libnrc is built for sm_100a (B200); device compute capability major = " + std::to_string(major);
         return bail(NRC_ERR_UNSUPPORTED);
     }
-    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_query_kernel<kQueryGroups>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                query_smem_bytes<kQueryGroups>()),
-                        "cudaFuncSetAttribute(query)")) != NRC_OK)
-        return bail(s);
+    h->query_cfg = 0;
+    if (const char* e = std::getenv("NRC_QUERY_CFG")) h->query_cfg = std::atoi(e);
+    if (h->query_cfg < 0 || h->query_cfg >= kNumQueryCfgs) h->query_cfg = 0;
+    for (int i = 0; i < kNumQueryCfgs; ++i)
+        if ((s = cuda_check(h, kQueryCfgs[i].set_smem(), "cudaFuncSetAttribute(query)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 kTrainSmemBytes),
                         "cudaFuncSetAttribute(train)")) != NRC_OK)
@@ -304,10 +328,10 @@ nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* 
     qa.ep = h->ep;
     qa.flags = h->cfg.flags & (NRC_FACTORIZE | NRC_CLAMP_QUERY);
     const uint64_t ntiles = (n + kTile - 1) / kTile;
-    const uint64_t ctas_needed = (ntiles + kQueryGroups - 1) / kQueryGroups;
-    const int grid = int(ctas_needed < uint64_t(h->num_sms) ? ctas_needed : uint64_t(h->num_sms));
-    nrc_query_kernel<kQueryGroups><<<grid, 128 * kQueryGroups, query_smem_bytes<kQueryGroups>(),
-                                     static_cast<cudaStream_t>(stream)>>>(qa);
+    const uint64_t G = uint64_t(kQueryCfgs[h->query_cfg].groups);
+    const uint64_t ctas = (ntiles + G - 1) / G;  // one tile stream per group
+    const int grid = int(ctas < uint64_t(h->num_sms) ? ctas : uint64_t(h->num_sms));
+    kQueryCfgs[h->query_cfg].launch(grid, qa, static_cast<cudaStream_t>(stream));
     NRC_LAUNCHED(h, "nrc_query_kernel");
     return NRC_OK;
 }
@@ -632,7 +656,7 @@ nrc_status nrc_frame_host(nrc_handle* h, const nrc_record* h_query, uint64_t n_q
 }
 
 nrc_status nrc_selftest_umma(int mode, const uint16_t* d_a, const uint16_t* d_b, float* d_d) {
-    if (mode < 0 || mode > 3 || !d_a || !d_b || !d_d || !aligned(d_a, 16) || !aligned(d_b, 16))
+    if (mode < 0 || mode > 4 || !d_a || !d_b || !d_d || !aligned(d_a, 16) || !aligned(d_b, 16))
         return NRC_ERR_INVALID_ARGUMENT;
     nrc_selftest_kernel<<<1, 128>>>(mode, d_a, d_b, d_d);
     if (cudaGetLastError() != cudaSuccess) return NRC_ERR_CUDA;

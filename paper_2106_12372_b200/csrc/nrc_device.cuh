@@ -48,6 +48,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Non-blocking probe: true once the phase with the given parity has completed.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Four probes issued back to back (their ~150-cycle latencies overlap);
+// bit i of the result is set when barrier i's phase with parity p_i completed.
+__device__ __forceinline__ uint32_t mbar_test4(uint32_t a0, uint32_t p0, uint32_t a1, uint32_t p1, uint32_t a2,
+                                               uint32_t p2, uint32_t a3, uint32_t p3) {
+    uint32_t m;
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2, q3;\n\t.reg .b32 t0, t1, t2, t3;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %2;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q1, [%3], %4;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q2, [%5], %6;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 q3, [%7], %8;\n\t"
+        "selp.b32 t0, 1, 0, q0;\n\tselp.b32 t1, 2, 0, q1;\n\tselp.b32 t2, 4, 0, q2;\n\tselp.b32 t3, 8, 0, q3;\n\t"
+        "or.b32 t0, t0, t1;\n\tor.b32 t2, t2, t3;\n\tor.b32 %0, t0, t2;\n}"
+        : "=r"(m)
+        : "r"(a0), "r"(p0), "r"(a1), "r"(p1), "r"(a2), "r"(p2), "r"(a3), "r"(p3)
+        : "memory");
+    return m;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -89,6 +122,16 @@ __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint6
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Same with the A operand read from TMEM (lane = row, 2 fp16 per column, K-major).
+__device__ __forceinline__ void umma_f16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread
@@ -150,6 +193,18 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
                  : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3])::"memory");
 }
+#define NRC_S8(o) "r"(r[o + 0]), "r"(r[o + 1]), "r"(r[o + 2]), "r"(r[o + 3]), "r"(r[o + 4]), "r"(r[o + 5]), \
+                  "r"(r[o + 6]), "r"(r[o + 7])
+// 32 lanes x 32 bit store of 32 consecutive columns, then wait for completion.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        NRC_S8(0), NRC_S8(8), NRC_S8(16), NRC_S8(24)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+#undef NRC_S8
 #undef NRC_R8
 #undef NRC_W8
 
@@ -189,17 +244,11 @@ struct EncodeParams {
     float inv[3];
 };
 
-// tri(x) = 2 |x mod 2 - 1| - 1, floored mod.  x = 2^d v is exact in
-// fp32, so floor(x/2) and x - 2 floor(x/2) are exact.
-__device__ __forceinline__ float tri_f(float x) {
-    float m = x - 2.0f * floorf(x * 0.5f);
-    return 2.0f * fabsf(m - 1.0f) - 1.0f;
-}
-// quartic(x) = 15/16 (1 - x^2)^2 on |x| <= 1, branchless.
+// quartic(x) = 15/16 (1 - x^2)^2 on |x| <= 1, else 0: clamping
+// 1 - x^2 at 0 gives the compact support without a compare.
 __device__ __forceinline__ float quartic_f(float x) {
-    float t = fmaf(-x, x, 1.0f);
-    float q = 0.9375f * t * t;
-    return fabsf(x) <= 1.0f ? q : 0.0f;
+    const float t = fmaxf(fmaf(-x, x, 1.0f), 0.0f);
+    return (0.9375f * t) * t;
 }
 // One-blob, k = 4, centres (i + 1/2)/4, width 1/4, clamp to [0,1] (R6).
 __device__ __forceinline__ void one_blob4(float s, float* o) {
@@ -208,22 +257,71 @@ __device__ __forceinline__ void one_blob4(float s, float* o) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[i] = quartic_f(x - (float(i) + 0.5f));
 }
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// acos(z), |error| <= 2.4e-7 rad in fp32 (Abramowitz & Stegun 4.4.46, 8 terms).
+__device__ __forceinline__ float acos_fast(float z) {
+    const float a = fabsf(z);
+    float p = -0.0012624911f;
+    p = fmaf(p, a, 0.0066700901f);
+    p = fmaf(p, a, -0.0170881256f);
+    p = fmaf(p, a, 0.0308918810f);
+    p = fmaf(p, a, -0.0501743046f);
+    p = fmaf(p, a, 0.0889789874f);
+    p = fmaf(p, a, -0.2145988016f);
+    p = fmaf(p, a, 1.5707963050f);
+    const float r = sqrt_approx(1.0f - a) * p;
+    return z < 0.0f ? 3.14159265358979323846f - r : r;
+}
+// atan2(y, x) with IEEE sign conventions (atan2(+-0, x<0) = +-pi), |error| <=
+// 1.2e-7 rad: atan(a) = a P(a^2) on [0,1] (degree-7 minimax fit, fp32 Horner).
+__device__ __forceinline__ float atan2_fast(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float a = mx > 0.0f ? __fdividef(mn, mx) : 0.0f;
+    const float s = a * a;
+    float p = -0.004053147975355387f;
+    p = fmaf(p, s, 0.021859295666217804f);
+    p = fmaf(p, s, -0.05590952932834625f);
+    p = fmaf(p, s, 0.09642207622528076f);
+    p = fmaf(p, s, -0.13908733427524567f);
+    p = fmaf(p, s, 0.19946610927581787f);
+    p = fmaf(p, s, -0.3332986831665039f);
+    p = fmaf(p, s, 0.9999993443489075f);
+    float r = a * p;
+    if (ay > ax) r = 1.57079632679489662f - r;
+    if (x < 0.0f) r = 3.14159265358979323846f - r;
+    return copysignf(r, y);
+}
 // sph (Table 1 caption; reading R7): (acos(z)/pi, (atan2(y,x)+pi)/(2 pi))
 __device__ __forceinline__ void sph_f(float x, float y, float z, float& th, float& ph) {
-    float l2 = x * x + y * y + z * z;
+    const float l2 = x * x + y * y + z * z;
     if (!(l2 > 0.0f)) {
         x = 0.0f;
         y = 0.0f;
         z = 1.0f;
     } else {
-        float il = 1.0f / sqrtf(l2);
+        const float il = rsqrt_approx(l2);
         x *= il;
         y *= il;
         z *= il;
     }
     z = fminf(fmaxf(z, -1.0f), 1.0f);
-    th = acosf(z) * 0.318309886183790672f;                      // 1/pi
-    ph = (atan2f(y, x) + 3.14159265358979323846f) * 0.159154943091895336f;  // 1/(2 pi)
+    th = acos_fast(z) * 0.318309886183790672f;                                  // 1/pi
+    ph = (atan2_fast(y, x) + 3.14159265358979323846f) * 0.159154943091895336f;  // 1/(2 pi)
 }
 
 // Encodes one record into 64 fp16 features packed as 32 f16x2 words, in the
@@ -233,9 +331,17 @@ __device__ __forceinline__ void encode_record(const float* rec, const EncodePara
     float e[64];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        float v = __fmul_rn(__fsub_rn(rec[a], ep.lo[a]), ep.inv[a]);
+        const float v = __fmul_rn(__fsub_rn(rec[a], ep.lo[a]), ep.inv[a]);
+        // m_d = 2^d v mod 2 by exact doubling: m_{d+1} = 2 (m_d - [m_d >= 1]);
+        // tri(2^d v) = 2 |m_d - 1| - 1, bit-identical to the direct form.
+        float m = v - 2.0f * floorf(v * 0.5f);
 #pragma unroll
-        for (int d = 0; d < 12; ++d) e[12 * a + d] = tri_f(v * float(1 << d));
+        for (int d = 0; d < 12; ++d) {
+            const float t = m - 1.0f;
+            e[12 * a + d] = fmaf(2.0f, fabsf(t), -1.0f);
+            m = t >= 0.0f ? t : m;
+            m = m + m;
+        }
     }
     float th, ph;
     sph_f(rec[3], rec[4], rec[5], th, ph);
@@ -244,7 +350,7 @@ __device__ __forceinline__ void encode_record(const float* rec, const EncodePara
     sph_f(rec[6], rec[7], rec[8], th, ph);
     one_blob4(th, e + 44);
     one_blob4(ph, e + 48);
-    one_blob4(1.0f - expf(-fmaxf(rec[9], 0.0f)), e + 52);
+    one_blob4(1.0f - ex2_approx(-1.44269504088896341f * fmaxf(rec[9], 0.0f)), e + 52);  // 1 - e^{-r}
 #pragma unroll
     for (int c = 0; c < 6; ++c) e[56 + c] = rec[10 + c];
     e[62] = 1.0f;

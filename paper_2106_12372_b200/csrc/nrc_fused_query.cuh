@@ -1,6 +1,15 @@
-// nrc_query.cuh -- the fused cache-query kernel (rows a1-a3 of SURVEY 8(a)):
+// nrc_fused_query.cuh -- the fused cache-query kernel (rows a1-a3 of SURVEY 8(a)):
 // encode (Table 1) -> 6 tcgen05 layers
 // -> reflectance factorisation and clamp, EMA weights.
+//
+// Design notes: a layer's MMA round trip (issue -> commit ->
+// mbarrier -> TMEM drain) is ~650 cycles against ~175 cycles of tensor work
+// (scripts/ubench_tcgen05.cu), so each SM keeps 8 tiles in flight (TMEM holds
+// 8 fp32 accumulators of 64 columns).  Warp-specialised variants (dedicated
+// encoder / epilogue / MMA-issuer warps with mbarrier or atomic hand-offs)
+// were measured slower than this "every warp does everything" layout on the
+// 1080p query (151.6 us vs 184-456 us): the hot path is latency-bound, and
+// 16 interchangeable warps per SM hide more latency than role-split ones.
 #pragma once
 #include "nrc_device.cuh"
 
@@ -20,28 +29,26 @@ struct QueryArgs {
 };
 
 constexpr int kRecTileBytes = kTile * kRecFloats * 4;  // 8 KB of records per tile
-constexpr int kQuerySlots = 2;                         // tiles in flight per group
 
-template <int G>
+template <int G, int S>
 __host__ __device__ constexpr int query_smem_bytes() {
-    return 1024 + kImgBytes + G * kQuerySlots * kTileBytes + G * kRecTileBytes + 8 * (1 + (kQuerySlots + 1) * G) +
+    return 1024 + kImgBytes + G * S * kTileBytes + G * kRecTileBytes + 8 * (1 + (S + 1) * G) +
            16;
 }
-template <int G>
+template <int G, int S>
 __host__ __device__ constexpr uint32_t query_tmem_cols() {
-    return (G * kQuerySlots * 64 <= 128) ? 128 : (G * kQuerySlots * 64 <= 256) ? 256 : 512;
+    return (G * S * 64 <= 128) ? 128 : (G * S * 64 <= 256) ? 256 : 512;
 }
 
 // Persistent: one CTA per SM, G independent 4-warp groups sharing one SMEM
-// copy of the weight image.  A group keeps kQuerySlots 128-row tiles in
+// copy of the weight image.  A group keeps S 128-row tiles in
 // flight (each with its own SMEM activation tile and TMEM accumulator) and
 // round-robins over them: while the tensor pipe runs slot s's layer, the
 // group's threads drain slot s^1's accumulator (ReLU + fp16) or encode its
 // next tile.  Thread r of a group owns row r (TMEM lane r); thread 0 of the
 // group issues the tcgen05.mma chain and the TMA bulk copies of the records.
-template <int G>
+template <int G, int S>
 __global__ void __launch_bounds__(128 * G, 1) nrc_query_kernel(QueryArgs args) {
-    constexpr int S = kQuerySlots;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     const uint32_t tid = threadIdx.x;
@@ -60,7 +67,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_kernel(QueryArgs args) {
         fence_mbar_init();
     }
     if (warp == 0) {
-        tmem_alloc(tmem_slot, query_tmem_cols<G>());
+        tmem_alloc(tmem_slot, query_tmem_cols<G, S>());
         tmem_relinquish();
     }
     tc_fence_before();
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_kernel(QueryArgs args) {
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem_base, query_tmem_cols<G>());
+    if (warp == 0) tmem_dealloc(tmem_base, query_tmem_cols<G, S>());
 }
 
 }  // namespace nrc

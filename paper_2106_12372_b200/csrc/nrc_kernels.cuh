@@ -11,7 +11,7 @@
 //   helpers            encode-only, partial reduction, image refresh, selftest
 #pragma once
 #include "nrc_device.cuh"
-#include "nrc_query.cuh"
+#include "nrc_fused_query.cuh"
 
 namespace nrc {
 
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(128, 1) nrc_selftest_kernel(int mode, const ui
         fence_mbar_init();
     }
     if (warp == 0) {
-        tmem_alloc(&tslot, 64);
+        tmem_alloc(&tslot, 128);
         tmem_relinquish();
     }
     fence_async_smem();
@@ -459,9 +459,21 @@ __global__ void __launch_bounds__(128, 1) nrc_selftest_kernel(int mode, const ui
     __syncthreads();
     tc_fence_after();
     const uint32_t tb = tslot;
+    if (mode == 4) {  // A row of this thread -> TMEM columns 64..95 (2 fp16 per column)
+        uint32_t row[32];
+        const uint32_t* A32 = reinterpret_cast<const uint32_t*>(A);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) row[q] = A32[tid * 32 + q];
+        tmem_st32(tb + ((warp * 32u) << 16) + 64, row);
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
     if (tid == 0) {
         const uint32_t a = smem_u32(sA), b = smem_u32(sB);
-        if (mode == 0) {
+        if (mode == 4) {
+            for (int k = 0; k < 4; ++k) umma_f16_ta(tb, tb + 64 + 8 * k, desc_kmajor(b, k), make_idesc(128, 64, 0, 0), k > 0);
+        } else if (mode == 0) {
             for (int k = 0; k < 4; ++k) umma_f16(tb, desc_kmajor(a, k), desc_kmajor(b, k), make_idesc(128, 64, 0, 0), k > 0);
         } else if (mode == 1) {
             for (int k = 0; k < 4; ++k) umma_f16(tb, desc_kmajor(a, k), desc_mnmajor(b, k), make_idesc(128, 64, 0, 1), k > 0);
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(128, 1) nrc_selftest_kernel(int mode, const ui
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tb, 64);
+    if (warp == 0) tmem_dealloc(tb, 128);
 }
 
 }  // namespace nrc

@@ -262,7 +262,7 @@ class RadianceCache:
 def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """Diagnostic tcgen05 tile product (nrc_selftest_umma) on fp16 inputs."""
     L = _lib.load()
-    shape = {0: (128, 64), 1: (128, 64), 2: (64, 64), 3: (128, 16)}[mode]
+    shape = {0: (128, 64), 1: (128, 64), 2: (64, 64), 3: (128, 16), 4: (128, 64)}[mode]
     d = torch.zeros(shape, dtype=torch.float32, device=a.device)
     a = a.contiguous()
     b = b.contiguous()

@@ -28,15 +28,15 @@ def dev(x):
 
 
 # ---------------------------------------------------------------- tcgen05 operand layouts
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 def test_selftest_umma_layouts(nrc, mode):
     g = torch.Generator().manual_seed(mode)
     a = torch.randn(128, 64, generator=g).half()
-    bshape = {0: (64, 64), 1: (64, 64), 2: (128, 64), 3: (16, 64)}[mode]
+    bshape = {0: (64, 64), 1: (64, 64), 2: (128, 64), 3: (16, 64), 4: (64, 64)}[mode]
     b = torch.randn(*bshape, generator=g).half()
     d = nrc.selftest_umma(mode, a.cuda(), b.cuda()).cpu()
     A, B = a.float(), b.float()
-    ref = {0: lambda: A @ B.T, 1: lambda: A @ B, 2: lambda: A.T @ B, 3: lambda: A @ B.T}[mode]()
+    ref = {0: lambda: A @ B.T, 1: lambda: A @ B, 2: lambda: A.T @ B, 3: lambda: A @ B.T, 4: lambda: A @ B.T}[mode]()
     torch.testing.assert_close(d, ref, rtol=1e-4, atol=1e-3)
 
 
