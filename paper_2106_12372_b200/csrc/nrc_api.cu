@@ -88,6 +88,9 @@ struct nrc_handle {
     std::string err;
     uint32_t launches;
     int query_cfg;
+    long long* dbg = nullptr;  // diagnostics only (nrc_debug_set_trace)
+    unsigned long long gbar = 0;  // arrivals so far on the train kernel's grid-barrier counter
+    bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
     float* d_w() { return reinterpret_cast<float*>(state + L.w); }
     float* d_m() { return reinterpret_cast<float*>(state + L.m); }
     float* d_v() { return reinterpret_cast<float*>(state + L.v); }
@@ -120,6 +123,41 @@ static nrc_status cuda_check(nrc_handle* h, cudaError_t e, const char* what) {
     } while (0)
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+// Launch with programmatic dependent launch (PDL): the kernel may start while
+// its predecessor in the stream drains; it calls griddepcontrol.wait before
+// touching anything the predecessor writes.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+// Cooperative launch (all CTAs co-resident; the fused train kernel has grid barriers).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 extern "C" {
 
@@ -265,6 +303,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
         return bail(NRC_ERR_UNSUPPORTED);
     }
     h->query_cfg = 0;
+    if (const char* e = std::getenv("NRC_COOP")) h->coop = std::atoi(e) != 0;
     if (const char* e = std::getenv("NRC_QUERY_CFG")) h->query_cfg = std::atoi(e);
     if (h->query_cfg < 0 || h->query_cfg >= kNumQueryCfgs) h->query_cfg = 0;
     for (int i = 0; i < kNumQueryCfgs; ++i)
@@ -341,10 +380,36 @@ struct Gather {
     uint64_t a, c, m, n, offset;
 };
 
-// fused forward/backward over n rows -> per-CTA partials; returns #partials
+// Adam bias corrections and EMA coefficients of optimisation step t >= 1
+static StepCoef step_coef(const nrc_config& c, uint64_t t) {
+    StepCoef k{};
+    k.inv_bc1 = float(1.0 / (1.0 - std::pow(double(c.adam_beta1), double(t))));
+    k.inv_bc2 = float(1.0 / (1.0 - std::pow(double(c.adam_beta2), double(t))));
+    // Eq.(2): eta_t = 1 - a^t.  R12: W-bar = [(1-a) W + a eta_{t-1} W-bar] / eta_t
+    const double al = c.ema_alpha;
+    const double eta_t = 1.0 - std::pow(al, double(t));
+    const double eta_p = 1.0 - std::pow(al, double(t - 1));
+    if (al == 0.0) {
+        k.ema_c1 = 1.0f;
+        k.ema_c2 = 0.0f;
+    } else if (c.flags & NRC_EMA_PRINTED_FORM) {
+        k.ema_c1 = float((1.0 - al) / eta_t);
+        k.ema_c2 = float(al * eta_p);
+    } else {
+        k.ema_c1 = float((1.0 - al) / eta_t);
+        k.ema_c2 = float(al * eta_p / eta_t);
+    }
+    return k;
+}
+
+// The train kernel over n rows per step.  nsteps == 0: one step, per-CTA
+// partials only (PDL launch; the caller reduces).  nsteps >= 1: fused
+// cooperative launch running nsteps optimisation steps (reduce + Adam + EMA
+// inside), batch-mean losses to d_losses[0..nsteps).  Returns #partials.
 static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
-                               const Gather& gth, cudaStream_t st, int* nparts) {
-    TrainArgs ta;
+                               const Gather& gth, cudaStream_t st, int* nparts, uint32_t nsteps = 0,
+                               float* d_losses = nullptr) {
+    TrainArgs ta{};
     ta.rec = reinterpret_cast<const float*>(d_rec);
     ta.tgt = d_tgt;
     ta.n = n;
@@ -361,20 +426,51 @@ static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const flo
     ta.partials = h->d_partials();
     ta.loss_part = h->d_loss_part();
     ta.bad_targets = h->d_counters() + 1;
+    ta.dbg = h->dbg;
     const uint32_t ntiles = (n + kTile - 1) / kTile;
     int grid = int(ntiles);
     const int cap = h->num_sms < kMaxPartials ? h->num_sms : kMaxPartials;
     if (grid > cap) grid = cap;
-    nrc_train_kernel<<<grid, 128, kTrainSmemBytes, st>>>(ta);
-    NRC_LAUNCHED(h, "nrc_train_kernel");
     *nparts = grid;
+    if (nsteps == 0) {
+        ta.fused = 0;
+        ta.nsteps = 1;
+        NRC_CUDA(h, launch_pdl(nrc_train_kernel, dim3(grid), dim3(kTrainBlock), kTrainSmemBytes, st, ta));
+        NRC_LAUNCHED(h, "nrc_train_kernel");
+        return NRC_OK;
+    }
+    const nrc_config& c = h->cfg;
+    ta.fused = 1;
+    ta.nsteps = nsteps;
+    ta.inv_n = float(1.0 / double(n));
+    ta.lr = c.learning_rate;
+    ta.b1 = c.adam_beta1;
+    ta.b2 = c.adam_beta2;
+    ta.adam_eps = c.adam_eps;
+    for (uint32_t k = 0; k < nsteps; ++k) ta.coef[k] = step_coef(c, h->step + 1 + k);
+    ta.w = h->d_w();
+    ta.m = h->d_m();
+    ta.v = h->d_v();
+    ta.ema = h->d_ema();
+    ta.wimg_out = h->d_wimg();
+    ta.eimg = h->d_eimg();
+    ta.bad_grads = h->d_counters() + 0;
+    ta.losses = d_losses;
+    ta.gbar = h->d_counters() + 2;
+    ta.gbar_base = h->gbar;
+    if (h->coop)
+        NRC_CUDA(h, launch_coop(nrc_train_kernel, dim3(grid), dim3(kTrainBlock), kTrainSmemBytes, st, ta));
+    else
+        nrc_train_kernel<<<grid, kTrainBlock, kTrainSmemBytes, st>>>(ta);
+    NRC_LAUNCHED(h, "nrc_train_kernel");
+    h->gbar += 2ull * nsteps * uint64_t(grid);
+    h->step += nsteps;
     return NRC_OK;
 }
 
 static AdamArgs adam_args(nrc_handle* h) {
     AdamArgs aa{};
     const nrc_config& c = h->cfg;
-    const uint64_t t = h->step;  // already incremented
     aa.w = h->d_w();
     aa.m = h->d_m();
     aa.v = h->d_v();
@@ -385,44 +481,19 @@ static AdamArgs adam_args(nrc_handle* h) {
     aa.b1 = c.adam_beta1;
     aa.b2 = c.adam_beta2;
     aa.eps = c.adam_eps;
-    aa.inv_bc1 = float(1.0 / (1.0 - std::pow(double(c.adam_beta1), double(t))));
-    aa.inv_bc2 = float(1.0 / (1.0 - std::pow(double(c.adam_beta2), double(t))));
-    // Eq.(2): eta_t = 1 - a^t.  R12: W-bar = [(1-a) W + a eta_{t-1} W-bar] / eta_t
-    const double al = c.ema_alpha;
-    const double eta_t = 1.0 - std::pow(al, double(t));
-    const double eta_p = 1.0 - std::pow(al, double(t - 1));
-    if (al == 0.0) {
-        aa.ema_c1 = 1.0f;
-        aa.ema_c2 = 0.0f;
-    } else if (c.flags & NRC_EMA_PRINTED_FORM) {
-        aa.ema_c1 = float((1.0 - al) / eta_t);
-        aa.ema_c2 = float(al * eta_p);
-    } else {
-        aa.ema_c1 = float((1.0 - al) / eta_t);
-        aa.ema_c2 = float(al * eta_p / eta_t);
-    }
+    const StepCoef k = step_coef(c, h->step);  // already incremented
+    aa.inv_bc1 = k.inv_bc1;
+    aa.inv_bc2 = k.inv_bc2;
+    aa.ema_c1 = k.ema_c1;
+    aa.ema_c2 = k.ema_c2;
     aa.bad_grads = h->d_counters() + 0;
     return aa;
 }
 
 static nrc_status train_step_impl(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
-                                  const Gather& gth, float* d_loss, cudaStream_t st) {
+                                  const Gather& gth, float* d_losses, uint32_t nsteps, cudaStream_t st) {
     int np = 0;
-    nrc_status s = launch_train(h, d_rec, d_tgt, n, gth, st, &np);
-    if (s != NRC_OK) return s;
-    h->step += 1;
-    AdamArgs aa = adam_args(h);
-    aa.src = h->d_partials();
-    aa.nsrc = np;
-    aa.src_logical = 0;
-    aa.inv_n = float(1.0 / double(n));
-    aa.loss_part = h->d_loss_part();
-    aa.nloss = np;
-    aa.loss_scale = float(1.0 / double(n));
-    aa.loss_out = d_loss;
-    nrc_adam_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(aa);
-    NRC_LAUNCHED(h, "nrc_adam_kernel");
-    return NRC_OK;
+    return launch_train(h, d_rec, d_tgt, n, gth, st, &np, nsteps, d_losses);
 }
 
 static nrc_status check_train_args(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint64_t n,
@@ -442,7 +513,7 @@ nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d
     if ((s = check_train_args(h, d_rec, d_tgt, n, "nrc_train_step")) != NRC_OK) return s;
     if (d_loss && !aligned(d_loss, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "misaligned d_loss");
     Gather g{false, 0, 0, 0, 0, 0};
-    return train_step_impl(h, d_rec, d_tgt, n, g, d_loss, static_cast<cudaStream_t>(stream));
+    return train_step_impl(h, d_rec, d_tgt, n, g, d_loss, 1, static_cast<cudaStream_t>(stream));
 }
 
 nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_local,
@@ -527,9 +598,11 @@ nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* 
     nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint32_t total = 0;
-    for (uint32_t j = 0; j < s_; ++j) {
+    for (uint32_t j = 0; j < s_; j += kMaxFusedSteps) {  // one launch per <= 8 steps
+        const uint32_t k = (s_ - j) < uint32_t(kMaxFusedSteps) ? (s_ - j) : uint32_t(kMaxFusedSteps);
         g.offset = uint64_t(j) * l;
-        if ((s = train_step_impl(h, d_rec, d_tgt, l, g, d_losses ? d_losses + j : nullptr, st)) != NRC_OK) return s;
+        if ((s = train_step_impl(h, d_rec, d_tgt, l, g, d_losses ? d_losses + j : nullptr, k, st)) != NRC_OK)
+            return s;
         total += h->launches;
         h->launches = 0;
     }
@@ -652,6 +725,14 @@ nrc_status nrc_frame_host(nrc_handle* h, const nrc_record* h_query, uint64_t n_q
     if (n_query) NRC_CUDA(h, cudaMemcpyAsync(h_rgb, drgb, n_query * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
     if (h_losses && s_) NRC_CUDA(h, cudaMemcpyAsync(h_losses, dloss, s_ * sizeof(float), cudaMemcpyDeviceToHost, st));
     h->launches = launches;
+    return NRC_OK;
+}
+
+// Undocumented diagnostic hook (not part of nrc.h): a device buffer of >= 64
+// int64 receives clock64 phase timestamps of the train kernel's CTA 0.
+nrc_status nrc_debug_set_trace(nrc_handle* h, long long* d_buf) {
+    if (!h) return NRC_ERR_STATE;
+    h->dbg = d_buf;
     return NRC_OK;
 }
 

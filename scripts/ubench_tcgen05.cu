@@ -48,6 +48,21 @@ __global__ void __launch_bounds__(128, 1) ubench(int mode, int iters, long long*
             phase ^= 1;
             continue;
         }
+        if (mode == 7 || mode == 8 || mode == 9) {  // backward shapes
+            if (tid == 0) {
+                tc_fence_after();
+                if (mode != 8)  // dgrad: M128 N64 K64, A K-major, B MN-major
+                    for (int k = 0; k < 4; ++k)
+                        umma_f16(tb, desc_kmajor(a, k), desc_mnmajor(b, k), make_idesc(128, 64, 0, 1), k > 0);
+                if (mode != 7)  // wgrad: M64 N64 K128, A and B MN-major
+                    for (int k = 0; k < 8; ++k)
+                        umma_f16(tb + 64, desc_mnmajor(a, k), desc_mnmajor(b, k), make_idesc(64, 64, 1, 1), k > 0);
+                umma_commit(&bar);
+            }
+            mbar_wait(&bar, phase);
+            phase ^= 1;
+            continue;
+        }
         if (tid == 0) {
             tc_fence_after();
             if (mode == 1 || mode == 4) {
@@ -93,8 +108,9 @@ int main() {
     cudaMalloc(&d, 8);
     const char* names[] = {"mma SS + commit + wait", "mma TS + commit + wait", "round: SS mma + epi(smem)",
                            "round: SS mma + epi(smem) [same]", "round: TS mma + epi(tmem st)",
-                           "16 layers back-to-back (per 16)", "SS mma + wait + syncthreads"};
-    for (int mode = 0; mode < 7; ++mode) {
+                           "16 layers back-to-back (per 16)", "SS mma + wait + syncthreads",
+                           "dgrad M128N64K64 (B MN-major)", "wgrad M64N64K128 (A,B MN-major)", "dgrad + wgrad"};
+    for (int mode = 0; mode < 10; ++mode) {
         ubench<<<1, 128>>>(mode, 2000, d);
         long long c = 0;
         cudaError_t e = cudaDeviceSynchronize();
