@@ -131,6 +131,28 @@ def oracle_frame_estimate(q_sample: int, t_sample: int, reps: int = 1):
     return ms, sample, tq, tt
 
 
+def frame_config(world: int) -> dict:
+    return {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
+            "parallelism": f"dp{world}" if world > 1 else "single",
+            "l2": "flushed (256 MB write) between timed steps"}
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from the newest committed
+    ncu --set full capture summary (profiles/rNN_traffic.json), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        try:
+            with open(f) as fh:
+                t = json.load(fh)
+            if kernel in t:
+                return float(t[kernel]["traffic_bytes"]), os.path.relpath(f, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def omp_threads():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
@@ -150,9 +172,10 @@ def run_reference(args):
     ms = float(np.mean(times))
     line = {
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (nrc_inputs seeded records)",
-        "config": {"workload": CONFIG_NAME + " (oracle, sampled)"},
+        "config": frame_config(args.gpus),
         "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": omp_threads(), "kind": "oracle", "sample": sample},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -184,8 +207,7 @@ def run_nrc(args):
             dist.barrier()
 
     # ---- inputs (synthetic, resident in HBM before timing)
-    q0 = rank * N_QUERY // world
-    q1 = (rank + 1) * N_QUERY // world
+    q0, q1 = nrc.shard(N_QUERY, rank, world)
     recs_q_all = nrc_inputs.records(N_QUERY, seed=nrc_inputs.SEED_QUERY)
     recs_q = torch.from_numpy(recs_q_all[q0:q1].copy()).to(dev)
     nq_local = q1 - q0
@@ -198,10 +220,8 @@ def run_nrc(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    # data-parallel pieces for world > 1
-    grad = torch.zeros(nrc.NPARAM, dtype=torch.float32, device=dev)
-    loss_sum = torch.zeros(1, dtype=torch.float32, device=dev)
-    row_lo, row_hi = rank * TRAIN_L // world, (rank + 1) * TRAIN_L // world
+    # data-parallel frame for world > 1 (query rows sharded, one all-reduce per train step)
+    dpf = nrc.DataParallelFrame(cache, device=dev) if world > 1 else None
 
     q_start = torch.cuda.Event(enable_timing=True)
     q_end = torch.cuda.Event(enable_timing=True)
@@ -220,13 +240,9 @@ def run_nrc(args):
             cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
             launches += cache.last_launch_count
         else:
-            for j in range(TRAIN_S):
-                # this rank's rows of shuffled batch j, gathered in-kernel
-                cache.train_frame_backward(d_r, d_t, TRAIN_L, 1000 + fi % 2, j, row_lo, row_hi, grad, loss_sum)
-                launches += cache.last_launch_count
-                dist.all_reduce(grad)
-                cache.train_apply(grad, TRAIN_L)
-                launches += cache.last_launch_count
+            # this rank's rows of every shuffled batch, gathered in-kernel
+            dpf.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
+            launches += dpf.last_launch_count
         return launches
 
     for i in range(args.warmup):
@@ -285,20 +301,21 @@ def run_nrc(args):
                "note": "nrc_frame_host: pinned host records -> device, query + 4 train steps, RGB + losses -> host"}
 
     peak_tf, peak_bw, peak_src = peaks()
+    traffic, traffic_src = ncu_traffic("nrc_query_kernel")
     q_flops = FLOP_QUERY * nq_local
     achieved = q_flops / (q_ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 Adam/EMA)", "data": "synthetic (nrc_inputs)",
-        "config": {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
-                   "parallelism": f"dp{world}" if world > 1 else "single",
-                   "l2": "flushed (256 MB write) between timed steps"},
+        "config": frame_config(world),
         "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
         "query_ms": q_ms, "train_ms": ms - q_ms,
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "nrc_query_kernel", "achieved": achieved, "peak": peak_tf,
-                     "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic, "traffic_unit": "bytes/launch",
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes": BYTES_QUERY * nq_local,
                      "peak_source": f"{peak_src} bf16 dense burst (fp16 same rate)",
                      "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_local} queries"},
         "clocks": clk.summary(),

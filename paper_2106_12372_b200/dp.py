@@ -1,0 +1,89 @@
+"""Multi-GPU partitioning of the NRC frame.
+
+One process per GPU.  Queries are independent rows: rank k of P
+takes rows [k N / P, (k + 1) N / P) and nothing is exchanged.  Training is
+data-parallel: every rank holds the full 20,672-parameter state, computes the
+un-normalised gradient sum over its l / P rows of each LCG-shuffled batch
+ with nrc_train_frame_backward, one all-reduce (SUM) of
+[gradient | loss sum] per step, then identical Adam + EMA on every rank
+(nrc_train_apply with n_global = l).  The result equals the single-GPU step up
+to the fp32 summation order of the gradient.
+
+This module is host orchestration only: every arithmetic step runs in the
+cache's CUDA kernels (or, in the CPU tests, in a test-side stand-in).
+"""
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .nrc import NPARAM
+
+
+def shard(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Rows [lo, hi) of n owned by `rank` of `world` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    return rank * n // world, (rank + 1) * n // world
+
+
+def frame_batches(n_total: int, s: int, l: int) -> Tuple[int, int]:
+    """(s, l) actually trained on: batches shrink proportionally when the frame
+    has fewer than s * l records, as nrc_train_frame does."""
+    if n_total == 0 or s == 0 or l == 0:
+        return 0, 0
+    if s * l > n_total:
+        l = n_total // s
+    return (s, l) if l > 0 else (0, 0)
+
+
+class DataParallelFrame:
+    """The N > 1 frame: sharded query + data-parallel training.
+
+    `cache` provides query / train_frame_backward / train_apply with the
+    signatures of paper_2106_12372_b200.RadianceCache.  `group` is the
+    process group (NCCL on GPUs; gloo in the CPU tests)."""
+
+    def __init__(self, cache, group: Optional[dist.ProcessGroup] = None, device=None,
+                 dtype: torch.dtype = torch.float32):
+        self.cache = cache
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device if device is not None else torch.device("cpu")
+        # one buffer so that gradient and loss travel in a single all-reduce
+        self.buf = torch.zeros(NPARAM + 1, dtype=dtype, device=self.device)
+        self.grad = self.buf[:NPARAM]
+        self.loss_sum = self.buf[NPARAM:]
+        self.last_launch_count = 0
+
+    def query_rows(self, n: int) -> Tuple[int, int]:
+        return shard(n, self.rank, self.world)
+
+    def query(self, records_local: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """This rank's rows of the frame's query (no communication)."""
+        return self.cache.query(records_local, out, stream=stream)
+
+    def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
+                    losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+        """All s steps of the frame's training on the full (replicated) record
+        set; each rank gathers only its rows of every shuffled batch."""
+        n_total = int(records.shape[0])
+        s, l = frame_batches(n_total, s, l)
+        launches = 0
+        if s == 0:
+            self.last_launch_count = 0
+            return losses
+        lo, hi = shard(l, self.rank, self.world)
+        for j in range(s):
+            self.cache.train_frame_backward(records, targets, l, shuffle_seed, j, lo, hi, self.grad, self.loss_sum)
+            launches += getattr(self.cache, "last_launch_count", 0)
+            dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=self.group)
+            self.cache.train_apply(self.grad, l)
+            launches += getattr(self.cache, "last_launch_count", 0)
+            if losses is not None:
+                losses[j] = self.loss_sum[0] / l
+        self.last_launch_count = launches
+        return losses

@@ -1,0 +1,120 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the N > 1 partitioning in
+paper_2106_12372_b200.dp: query row shards, per-rank rows of each LCG-shuffled
+batch, one all-reduce of [gradient | loss] per step, identical Adam + EMA on
+every rank.  The per-rank compute is a test-side stand-in built on the fp64
+oracle (no GPU here); what is under test is the orchestration the bench runs
+for N > 1, against single-process oracle training on the gathered batches
+(P:L487-491 shuffle into s batches of l; Adam P:L896-902; EMA Eq. 2)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import nrc_inputs
+import oracle
+from paper_2106_12372_b200 import dp
+
+
+def test_shard_partition():
+    for n in [0, 1, 2, 7, 1000, 16384, 2073600]:
+        for world in [1, 2, 3, 4, 8]:
+            spans = [dp.shard(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+                assert a1 == b0
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        dp.shard(10, 2, 2)
+
+
+def test_frame_batches_shrink():
+    assert dp.frame_batches(65536, 4, 16384) == (4, 16384)
+    assert dp.frame_batches(65535, 4, 16384) == (4, 16383)  # batches shrink proportionally
+    assert dp.frame_batches(3, 4, 16384) == (0, 0)
+    assert dp.frame_batches(0, 4, 16384) == (0, 0)
+
+
+class OracleShard:
+    """Test stand-in for RadianceCache's data-parallel calls, on the oracle."""
+
+    def __init__(self, seed):
+        self.oc = oracle.OracleCache(seed=seed)
+
+    def train_frame_backward(self, records, targets, l, seed, j, lo, hi, grad, loss_sum):
+        recs, tg = records.numpy(), targets.numpy()
+        a, c, m = oracle.lcg_params(recs.shape[0], seed)
+        perm = oracle.lcg_permute(recs.shape[0], a, c, m).astype(np.int64)
+        idx = perm[j * l + lo: j * l + hi]
+        G, ls, _ = oracle.grad_batch(self.oc.w, recs[idx], tg[idx])
+        grad.copy_(torch.from_numpy(G))
+        loss_sum[0] = ls
+
+    def train_apply(self, grad_sum, n):
+        oc = self.oc
+        oc.t += 1
+        oracle.adam(oc.w, oc.m, oc.v, grad_sum.numpy().astype(np.float64) / n, oc.t)
+        oracle.ema(oc.wbar, oc.w, oc.t)
+
+    def query(self, records, out, stream=None):
+        out.copy_(torch.from_numpy(self.oc.query(records.numpy())))
+        return out
+
+
+N_TOTAL, S, L, SEED = 3 * 1001 + 5, 3, 1001, 77
+
+
+def _worker(rank, world, port, out_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        recs, tgts = nrc_inputs.train_frame(0, n=N_TOTAL, noise=0.3)
+        shard_cache = OracleShard(seed=5)
+        frame = dp.DataParallelFrame(shard_cache, dtype=torch.float64)
+        losses = torch.zeros(S, dtype=torch.float64)
+        frame.train_frame(torch.from_numpy(recs), torch.from_numpy(tgts), S, L, SEED, losses)
+        q = nrc_inputs.records(999, seed=nrc_inputs.SEED_QUERY)
+        q0, q1 = frame.query_rows(q.shape[0])
+        rgb = torch.zeros((q1 - q0, 3), dtype=torch.float64)
+        frame.query(torch.from_numpy(q[q0:q1].copy()), rgb)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), w=shard_cache.oc.w, wbar=shard_cache.oc.wbar,
+                 losses=losses.numpy(), rgb=rgb.numpy(), q0=q0, q1=q1)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_data_parallel_frame_equals_single_process(tmp_path):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    res = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    # single process: s oracle steps on the gathered batches
+    recs, tgts = nrc_inputs.train_frame(0, n=N_TOTAL, noise=0.3)
+    a, c, m = oracle.lcg_params(N_TOTAL, SEED)
+    perm = oracle.lcg_permute(N_TOTAL, a, c, m).astype(np.int64)
+    ref = oracle.OracleCache(seed=5)
+    ref_losses = []
+    for j in range(S):
+        idx = perm[j * L:(j + 1) * L]
+        ref_losses.append(ref.train_step(recs[idx], tgts[idx]))
+    for r in res:
+        # identical state on every rank, equal to the single-process result up to
+        # fp64 summation order of the two shard gradients
+        np.testing.assert_allclose(r["w"], ref.w, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(r["wbar"], ref.wbar, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(r["losses"], ref_losses, rtol=1e-12)
+    np.testing.assert_array_equal(res[0]["w"], res[1]["w"])
+    # query shards tile the batch and match the unsharded query
+    q = nrc_inputs.records(999, seed=nrc_inputs.SEED_QUERY)
+    assert int(res[0]["q0"]) == 0 and int(res[0]["q1"]) == int(res[1]["q0"]) and int(res[1]["q1"]) == 999
+    full = ref.query(q)
+    got = np.concatenate([res[0]["rgb"], res[1]["rgb"]])
+    np.testing.assert_allclose(got, full, rtol=1e-9, atol=1e-12)

@@ -1,0 +1,61 @@
+"""The N > 1 data-parallel path (paper_2106_12372_b200.dp) on one GPU with a
+world-size-1 NCCL group: the all-reduce is the identity, so the frame trained
+through nrc_train_frame_backward + all-reduce + nrc_train_apply must agree
+with the fused nrc_train_frame (same gradient up to fp32 summation order) and
+with the fp64 oracle on the gathered batches."""
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import nrc_inputs
+from parity import TOL_RADIANCE, radiance_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def group():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    yield None
+    dist.destroy_process_group()
+
+
+def test_dp_frame_world1_matches_fused_frame_and_oracle(group, orc):
+    import paper_2106_12372_b200 as nrc
+    n, s, l, seed = 8192 + 3, 4, 2048, 21
+    recs, tg = nrc_inputs.train_frame(2, n=n, noise=0.3)
+    d_r = torch.from_numpy(recs).cuda()
+    d_t = torch.from_numpy(tg).cuda()
+    fused = nrc.RadianceCache()
+    lf = fused.train_frame(d_r, d_t, s, l, seed).cpu().numpy()
+    cache = nrc.RadianceCache()
+    frame = nrc.DataParallelFrame(cache, device=torch.device("cuda", 0))
+    ld = torch.zeros(s, dtype=torch.float32, device="cuda")
+    frame.train_frame(d_r, d_t, s, l, seed, ld)
+    ld = ld.cpu().numpy()
+    assert frame.last_launch_count == 3 * s  # train + reduce, adam per step
+    np.testing.assert_allclose(ld, lf, rtol=1e-4)
+    q = torch.from_numpy(nrc_inputs.records(4096, seed=3)).cuda()
+    assert max(radiance_err(cache.query(q).cpu().numpy(), fused.query(q).cpu().numpy())) <= TOL_RADIANCE
+    # oracle on the gathered batches: per-step losses (C3 criterion) and radiance
+    pa, pc, pm = orc.lcg_params(n, seed)
+    perm = orc.lcg_permute(n, pa, pc, pm).astype(np.int64)
+    ref = orc.OracleCache(W32=nrc.RadianceCache().get_params("train"))
+    lo = []
+    for j in range(s):
+        idx = perm[j * l:(j + 1) * l]
+        lo.append(ref.train_step(recs[idx], tg[idx]))
+    np.testing.assert_allclose(ld, lo, rtol=1e-2)
+    assert max(radiance_err(cache.query(q).cpu().numpy(), ref.query(q.cpu().numpy()))) <= TOL_RADIANCE
