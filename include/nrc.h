@@ -135,7 +135,11 @@ nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* 
 /* One optimisation step on a batch: forward, relative
  * L2 loss (Eq. 5) of the factored prediction, backward, Adam on the batch-
  * mean gradient, EMA update.  d_rec: n records; d_tgt: 3n fp32 targets;
- * d_loss (optional, 1 fp32): the batch-mean loss.  n <= max_batch. */
+ * d_loss (optional, 1 fp32): the batch-mean loss.  n <= max_batch.  One
+ * cooperative kernel launch (the fused train kernel with its in-kernel
+ * reduction + Adam + EMA); it occupies up to min(#SMs, ceil(n/128)) SMs and
+ * must not share the device with a concurrently running kernel that holds
+ * them (the launch fails with NRC_ERR_CUDA if co-residency is impossible). */
 nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n, float* d_loss,
                           void* stream);
 
@@ -155,7 +159,8 @@ nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_gl
  * s disjoint batches of l records (P:L350 footnote); batch j is records
  * perm(j*l + k), k < l, gathered inside the kernel (nothing materialised).
  * If s*l > n_total, l shrinks to n_total / s.  d_losses: s fp32
- * (optional).  Equivalent to s nrc_train_step calls on the gathered batches. */
+ * (optional).  Equivalent (bitwise) to s nrc_train_step calls on the
+ * gathered batches; runs as one cooperative launch per 8 steps. */
 nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s,
                            uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream);
 
