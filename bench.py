@@ -301,7 +301,7 @@ def run_nrc(args):
                "note": "nrc_frame_host: pinned host records -> device, query + 4 train steps, RGB + losses -> host"}
 
     peak_tf, peak_bw, peak_src = peaks()
-    traffic, traffic_src = ncu_traffic("nrc_query_kernel")
+    traffic, traffic_src = ncu_traffic("nrc_query_ts_kernel")
     q_flops = FLOP_QUERY * nq_local
     achieved = q_flops / (q_ms * 1e-3) / 1e12
     line = {
@@ -312,7 +312,7 @@ def run_nrc(args):
         "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
         "query_ms": q_ms, "train_ms": ms - q_ms,
         "gpu_launches": launches,
-        "roofline": {"bound": "tensor", "kernel": "nrc_query_kernel", "achieved": achieved, "peak": peak_tf,
+        "roofline": {"bound": "tensor", "kernel": "nrc_query_ts_kernel", "achieved": achieved, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic, "traffic_unit": "bytes/launch",
                      "traffic_source": traffic_src,
                      "algorithmic_bytes": BYTES_QUERY * nq_local,

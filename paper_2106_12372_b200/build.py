@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnrc.so")
 SOURCES = ["nrc_api.cu"]
-DEPS = ["nrc_api.cu", "nrc_kernels.cuh", "nrc_fused_query.cuh", "nrc_train.cuh", "nrc_device.cuh"]
+DEPS = ["nrc_api.cu", "nrc_kernels.cuh", "nrc_fused_query.cuh", "nrc_query_ts.cuh", "nrc_train.cuh", "nrc_device.cuh"]
 
 
 def nvcc() -> str:
@@ -35,6 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xcompiler", "-fPIC", "-shared", "-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    # diagnostics builds only, e.g. NRC_NVCC_DEFINES=NRC_TRACE_QUERY
+    cmd += ["-D" + d for d in os.environ.get("NRC_NVCC_DEFINES", "").split()]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)

@@ -35,9 +35,24 @@ struct QueryLauncher {
         nrc_query_kernel<G, S><<<grid, 128 * G, query_smem_bytes<G, S>(), st>>>(qa);
     }
 };
+template <int G, int S>
+struct QueryLauncherTS {
+    static cudaError_t set_smem() {
+        return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    query_ts_smem_bytes<G, S>());
+    }
+    static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
+        nrc_query_ts_kernel<G, S><<<grid, 128 * G, query_ts_smem_bytes<G, S>(), st>>>(qa);
+    }
+};
 #define NRC_QCFG(G, S) {&QueryLauncher<G, S>::set_smem, &QueryLauncher<G, S>::launch, G}
-const QueryEntry kQueryCfgs[] = {NRC_QCFG(4, 2), NRC_QCFG(3, 2), NRC_QCFG(2, 4)};
+#define NRC_QCFG_TS(G, S) {&QueryLauncherTS<G, S>::set_smem, &QueryLauncherTS<G, S>::launch, G}
+// Entry 0 (activations in TMEM, 5 groups x 1 tile) is the default; the
+// shared-memory-activation variants are kept for comparison.
+const QueryEntry kQueryCfgs[] = {NRC_QCFG_TS(5, 1), NRC_QCFG(4, 2), NRC_QCFG(3, 2), NRC_QCFG(2, 4),
+                                 NRC_QCFG(6, 1),    NRC_QCFG_TS(2, 2), NRC_QCFG_TS(1, 5)};
 #undef NRC_QCFG
+#undef NRC_QCFG_TS
 constexpr int kNumQueryCfgs = int(sizeof(kQueryCfgs) / sizeof(kQueryCfgs[0]));
 constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
 
@@ -366,6 +381,7 @@ nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* 
     qa.wimg = raw ? h->d_wimg() : h->d_eimg();
     qa.ep = h->ep;
     qa.flags = h->cfg.flags & (NRC_FACTORIZE | NRC_CLAMP_QUERY);
+    qa.dbg = h->dbg;
     const uint64_t ntiles = (n + kTile - 1) / kTile;
     const uint64_t G = uint64_t(kQueryCfgs[h->query_cfg].groups);
     const uint64_t ctas = (ntiles + G - 1) / G;  // one tile stream per group

@@ -141,6 +141,84 @@ __device__ __forceinline__ void umma_f16_ta(uint32_t d_tmem, uint32_t a_tmem, ui
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// One lane of a converged warp (elect.sync).  Issuing tcgen05.mma from an
+// elected lane of a converged warp, with operands made warp-uniform by
+// __shfl_sync, lets ptxas keep the descriptors in uniform registers: ~170
+// cycles for a 4-MMA chain + commit instead of ~650 from a lone divergent
+// thread (scripts/ubench_tcgen05.cu modes 10/17).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p = 0;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n}" : "=r"(p));
+    return p != 0;
+}
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
+__device__ __forceinline__ uint64_t warp_uniform(uint64_t x) {
+    const uint32_t lo = __shfl_sync(0xffffffffu, uint32_t(x), 0), hi = __shfl_sync(0xffffffffu, uint32_t(x >> 32), 0);
+    return (uint64_t(hi) << 32) | lo;
+}
+// K chains of 4 or 8 MMAs with both operands in shared memory; operand
+// descriptors advance by ASTEP / BSTEP (16-byte units) per K=16 step.  The
+// first MMA accumulates iff acc0 != 0.  Issue from an elected lane of a
+// converged warp (see elect_one), then umma_commit from the same lane.
+template <int ASTEP, int BSTEP>
+__device__ __forceinline__ void umma_ss4(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "add.u64 a1, %1, %5;\n\tadd.u64 a2, %1, %6;\n\tadd.u64 a3, %1, %7;\n\t"
+        "add.u64 b1, %2, %8;\n\tadd.u64 b2, %2, %9;\n\tadd.u64 b3, %2, %10;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc0), "n"(ASTEP), "n"(2 * ASTEP), "n"(3 * ASTEP), "n"(BSTEP),
+        "n"(2 * BSTEP), "n"(3 * BSTEP)
+        : "memory");
+}
+template <int ASTEP, int BSTEP>
+__device__ __forceinline__ void umma_ss8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+    umma_ss4<ASTEP, BSTEP>(d_tmem, a, b, idesc, acc0);
+    umma_ss4<ASTEP, BSTEP>(d_tmem, a + 4 * ASTEP, b + 4 * BSTEP, idesc, 1u);
+}
+// descriptor K-step increments (16-byte units): K-major +32 B, MN-major +2048 B
+constexpr int kKmajStep = 2, kMNmajStep = 128;
+
+// One 64-deep K chain (4 x K=16) with A in TMEM and B a K-major SWIZZLE_128B
+// smem tile, then a commit to `bar`, in ONE asm block: the K steps are
+// a + 8 columns and b_desc + 2 (32 B) computed inside, so ptxas materialises
+// the uniform operands once instead of re-broadcasting six registers per MMA
+// (each re-broadcast waits for the previous tcgen05.mma to read its operands).
+__device__ __forceinline__ void umma_chain4_ta_commit(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                      uint32_t idesc, uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred f, t;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+        "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+        "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, f;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n\t"
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(smem_u32(bar))
+        : "memory");
+}
+// Same with A a K-major SWIZZLE_128B smem tile.
+__device__ __forceinline__ void umma_chain4_ss_commit(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                      uint32_t idesc, uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred f, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t"
+        "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t"
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(smem_u32(bar))
+        : "memory");
+}
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread
 // have completed (implies tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -211,6 +289,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// 16 consecutive columns, no wait (pair with tmem_wait_st before the data is used)
+__device__ __forceinline__ void tmem_st16_nowait(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        NRC_S8(0), NRC_S8(8)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 #undef NRC_S8
 #undef NRC_R8
 #undef NRC_W8

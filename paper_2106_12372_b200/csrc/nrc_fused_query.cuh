@@ -26,6 +26,7 @@ struct QueryArgs {
     const uint8_t* wimg; // fp16 operand image (43,008 B), EMA or raw
     EncodeParams ep;
     uint32_t flags;      // NRC_FACTORIZE | NRC_CLAMP_QUERY
+    long long* dbg;      // per-round clock64 trace (builds with -DNRC_TRACE_QUERY only), else unused
 };
 
 constexpr int kRecTileBytes = kTile * kRecFloats * 4;  // 8 KB of records per tile

@@ -12,6 +12,7 @@
 #pragma once
 #include "nrc_device.cuh"
 #include "nrc_fused_query.cuh"
+#include "nrc_query_ts.cuh"
 #include "nrc_train.cuh"
 
 namespace nrc {

@@ -1,0 +1,237 @@
+// nrc_query_ts.cuh -- fused cache query with the activations in TMEM
+// (rows a1-a3 of SURVEY 8(a)).
+//
+// Why: with the A operand in shared memory, every 128-row layer moves
+// 40 KB through the SM's shared-memory port (MMA reads A 16 KB + W 8 KB, the
+// epilogue writes A 16 KB), ~250 KB per tile, which bounds the SMEM variant
+// (nrc_fused_query.cuh) at ~2k cycles per tile.  Here the encoder and the
+// ReLU epilogue write the fp16 activations straight into tensor memory
+// (tcgen05.st) and the MMA reads A from TMEM (".kind::f16 [d], [a], b_desc"),
+// so shared memory only feeds the 8 KB weight tile per layer.
+//
+// TMEM per in-flight tile: fp32 accumulator D (64 columns) + fp16 A
+// (128 rows x 64 halves = 32 columns) -> 5 tiles per SM in 480 of 512
+// columns.  Layer L reads A at column a and writes D; its epilogue reads D
+// and writes the next A over the dead A (same columns).
+#pragma once
+#include "nrc_fused_query.cuh"
+
+namespace nrc {
+
+constexpr int kTsMaxSlots = 5;
+
+template <int G, int S>
+__host__ __device__ constexpr int query_ts_smem_bytes() {
+    return 1024 + kImgBytes + G * kRecTileBytes + 8 * (1 + (S + 1) * G) + 16;
+}
+
+// G independent 4-warp groups, S tiles in flight per group (G*S <= 5).
+template <int G, int S>
+__global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args) {
+    static_assert(G * S <= kTsMaxSlots, "TMEM holds 5 tiles");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    const uint32_t tid = threadIdx.x;
+    const uint32_t g = tid >> 7, r = tid & 127, warp = tid >> 5, wq = warp & 3;
+    // the group's MMA / TMA issuer: warp g % 4 of the group (an elected lane
+    // issues), so the issuers of the groups sit on different SM sub-partitions
+    const bool issuer_warp = wq == (g & 3u);
+    const bool issuer = r == 32u * (g & 3u);
+    uint8_t* sW = smem;
+    const float* sRec = reinterpret_cast<const float*>(smem + kImgBytes + g * kRecTileBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImgBytes + G * kRecTileBytes);
+    uint64_t* wbar = &bars[0];
+    uint64_t* mma_bar = &bars[1 + (S + 1) * g];  // [S]
+    uint64_t* rec_bar = &bars[1 + (S + 1) * g + S];
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + (S + 1) * G);
+
+    if (tid == 0) {
+        for (int i = 0; i < 1 + (S + 1) * G; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(tmem_slot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (tid == 0) {
+        mbar_arrive_expect_tx(wbar, kImgBytes);
+        bulk_g2s(sW, args.wimg, kImgBytes, wbar);
+    }
+
+    const uint64_t n = args.n;
+    const uint64_t ntiles = (n + kTile - 1) / kTile;
+    const uint64_t q0 = uint64_t(blockIdx.x) * G + g;  // this group's k-th tile is q0 + k * Q
+    const uint64_t Q = uint64_t(gridDim.x) * G;
+    uint64_t k_next = 0;
+    uint32_t rec_phase = 0;
+
+    auto issue_records = [&](uint64_t t) {
+        const uint64_t row0 = t * kTile;
+        const uint64_t nv = (n - row0) < uint64_t(kTile) ? (n - row0) : uint64_t(kTile);
+        const uint32_t bytes = uint32_t(nv) * kRecFloats * 4;
+        mbar_arrive_expect_tx(rec_bar, bytes);
+        bulk_g2s(const_cast<float*>(sRec), args.rec + row0 * kRecFloats, bytes, rec_bar);
+    };
+    if (issuer && q0 < ntiles) issue_records(q0);
+    mbar_wait(wbar, 0);
+
+    const uint32_t sW_a = smem_u32(sW);
+    const uint32_t lane_off = (wq * 32u) << 16;
+    auto d_col = [&](int s) -> uint32_t { return tmem_base + 64u * uint32_t(g * S + s); };
+    auto a_col = [&](int s) -> uint32_t { return tmem_base + 320u + 32u * uint32_t(g * S + s); };
+    // called by the whole issuer warp (converged)
+    auto issue_layer = [&](int s, int L) {
+        const uint32_t wl = sW_a + layer_off(L) * 2;
+        const uint32_t idesc = (L < 5) ? make_idesc(128, 64, 0, 0) : make_idesc(128, 16, 0, 0);
+        const uint32_t d = warp_uniform(d_col(s)), a = warp_uniform(a_col(s));
+        const uint64_t b = warp_uniform(desc_kmajor(wl, 0));
+        tc_fence_after();
+        if (elect_one()) umma_chain4_ta_commit(d, a, b, idesc, &mma_bar[s]);
+        __syncwarp();
+    };
+
+#ifdef NRC_TRACE_QUERY
+    // dbg[4096 + 8 (4 k + wq) + f] for the k-th round of CTA 0 group 0; f: 0 before
+    // the MMA wait, 1 MMA done, 2 epilogue done, 4 slot*16+layer, 5 encode start,
+    // 6 encode done; dbg[4096 + 3072 + 2k (+1)]: issue start / end
+    uint32_t kr = 0;
+    const bool trc = args.dbg != nullptr && blockIdx.x == 0 && g == 0 && (tid & 31) == 0;
+#define TQ(f) \
+    if (trc && kr < 96) args.dbg[4096 + 8 * (4 * kr + wq) + (f)] = clock64()
+#define TQI(f) \
+    if (trc && kr < 96 && issuer) args.dbg[4096 + 3072 + 2 * kr + (f)] = clock64()
+#define TQK() ++kr
+#else
+#define TQ(f)
+#define TQI(f)
+#define TQK()
+#endif
+    uint64_t row[S];
+    float fac[S][3];
+    int layer[S];
+    bool active[S];
+    uint32_t phase[S];
+
+    auto start_tile = [&](int s) -> bool {
+        const uint64_t t = q0 + k_next * Q;
+        if (t >= ntiles) return false;
+        TQ(5);
+        mbar_wait(rec_bar, rec_phase);
+        rec_phase ^= 1;
+        row[s] = t * kTile + r;
+        const bool valid = row[s] < n;
+        float rec[16];
+        const float4* src = reinterpret_cast<const float4*>(sRec + r * kRecFloats);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float4 v = valid ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            rec[4 * c + 0] = v.x;
+            rec[4 * c + 1] = v.y;
+            rec[4 * c + 2] = v.z;
+            rec[4 * c + 3] = v.w;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) fac[s][c] = (args.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
+        {
+            uint32_t h[32];
+            encode_record(rec, args.ep, h);
+            tmem_st32(a_col(s) + lane_off, h);  // includes tcgen05.wait::st
+        }
+        fence_async_smem();  // record reads before the next TMA overwrite
+        tc_fence_before();
+        TQ(6);
+        named_bar_sync(1 + g, 128);  // A written; records consumed; previous TMEM reads of slot s done
+        ++k_next;
+        if (issuer_warp) {
+            const uint64_t tn = q0 + k_next * Q;
+            if (issuer && tn < ntiles) issue_records(tn);
+            __syncwarp();
+            issue_layer(s, 0);
+        }
+        return true;
+    };
+
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        phase[s] = 0;
+        layer[s] = 0;
+        active[s] = start_tile(s);
+    }
+    bool any = active[0];
+#pragma unroll
+    for (int s = 1; s < S; ++s) any = any || active[s];
+
+#pragma unroll 1
+    while (any) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (!active[s]) continue;
+            TQ(0);
+            mbar_wait(&mma_bar[s], phase[s]);
+            TQ(1);
+#ifdef NRC_TRACE_QUERY
+            if (trc && kr < 96) args.dbg[4096 + 8 * (4 * kr + wq) + 4] = s * 16 + layer[s];
+#endif
+            phase[s] ^= 1;
+            tc_fence_after();
+            const uint32_t t_d = d_col(s) + lane_off;
+            if (layer[s] < 5) {
+                // h_{L+1} = relu(acc) -> fp16, written over h_L in the slot's TMEM A
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    uint32_t v[32];
+                    tmem_ld32(t_d + 32 * half, v);
+                    uint32_t hp[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q)
+                        hp[q] = pack_h2_relu(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+                    tmem_st16_nowait(a_col(s) + lane_off + 16 * half, hp);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                TQ(2);
+                named_bar_sync(1 + g, 128);
+                ++layer[s];
+                if (issuer_warp) {
+                    TQI(0);
+                    issue_layer(s, layer[s]);
+                    TQI(1);
+                }
+                TQK();
+            } else {
+                // output: q = max(0, y * (alpha + beta))
+                uint32_t v[4];
+                tmem_ld4(t_d, v);
+                tc_fence_before();
+                if (row[s] < n) {
+                    float* o = args.out + row[s] * 3;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        float qv = __uint_as_float(v[c]) * fac[s][c];
+                        if (args.flags & 2u) qv = fmaxf(qv, 0.0f);
+                        o[c] = qv;
+                    }
+                }
+                layer[s] = 0;
+                TQ(2);
+                active[s] = start_tile(s);
+                TQK();
+            }
+        }
+        any = active[0];
+#pragma unroll
+        for (int s = 1; s < S; ++s) any = any || active[s];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem_base, 512);
+#undef TQ
+#undef TQI
+#undef TQK
+}
+
+}  // namespace nrc

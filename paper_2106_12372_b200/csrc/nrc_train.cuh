@@ -154,6 +154,28 @@ __device__ __forceinline__ long long global_ns() {
     do {                                                                                      \
         if (a.dbg != nullptr && step == 1 && threadIdx.x == 0) a.dbg[256 + 8 * blockIdx.x + (k)] = global_ns(); \
     } while (0)
+// Called by a whole converged warp: one elected lane issues a chain of 4 (or
+// 8) MMAs and, if bar != nullptr, commits them to bar (see elect_one()).
+template <int AS, int BS, int NCHAIN>
+__device__ __forceinline__ void warp_issue(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc0,
+                                           uint64_t* bar) {
+    d = warp_uniform(d);
+    a = warp_uniform(a);
+    b = warp_uniform(b);
+    acc0 = warp_uniform(acc0);
+    tc_fence_after();
+    if (elect_one()) {
+        if (NCHAIN == 8)
+            umma_ss8<AS, BS>(d, a, b, idesc, acc0);
+        else if (NCHAIN == 4)
+            umma_ss4<AS, BS>(d, a, b, idesc, acc0);
+        else
+            umma_f16(d, a, b, idesc, acc0);
+        if (bar != nullptr) umma_commit(bar);
+    }
+    __syncwarp();
+}
+
 #define NRC_TRC(i)                                                                          \
     do {                                                                                    \
         if (a.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.dbg[trc + (i)] = clock64(); \
@@ -256,11 +278,10 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
     };
     // wgrad of layer i (M=64 over outputs o, N=64 over inputs k, K=128 rows):
     // G_i += g_{i+1}^T h_i, both operands MN-major views of the stored tiles
-    auto issue_wgrad = [&](int i, uint32_t g_next) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-            umma_f16(t_wg(i), desc_mnmajor(g_next, kk), desc_mnmajor(hs(i), kk), idesc_wgrad,
-                     (first && kk == 0) ? 0u : 1u);
+    // (whole warp 4; commit to wg_bar if commit)
+    auto issue_wgrad = [&](int i, uint32_t g_next, bool commit) {
+        warp_issue<kMNmajStep, kMNmajStep, 8>(t_wg(i), desc_mnmajor(g_next, 0), desc_mnmajor(hs(i), 0), idesc_wgrad,
+                                              first ? 0u : 1u, commit ? wg_bar : nullptr);
     };
     // Stage layer i's fp32 gradient (64 x 64, or 16 x 64 for W5) from TMEM into
     // the dead stash slot i (h_i's last readers -- its mask epilogue and
@@ -323,21 +344,11 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
 #pragma unroll 1
                 for (int i = 4; i >= 1; --i) {
                     named_bar_sync(kBarDgrad, 64);
-                    if (lane == 0) {
-                        tc_fence_after();
-                        issue_wgrad(i + 1, i == 4 ? sG6_a : gb(i + 2));  // G_{i+1} += g_{i+2}^T h_{i+1}
-                        umma_commit(wg_bar);
-                    }
-                    __syncwarp();
+                    issue_wgrad(i + 1, i == 4 ? sG6_a : gb(i + 2), true);  // G_{i+1} += g_{i+2}^T h_{i+1}
                 }
                 named_bar_sync(kBarG1, kTrainThreads);  // g_1 written
-                if (lane == 0) {
-                    tc_fence_after();
-                    issue_wgrad(1, gb(2));  // G_1 += g_2^T h_1
-                    issue_wgrad(0, gb(1));  // G_0 += g_1^T h_0 (no gradient w.r.t. the encoding)
-                    umma_commit(wg_bar);
-                }
-                __syncwarp();
+                issue_wgrad(1, gb(2), false);  // G_1 += g_2^T h_1
+                issue_wgrad(0, gb(1), true);   // G_0 += g_1^T h_0 (no gradient w.r.t. the encoding)
                 first = false;
                 continue;
             }
@@ -375,14 +386,10 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
             // ---------------- forward: h_{i+1} = relu(W_i h_i), y = W5 h5
 #pragma unroll 1
             for (int L = 0; L < 5; ++L) {
-                if (tid == 0) {
-                    tc_fence_after();
-                    const uint32_t wl = sW_a + layer_off(L) * 2;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        umma_f16(t_acc, desc_kmajor(hs(L), k), desc_kmajor(wl, k), idesc_fwd, k > 0);
-                    umma_commit(mma_bar);
-                }
+                if (warp == 0)
+                    warp_issue<kKmajStep, kKmajStep, 4>(t_acc, desc_kmajor(hs(L), 0),
+                                                        desc_kmajor(sW_a + layer_off(L) * 2, 0), idesc_fwd, 0u,
+                                                        mma_bar);
                 mma_wait();
 #pragma unroll
                 for (int half = 0; half < 2; ++half) {
@@ -398,14 +405,9 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
                 sync_rows();
                 NRC_TRC(5 + L);
             }
-            if (tid == 0) {
-                tc_fence_after();
-                const uint32_t wl = sW_a + layer_off(5) * 2;
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    umma_f16(t_acc, desc_kmajor(hs(5), k), desc_kmajor(wl, k), idesc_out, k > 0);
-                umma_commit(mma_bar);
-            }
+            if (warp == 0)
+                warp_issue<kKmajStep, kKmajStep, 4>(t_acc, desc_kmajor(hs(5), 0), desc_kmajor(sW_a + layer_off(5) * 2, 0),
+                                                    idesc_out, 0u, mma_bar);
             mma_wait();
             // ---------------- relative L2 loss, Eq.(5) (R8-R10, R13)
             {
@@ -440,28 +442,19 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
             // dgrad_i and commits it, then warp 4 queues wgrad_{i+1} behind it; the
             // rows wait for dgrad_i only.  G_{i+2} is staged and bulk-stored in
             // round i (its wgrad was queued a round earlier).
-            if (tid == 0) {
-                tc_fence_after();
-                const uint32_t w5 = sW_a + layer_off(5) * 2;
-                umma_f16(t_acc, desc_kmajor(sG6_a, 0), desc_mnmajor(w5, 0), idesc_dgrad, 0);  // delta5 = gy W5
-                umma_commit(mma_bar);
-            }
+            if (warp == 0)  // delta5 = gy W5 (one K=16 step)
+                warp_issue<0, 0, 1>(t_acc, desc_kmajor(sG6_a, 0), desc_mnmajor(sW_a + layer_off(5) * 2, 0), idesc_dgrad,
+                                    0u, mma_bar);
             mma_wait();
             mask_epilogue(5);
             sync_rows();
             NRC_TRC(11);
 #pragma unroll 1
             for (int i = 4; i >= 1; --i) {
-                if (warp == 0) {
-                    if (lane == 0) {
-                        tc_fence_after();
-                        const uint32_t wl = sW_a + layer_off(i) * 2;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)  // delta_i = g_{i+1} W_i
-                            umma_f16(t_acc, desc_kmajor(gb(i + 1), k), desc_mnmajor(wl, k), idesc_dgrad, k > 0);
-                        umma_commit(mma_bar);
-                    }
-                    __syncwarp();
+                if (warp == 0) {  // delta_i = g_{i+1} W_i
+                    warp_issue<kKmajStep, kMNmajStep, 4>(t_acc, desc_kmajor(gb(i + 1), 0),
+                                                         desc_mnmajor(sW_a + layer_off(i) * 2, 0), idesc_dgrad, 0u,
+                                                         mma_bar);
                     named_bar_arrive(kBarDgrad, 64);  // warp 4 may queue wgrad_{i+1} now
                 }
                 if (i <= 3) {

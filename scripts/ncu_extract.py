@@ -46,7 +46,7 @@ def main(tag, d):
     open(os.path.join(prof, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     traffic = {}
-    for name, rep in [("nrc_query_kernel", "prof_query.ncu-rep"), ("nrc_train_kernel", "prof_train.ncu-rep")]:
+    for name, rep in [("nrc_query_ts_kernel", "prof_query.ncu-rep"), ("nrc_train_kernel", "prof_train.ncu-rep")]:
         p = os.path.join(d, rep)
         if os.path.exists(p):
             m = raw(p, ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"])

@@ -8,7 +8,13 @@
 
 using namespace nrc;
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p = 0;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n}" : "=r"(p));
+    return p != 0;
+}
 __global__ void __launch_bounds__(128, 1) ubench(int mode, int iters, long long* out) {
+    long long issue_sum = 0;
     __shared__ __align__(1024) uint8_t sA[kTileBytes];
     __shared__ __align__(1024) uint8_t sB[kTileBytes];
     __shared__ uint64_t bar;
@@ -43,6 +49,59 @@ __global__ void __launch_bounds__(128, 1) ubench(int mode, int iters, long long*
                 for (int l = 0; l < 16; ++l)
                     for (int k = 0; k < 4; ++k) umma_f16(tb, desc_kmajor(a, k), desc_kmajor(b, k), idesc, k > 0);
                 umma_commit(&bar);
+            }
+            mbar_wait(&bar, phase);
+            phase ^= 1;
+            continue;
+        }
+        if (mode == 16 || mode == 17) {  // warp-converged issue with elect.sync inside the asm
+            if (warp == 0) {
+                const uint32_t d_u = __shfl_sync(0xffffffffu, tb, 0);
+                const uint32_t a_u = __shfl_sync(0xffffffffu, tb + 64, 0);
+                const uint64_t b0 = desc_kmajor(b, 0);
+                const uint32_t blo = __shfl_sync(0xffffffffu, uint32_t(b0), 0);
+                const uint32_t bhi = __shfl_sync(0xffffffffu, uint32_t(b0 >> 32), 0);
+                const uint64_t bd = (uint64_t(bhi) << 32) | blo;
+                const uint32_t bar_u = __shfl_sync(0xffffffffu, smem_u32(&bar), 0);
+                tc_fence_after();
+                const long long a0 = clock64();
+                if (mode == 16) {
+                    asm volatile(
+                        "{\n\t.reg .pred e, f, t;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+                        "elect.sync _|e, 0xffffffff;\n\t"
+                        "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+                        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+                        "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
+                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, f;\n\t"
+                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n\t"
+                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n\t"
+                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n\t"
+                        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}" ::"r"(d_u),
+                        "r"(a_u), "l"(bd), "r"(idesc), "r"(bar_u)
+                        : "memory");
+                } else {
+                    if (elect_one()) umma_chain4_ta_commit(d_u, a_u, bd, idesc, &bar);
+                }
+                __syncwarp();
+                if (tid == 0) issue_sum += clock64() - a0;
+            }
+            mbar_wait(&bar, phase);
+            phase ^= 1;
+            continue;
+        }
+        if (mode >= 10) {  // issue cost: clock around the issue of n MMAs + commit only
+            if (tid == 0) {
+                tc_fence_after();
+                const long long a0 = clock64();
+                const int nm = mode == 10 ? 4 : mode == 11 ? 1 : mode == 13 ? 2 : mode == 14 ? 16 : mode == 15 ? 64 : 4;
+                for (int k = 0; k < nm; ++k) {
+                    if (mode == 12)
+                        umma_f16_ta(tb, tb + 64 + 8 * (k & 3), desc_kmajor(b, k & 3), idesc, k > 0);
+                    else
+                        umma_f16(tb, desc_kmajor(a, k & 3), desc_kmajor(b, k & 3), idesc, k > 0);
+                }
+                umma_commit(&bar);
+                issue_sum += clock64() - a0;
             }
             mbar_wait(&bar, phase);
             phase ^= 1;
@@ -98,6 +157,7 @@ __global__ void __launch_bounds__(128, 1) ubench(int mode, int iters, long long*
     }
     long long t1 = clock64();
     if (tid == 0) out[0] = (t1 - t0) / iters;
+    if (tid == 0 && mode >= 10) out[0] = issue_sum / iters;
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tb, 128);
@@ -109,8 +169,12 @@ int main() {
     const char* names[] = {"mma SS + commit + wait", "mma TS + commit + wait", "round: SS mma + epi(smem)",
                            "round: SS mma + epi(smem) [same]", "round: TS mma + epi(tmem st)",
                            "16 layers back-to-back (per 16)", "SS mma + wait + syncthreads",
-                           "dgrad M128N64K64 (B MN-major)", "wgrad M64N64K128 (A,B MN-major)", "dgrad + wgrad"};
-    for (int mode = 0; mode < 10; ++mode) {
+                           "dgrad M128N64K64 (B MN-major)", "wgrad M64N64K128 (A,B MN-major)", "dgrad + wgrad",
+                           "ISSUE ONLY: 4 SS mma + commit", "ISSUE ONLY: 1 SS mma + commit",
+                           "ISSUE ONLY: 4 TS mma + commit", "ISSUE ONLY: 2 SS mma + commit",
+                           "ISSUE ONLY: 16 SS mma + commit", "ISSUE ONLY: 64 SS mma + commit",
+                           "ISSUE: warp elect.sync asm chain4 TS", "ISSUE: elect_one() + chain4 TS"};
+    for (int mode = 0; mode < 18; ++mode) {
         ubench<<<1, 128>>>(mode, 2000, d);
         long long c = 0;
         cudaError_t e = cudaDeviceSynchronize();
