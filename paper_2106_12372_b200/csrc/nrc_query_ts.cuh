@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
                     tmem_st16_nowait(a_col(s) + lane_off + 16 * half, hp);
                 }
                 tmem_wait_st();
+
                 tc_fence_before();
                 TQ(2);
                 named_bar_sync(1 + g, 128);

@@ -38,6 +38,30 @@ __device__ __forceinline__ void gsync(unsigned long long* ctr, unsigned long lon
     __syncthreads();
 }
 
+// flag barrier: CTA b publishes epoch in its own 8-byte slot; warp 0 polls all slots
+__device__ __forceinline__ void fsync(unsigned long long* flags, unsigned long long epoch) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + blockIdx.x), "l"(epoch) : "memory");
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
+            unsigned long long v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + b) : "memory");
+            } while (v < epoch);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+}
+__global__ void flag_bench(unsigned long long* flags, int iters, long long* out) {
+    fsync(flags, 1);
+    const long long t0 = gns();
+    for (int i = 0; i < iters; ++i) fsync(flags, i + 2);
+    const long long t1 = gns();
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+}
+
 template <int MODE>
 __global__ void barrier_bench(unsigned long long* ctr, int iters, long long* out) {
     const unsigned long long G = gridDim.x;
@@ -128,6 +152,15 @@ int main() {
         cudaDeviceSynchronize();
         cudaMemcpy(&ns, d, 8, cudaMemcpyDeviceToHost);
         printf("barrier mode 3 (fence.acq_rel + relaxed)       grid %d: %lld ns\n", grid, ns);
+    }
+    unsigned long long* flags;
+    cudaMalloc(&flags, 8 * 256);
+    for (int grid : {128, 148}) {
+        cudaMemset(flags, 0, 8 * 256);
+        flag_bench<<<grid, 160>>>(flags, 1000, d);
+        cudaDeviceSynchronize();
+        cudaMemcpy(&ns, d, 8, cudaMemcpyDeviceToHost);
+        printf("flag barrier (st.release / ld.acquire per CTA slot) grid %d: %lld ns\n", grid, ns);
     }
     for (int block : {160, 256, 512}) {
         cudaMemset(ctr, 0, 8);

@@ -101,6 +101,37 @@ def test_query_parity_1080p_sampled(nrc, orc):
     assert np.all(np.isfinite(q))
 
 
+def test_query_parity_4k_sampled_and_all_configs(nrc, orc):
+    """C5-size query (3840 x 2160 = 8,294,400 records, default max_batch) on
+    one GPU, sampled against the oracle; every query-kernel configuration
+    (NRC_QUERY_CFG table, TMEM and SMEM activation variants) must produce
+    the same bits."""
+    import os
+    n = nrc_inputs.N_4K
+    recs = nrc_inputs.records(n, seed=nrc_inputs.SEED_QUERY + 1)
+    d_recs = dev(recs)
+    tr, tg = nrc_inputs.train_frame(1)
+    cache = nrc.RadianceCache()
+    cache.train_frame(dev(tr), dev(tg), 4, 16384, 2)
+    q = cache.query(d_recs).cpu().numpy()
+    idx = np.unique(np.concatenate([np.linspace(0, n - 1, 12000).astype(np.int64), np.arange(n - 200, n)]))
+    ref = orc.query(cache.get_params("ema").astype(np.float64), recs[idx])
+    errs = radiance_err(q[idx], ref)
+    assert max(errs) <= TOL_RADIANCE, errs
+    w = cache.get_params("train")
+    small = d_recs[:50000]
+    base = cache.query(small).cpu().numpy()
+    for cfg in range(7):
+        os.environ["NRC_QUERY_CFG"] = str(cfg)
+        try:
+            c2 = nrc.RadianceCache()
+        finally:
+            del os.environ["NRC_QUERY_CFG"]
+        c2.set_params(w, "train")
+        c2.set_params(cache.get_params("ema"), "ema")
+        np.testing.assert_array_equal(c2.query(small).cpu().numpy(), base, err_msg=f"cfg {cfg}")
+
+
 def test_query_raw_vs_ema_and_factorization_off(nrc, orc):
     recs = nrc_inputs.records(700, seed=7)
     tr, tg = nrc_inputs.train_frame(3, n=4096)
