@@ -77,6 +77,11 @@ def lib():
         L.orc_lcg_permute.restype = None; L.orc_lcg_permute.argtypes = [u64, u64, u64, u64, vp]
         L.orc_init_weights.restype = None; L.orc_init_weights.argtypes = [u64, vp]
         L.orc_param_count.restype = i64; L.orc_param_count.argtypes = []
+        L.orc_param_count_w.restype = i64; L.orc_param_count_w.argtypes = [ctypes.c_int]
+        L.orc_forward_w.restype = None; L.orc_forward_w.argtypes = [ctypes.c_int, vp, vp, vp]
+        L.orc_query_batch_w.restype = None
+        L.orc_query_batch_w.argtypes = [ctypes.c_int, vp, vp, i64, vp, vp, ctypes.c_uint, vp]
+        L.orc_init_weights_w.restype = None; L.orc_init_weights_w.argtypes = [ctypes.c_int, u64, vp]
         L.orc_train_step.restype = d
         L.orc_train_step.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp, d, ctypes.c_uint,
                                      d, d, d, d, d, ctypes.c_int, vp, vp, vp]
@@ -145,6 +150,35 @@ def query(W, recs, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), flags=FACTORIZE | CLAMP
     lib().orc_query_batch(W.ctypes.data, recs.ctypes.data, recs.shape[0], lo.ctypes.data, hi.ctypes.data,
                           int(flags), q.ctypes.data)
     return q
+
+
+# ---------------------------------------------------------------- width ablation (C4)
+def param_count_w(hw: int) -> int:
+    return int(lib().orc_param_count_w(int(hw)))
+
+
+def forward_w(hw, W, e):
+    W = _c(W, np.float64); e = _c(e, np.float64)
+    y = np.zeros(3, np.float64)
+    lib().orc_forward_w(int(hw), W.ctypes.data, e.ctypes.data, y.ctypes.data)
+    return y
+
+
+def query_w(hw, W, recs, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), flags=FACTORIZE | CLAMP_QUERY) -> np.ndarray:
+    W = _c(W, np.float64)
+    assert W.size == param_count_w(hw)
+    recs = _c(recs, np.float32).reshape(-1, 16)
+    lo, hi = _c(aabb_lo, np.float32), _c(aabb_hi, np.float32)
+    q = np.zeros((recs.shape[0], 3), np.float64)
+    lib().orc_query_batch_w(int(hw), W.ctypes.data, recs.ctypes.data, recs.shape[0], lo.ctypes.data,
+                            hi.ctypes.data, int(flags), q.ctypes.data)
+    return q
+
+
+def init_weights_w(hw: int, seed: int) -> np.ndarray:
+    W = np.zeros(param_count_w(hw), np.float32)
+    lib().orc_init_weights_w(int(hw), int(seed) & (2**64 - 1), W.ctypes.data)
+    return W
 
 
 def loss(yhat, t, eps=0.01):

@@ -23,6 +23,8 @@
  *       forms, SPEC worked examples, periodicity, integral of quartic = 1)
  *   orc_encode ............................................. pinned (golden
  *       vector tests/golden/encode_c0.txt, structural invariants)
+ *   orc_forward_w / orc_query_batch_w / orc_init_weights_w . pinned (width
+ *       embedding into the 64 net, numpy matmul chain, Glorot moments)
  *   orc_forward / orc_query ................................ pinned (zero net,
  *       constant net via pad channel, linear chain, homogeneity, permutation)
  *   orc_loss ............................................... pinned (S:L193-195
@@ -212,6 +214,63 @@ void orc_query_batch(const double* W, const float* recs, int64_t n, const float*
         const float* rec = recs + 16 * i;
         orc_encode(rec, lo, hi, e);
         orc_forward(W, e, H, y);
+        for (int c = 0; c < 3; ++c) {
+            double v = y[c];
+            if (flags & ORC_FACTORIZE) v *= (double)rec[10 + c] + (double)rec[13 + c];
+            if ((flags & ORC_CLAMP_QUERY) && v < 0.0) v = 0.0;
+            q[3 * i + c] = v;
+        }
+    }
+}
+
+/* ---- width ablation (BASELINE.json configs[3]): the same network
+ * with hidden width hw in {32, 64, 128} instead of 64 (the input stays the
+ * 64-dim encoding; the depth stays 5 hidden layers).
+ * Logical layout: W0 [hw][64], W1..W4 [hw][hw], W5 [3][hw], row-major
+ * [out][in]; P(hw) = 64 hw + 4 hw^2 + 3 hw parameters.  Plain definition:
+ * H0 = e; H_{i+1} = ReLU(W_i H_i), i = 0..4; y = W5 H5. */
+int64_t orc_param_count_w(int hw) { return 64 * (int64_t)hw + 4 * (int64_t)hw * hw + 3 * (int64_t)hw; }
+
+static int64_t orc_mat_off_w(int hw, int i)
+{
+    if (i == 0) return 0;
+    return 64 * (int64_t)hw + (int64_t)(i - 1) * hw * hw;
+}
+
+void orc_forward_w(int hw, const double* W, const double* e, double* y)
+{
+    double h[128], hn[128];
+    for (int o = 0; o < hw; ++o) {
+        double acc = 0.0;
+        for (int k = 0; k < ORC_IN; ++k) acc += W[orc_mat_off_w(hw, 0) + ORC_IN * o + k] * e[k];
+        h[o] = acc > 0.0 ? acc : 0.0;
+    }
+    for (int i = 1; i < 5; ++i) {
+        const double* Wi = W + orc_mat_off_w(hw, i);
+        for (int o = 0; o < hw; ++o) {
+            double acc = 0.0;
+            for (int k = 0; k < hw; ++k) acc += Wi[hw * o + k] * h[k];
+            hn[o] = acc > 0.0 ? acc : 0.0;
+        }
+        for (int o = 0; o < hw; ++o) h[o] = hn[o];
+    }
+    const double* W5 = W + orc_mat_off_w(hw, 5);
+    for (int o = 0; o < 3; ++o) {
+        double acc = 0.0;
+        for (int k = 0; k < hw; ++k) acc += W5[hw * o + k] * h[k];
+        y[o] = acc;
+    }
+}
+
+void orc_query_batch_w(int hw, const double* W, const float* recs, int64_t n, const float* lo, const float* hi,
+                       unsigned flags, double* q)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double e[64], y[3];
+        const float* rec = recs + 16 * i;
+        orc_encode(rec, lo, hi, e);
+        orc_forward_w(hw, W, e, y);
         for (int c = 0; c < 3; ++c) {
             double v = y[c];
             if (flags & ORC_FACTORIZE) v *= (double)rec[10 + c] + (double)rec[13 + c];
@@ -439,6 +498,23 @@ void orc_init_weights(uint64_t seed, float* W32)
                 uint64_t ctr = ((uint64_t)i << 32) | (uint64_t)(r * 64 + c);
                 double u = (double)(orc_splitmix64(seed ^ ctr) >> 11) * (1.0 / 9007199254740992.0);
                 W32[orc_mat_off[i] + 64 * r + c] = (float)((2.0 * u - 1.0) * bound);
+            }
+    }
+}
+
+/* Reading R16 at hidden width hw: the same Glorot-uniform counter stream,
+ * fan_in = 64 (W0) or hw, fan_out = hw (W0..W4) or 3 (W5); counter
+ * (i << 32 | r * fan_in + c).  At hw = 64 this is orc_init_weights. */
+void orc_init_weights_w(int hw, uint64_t seed, float* W32)
+{
+    for (int i = 0; i < ORC_NMAT; ++i) {
+        int rows = i < 5 ? hw : 3, cols = i == 0 ? ORC_IN : hw;
+        double bound = sqrt(6.0 / ((double)cols + (double)rows));
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) {
+                uint64_t ctr = ((uint64_t)i << 32) | (uint64_t)(r * cols + c);
+                double u = (double)(orc_splitmix64(seed ^ ctr) >> 11) * (1.0 / 9007199254740992.0);
+                W32[orc_mat_off_w(hw, i) + (int64_t)cols * r + c] = (float)((2.0 * u - 1.0) * bound);
             }
     }
 }
