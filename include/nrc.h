@@ -89,7 +89,11 @@ enum {
 
 typedef struct nrc_config {
     uint32_t abi_version;      /* must equal NRC_ABI_VERSION                          */
-    uint32_t hidden_width;     /* 64 ("five hidden layers have 64 neurons")   */
+    uint32_t hidden_width;     /* 64 ("five hidden layers have 64 neurons");
+                                * 32 or 128 for the width ablation (BASELINE configs[3]):
+                                * query and parameter calls only, training calls return
+                                * NRC_ERR_UNSUPPORTED.  nrc_param_count() gives
+                                * 64 W + 4 W^2 + 3 W.                                   */
     uint32_t n_hidden_layers;  /* 5; fixed in ABI v1                         */
     uint32_t max_batch;        /* largest n accepted by query/train calls             */
     float aabb_min[3];         /* position normalisation domain (R3)           */

@@ -54,7 +54,45 @@ const QueryEntry kQueryCfgs[] = {NRC_QCFG_TS(5, 1), NRC_QCFG(4, 2), NRC_QCFG(3, 
 #undef NRC_QCFG
 #undef NRC_QCFG_TS
 constexpr int kNumQueryCfgs = int(sizeof(kQueryCfgs) / sizeof(kQueryCfgs[0]));
+// width ablation: one TMEM-activation configuration per width
+template <int G, int S, int W>
+struct QueryLauncherW {
+    static cudaError_t set_smem() {
+        return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    query_ts_smem_bytes<G, S, W>());
+    }
+    static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
+        nrc_query_ts_kernel<G, S, W><<<grid, 128 * G, query_ts_smem_bytes<G, S, W>(), st>>>(qa);
+    }
+};
+const QueryEntry kQueryW32 = {&QueryLauncherW<5, 1, 32>::set_smem, &QueryLauncherW<5, 1, 32>::launch, 5};
+const QueryEntry kQueryW128 = {&QueryLauncherW<2, 1, 128>::set_smem, &QueryLauncherW<2, 1, 128>::launch, 2};
 constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
+
+// Runtime view of NetDims<W> (nrc_device.cuh) for the host code.
+struct WidthInfo {
+    int W = 64, padded = 0, logical = 0, img = 0;
+    int pad_off[7] = {}, rows[6] = {}, cols[6] = {};
+};
+template <int W>
+WidthInfo width_info_t() {
+    using D = NetDims<W>;
+    WidthInfo w;
+    w.W = W;
+    w.padded = D::kPadded;
+    w.logical = D::kLogical;
+    w.img = D::kImg;
+    for (int i = 0; i < 7; ++i) w.pad_off[i] = D::pad_off(i);
+    for (int i = 0; i < 6; ++i) {
+        w.rows[i] = i < 5 ? W : 3;  // logical rows (W5 has 3)
+        w.cols[i] = D::cols(i);
+    }
+    return w;
+}
+bool width_supported(uint32_t W) { return W == 32 || W == 64 || W == 128; }
+WidthInfo width_info(int W) {
+    return W == 32 ? width_info_t<32>() : W == 128 ? width_info_t<128>() : width_info_t<64>();
+}
 
 struct StateLayout {
     size_t w, m, v, ema, wimg, eimg, partials, loss_part, counters, total;
@@ -62,7 +100,8 @@ struct StateLayout {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-StateLayout layout() {
+StateLayout layout(int W) {
+    const WidthInfo wi = width_info(W);
     StateLayout L{};
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -70,14 +109,15 @@ StateLayout layout() {
         o = align_up(o + bytes, 256);
         return at;
     };
-    const size_t pf = sizeof(float) * kParamPadded;
+    const size_t pf = sizeof(float) * size_t(wi.padded);
     L.w = take(pf);
     L.m = take(pf);
     L.v = take(pf);
     L.ema = take(pf);
-    L.wimg = take(kImgBytes);
-    L.eimg = take(kImgBytes);
-    L.partials = take(pf * kMaxPartials);
+    L.wimg = take(size_t(wi.img));
+    L.eimg = take(size_t(wi.img));
+    // training (hidden width 64 only) scratch
+    L.partials = take(W == 64 ? sizeof(float) * kParamPadded * kMaxPartials : 256);
     L.loss_part = take(sizeof(float) * kMaxPartials);
     L.counters = take(sizeof(unsigned long long) * 4);
     L.total = o;
@@ -106,6 +146,7 @@ struct nrc_handle {
     long long* dbg = nullptr;  // diagnostics only (nrc_debug_set_trace)
     unsigned long long gbar = 0;  // arrivals so far on the train kernel's grid-barrier counter
     bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
+    WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     float* d_w() { return reinterpret_cast<float*>(state + L.w); }
     float* d_m() { return reinterpret_cast<float*>(state + L.m); }
     float* d_v() { return reinterpret_cast<float*>(state + L.v); }
@@ -174,6 +215,13 @@ static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, si
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+template <int W>
+static void launch_images(nrc_handle* h, cudaStream_t st) {
+    const int blocks = (NetDims<W>::kPadded + 255) / 256;
+    nrc_image_w_kernel<W><<<blocks, 256, 0, st>>>(h->d_w(), h->d_wimg());
+    nrc_image_w_kernel<W><<<blocks, 256, 0, st>>>(h->d_ema(), h->d_eimg());
+}
+
 extern "C" {
 
 void nrc_default_config(nrc_config* c) {
@@ -207,8 +255,8 @@ static nrc_status validate_config(const nrc_config* c, std::string* why) {
         *why = "ABI version mismatch";
         return NRC_ERR_UNSUPPORTED;
     }
-    if (c->hidden_width != 64 || c->n_hidden_layers != 5) {
-        *why = "only hidden_width 64 with 5 hidden layers is built (P:L694)";
+    if (!width_supported(c->hidden_width) || c->n_hidden_layers != 5) {
+        *why = "hidden_width must be 32, 64 (P:L694) or 128 (width ablation) with 5 hidden layers";
         return NRC_ERR_UNSUPPORTED;
     }
     if (c->max_batch == 0) {
@@ -234,7 +282,7 @@ static nrc_status validate_config(const nrc_config* c, std::string* why) {
 size_t nrc_state_bytes(const nrc_config* cfg) {
     std::string why;
     if (validate_config(cfg, &why) != NRC_OK) return 0;
-    return layout().total;
+    return layout(int(cfg->hidden_width)).total;
 }
 
 const char* nrc_status_string(nrc_status s) {
@@ -252,7 +300,7 @@ const char* nrc_status_string(nrc_status s) {
 
 const char* nrc_last_error(const nrc_handle* h) { return h ? h->err.c_str() : "NULL handle"; }
 uint32_t nrc_last_launch_count(const nrc_handle* h) { return h ? h->launches : 0; }
-size_t nrc_param_count(const nrc_handle*) { return kParamLogical; }
+size_t nrc_param_count(const nrc_handle* h) { return h ? size_t(h->wi.logical) : size_t(kParamLogical); }
 
 nrc_status nrc_lcg_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* c, uint64_t* m) {
     if (!a || !c || !m || n == 0) return NRC_ERR_INVALID_ARGUMENT;
@@ -268,12 +316,15 @@ nrc_status nrc_lcg_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* c, u
 }
 
 static nrc_status refresh_images(nrc_handle* h, cudaStream_t st) {
-    const int blocks = (kParamPadded + 255) / 256;
-    nrc_image_kernel<<<blocks, 256, 0, st>>>(h->d_w(), h->d_wimg());
-    NRC_LAUNCHED(h, "nrc_image_kernel");
-    nrc_image_kernel<<<blocks, 256, 0, st>>>(h->d_ema(), h->d_eimg());
-    NRC_LAUNCHED(h, "nrc_image_kernel");
-    return NRC_OK;
+    if (h->wi.W == 32)
+        launch_images<32>(h, st);
+    else if (h->wi.W == 128)
+        launch_images<128>(h, st);
+    else
+        launch_images<64>(h, st);
+    nrc_status s = cuda_check(h, cudaGetLastError(), "nrc_image_w_kernel");
+    if (s == NRC_OK) h->launches += 2;
+    return s;
 }
 
 nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nrc_handle** out) {
@@ -285,7 +336,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
         std::fprintf(stderr, "nrc_init: %s\n", why.c_str());
         return s;
     }
-    const StateLayout L = layout();
+    const StateLayout L = layout(int(cfg->hidden_width));
     if (!d_state || !aligned(d_state, 256)) return NRC_ERR_INVALID_ARGUMENT;
     if (state_bytes < L.total) return NRC_ERR_OUT_OF_MEMORY;
 
@@ -293,6 +344,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     h->cfg = *cfg;
     h->state = static_cast<uint8_t*>(d_state);
     h->L = L;
+    h->wi = width_info(int(cfg->hidden_width));
     h->step = 0;
     h->launches = 0;
     for (int i = 0; i < 3; ++i) {
@@ -323,24 +375,28 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     if (h->query_cfg < 0 || h->query_cfg >= kNumQueryCfgs) h->query_cfg = 0;
     for (int i = 0; i < kNumQueryCfgs; ++i)
         if ((s = cuda_check(h, kQueryCfgs[i].set_smem(), "cudaFuncSetAttribute(query)")) != NRC_OK) return bail(s);
+    if ((s = cuda_check(h, kQueryW32.set_smem(), "cudaFuncSetAttribute(query w32)")) != NRC_OK) return bail(s);
+    if ((s = cuda_check(h, kQueryW128.set_smem(), "cudaFuncSetAttribute(query w128)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 kTrainSmemBytes),
                         "cudaFuncSetAttribute(train)")) != NRC_OK)
         return bail(s);
 
-    // Glorot-uniform init from the counter-based splitmix64 stream (R16).
-    std::vector<float> w(kParamPadded, 0.0f);
-    const int rows_of[6] = {64, 64, 64, 64, 64, 3};
+    // Glorot-uniform init from the counter-based splitmix64 stream (R16):
+    // counter (layer << 32 | r * fan_in + c), bound sqrt(6 / (fan_in + fan_out)).
+    const WidthInfo& wi = h->wi;
+    std::vector<float> w(size_t(wi.padded), 0.0f);
     for (int i = 0; i < 6; ++i) {
-        const double bound = std::sqrt(6.0 / (64.0 + double(rows_of[i])));
-        for (int r = 0; r < rows_of[i]; ++r)
-            for (int c = 0; c < 64; ++c) {
-                const uint64_t ctr = (uint64_t(i) << 32) | uint64_t(r * 64 + c);
+        const int rows = wi.rows[i], cols = wi.cols[i];
+        const double bound = std::sqrt(6.0 / (double(cols) + double(rows)));
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) {
+                const uint64_t ctr = (uint64_t(i) << 32) | uint64_t(r * cols + c);
                 const double u = double(splitmix64(cfg->seed ^ ctr) >> 11) * (1.0 / 9007199254740992.0);
-                w[layer_off(i) + r * 64 + c] = float((2.0 * u - 1.0) * bound);
+                w[size_t(wi.pad_off[i]) + size_t(r) * cols + c] = float((2.0 * u - 1.0) * bound);
             }
     }
-    const size_t pf = sizeof(float) * kParamPadded;
+    const size_t pf = sizeof(float) * size_t(wi.padded);
     if ((s = cuda_check(h, cudaMemset(h->state, 0, L.total), "cudaMemset(state)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, cudaMemcpy(h->d_w(), w.data(), pf, cudaMemcpyHostToDevice), "cudaMemcpy(w)")) != NRC_OK)
         return bail(s);
@@ -357,6 +413,11 @@ nrc_status nrc_destroy(nrc_handle* h) {
     return NRC_OK;
 }
 
+// training kernels are built for the paper's width only (the C4 ablation is query-only)
+static nrc_status check_train_width(nrc_handle* h) {
+    if (h->wi.W == 64) return NRC_OK;
+    return fail(h, NRC_ERR_UNSUPPORTED, "training is built for hidden_width 64 only (width ablation is query-only)");
+}
 static nrc_status check_handle(nrc_handle* h) {
     if (!h || !h->state) return NRC_ERR_STATE;
     int dev = -1;
@@ -382,11 +443,12 @@ nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* 
     qa.ep = h->ep;
     qa.flags = h->cfg.flags & (NRC_FACTORIZE | NRC_CLAMP_QUERY);
     qa.dbg = h->dbg;
+    const QueryEntry& qe = h->wi.W == 32 ? kQueryW32 : h->wi.W == 128 ? kQueryW128 : kQueryCfgs[h->query_cfg];
     const uint64_t ntiles = (n + kTile - 1) / kTile;
-    const uint64_t G = uint64_t(kQueryCfgs[h->query_cfg].groups);
+    const uint64_t G = uint64_t(qe.groups);
     const uint64_t ctas = (ntiles + G - 1) / G;  // one tile stream per group
     const int grid = int(ctas < uint64_t(h->num_sms) ? ctas : uint64_t(h->num_sms));
-    kQueryCfgs[h->query_cfg].launch(grid, qa, static_cast<cudaStream_t>(stream));
+    qe.launch(grid, qa, static_cast<cudaStream_t>(stream));
     NRC_LAUNCHED(h, "nrc_query_kernel");
     return NRC_OK;
 }
@@ -524,6 +586,7 @@ nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d
                           void* stream) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
     if (n == 0) return NRC_OK;
     if ((s = check_train_args(h, d_rec, d_tgt, n, "nrc_train_step")) != NRC_OK) return s;
@@ -536,6 +599,7 @@ nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const floa
                               float* d_grad, float* d_loss_sum, void* stream) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
     if (!d_grad || !aligned(d_grad, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_backward: bad d_grad");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -559,6 +623,7 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
                                     uint32_t row_end, float* d_grad, float* d_loss_sum, void* stream) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
     if (!d_grad || !aligned(d_grad, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_backward: bad d_grad");
     if (row_begin > row_end || row_end > l || uint64_t(j + 1) * l > n_total)
@@ -584,6 +649,7 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
 nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, void* stream) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
     if (n_global == 0) return NRC_OK;
     if (!d_grad_sum || !aligned(d_grad_sum, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply: bad grad");
@@ -603,6 +669,7 @@ nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* 
                            uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
     if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
     if (!d_rec || !d_tgt || !aligned(d_rec, 16) || !aligned(d_tgt, 4))
@@ -650,26 +717,24 @@ static float* param_ptr(nrc_handle* h, nrc_param_set which) {
     return nullptr;
 }
 
-// logical (20,672) <-> padded (21,504): only W5's rows 3..15 are padding
-static void logical_to_padded(const float* lg, float* pd) {
-    std::memset(pd, 0, sizeof(float) * kParamPadded);
-    std::memcpy(pd, lg, sizeof(float) * 20480);
-    std::memcpy(pd + 20480, lg + 20480, sizeof(float) * 192);
+// logical <-> padded: only W5's rows 3..15 are padding (W0..W4 identical)
+static void logical_to_padded(const WidthInfo& wi, const float* lg, float* pd) {
+    std::memset(pd, 0, sizeof(float) * size_t(wi.padded));
+    std::memcpy(pd, lg, sizeof(float) * size_t(wi.logical));
 }
-static void padded_to_logical(const float* pd, float* lg) {
-    std::memcpy(lg, pd, sizeof(float) * 20480);
-    std::memcpy(lg + 20480, pd + 20480, sizeof(float) * 192);
+static void padded_to_logical(const WidthInfo& wi, const float* pd, float* lg) {
+    std::memcpy(lg, pd, sizeof(float) * size_t(wi.logical));
 }
 
 nrc_status nrc_get_params(nrc_handle* h, nrc_param_set which, float* h_out, size_t n) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
     float* src = param_ptr(h, which);
-    if (!src || !h_out || n < size_t(kParamLogical)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_get_params");
-    std::vector<float> pd(kParamPadded);
+    if (!src || !h_out || n < size_t(h->wi.logical)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_get_params");
+    std::vector<float> pd(size_t(h->wi.padded));
     NRC_CUDA(h, cudaDeviceSynchronize());
-    NRC_CUDA(h, cudaMemcpy(pd.data(), src, sizeof(float) * kParamPadded, cudaMemcpyDeviceToHost));
-    padded_to_logical(pd.data(), h_out);
+    NRC_CUDA(h, cudaMemcpy(pd.data(), src, sizeof(float) * pd.size(), cudaMemcpyDeviceToHost));
+    padded_to_logical(h->wi, pd.data(), h_out);
     return NRC_OK;
 }
 
@@ -677,11 +742,11 @@ nrc_status nrc_set_params(nrc_handle* h, nrc_param_set which, const float* h_in,
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
     float* dst = param_ptr(h, which);
-    if (!dst || !h_in || n < size_t(kParamLogical)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_set_params");
-    std::vector<float> pd(kParamPadded);
-    logical_to_padded(h_in, pd.data());
+    if (!dst || !h_in || n < size_t(h->wi.logical)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_set_params");
+    std::vector<float> pd(size_t(h->wi.padded));
+    logical_to_padded(h->wi, h_in, pd.data());
     NRC_CUDA(h, cudaDeviceSynchronize());
-    NRC_CUDA(h, cudaMemcpy(dst, pd.data(), sizeof(float) * kParamPadded, cudaMemcpyHostToDevice));
+    NRC_CUDA(h, cudaMemcpy(dst, pd.data(), sizeof(float) * pd.size(), cudaMemcpyHostToDevice));
     h->launches = 0;
     if ((s = refresh_images(h, 0)) != NRC_OK) return s;
     NRC_CUDA(h, cudaDeviceSynchronize());

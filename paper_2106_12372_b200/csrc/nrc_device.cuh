@@ -25,6 +25,37 @@ constexpr int kParamPaddedEnd = kParamPadded;
 // start of layer i in the padded parameter layout (i = 6: end)
 __host__ __device__ constexpr int layer_off(int i) { return i < 6 ? i * 4096 : kParamPaddedEnd; }
 constexpr int kImgBytes = kParamPadded * 2;           // 43,008 B fp16 image
+
+// Hidden width W in {32, 64, 128} (width ablation; W = 64 is the
+// paper's network and the layout above).  Layer i has rows(i) outputs (W,
+// W5 padded to 16) and cols(i) inputs (64 for W0, else W).
+//  * fp32 padded arrays: element (i, r, c) at pad_off(i) + r cols(i) + c.
+//  * fp16 operand image: layer i is cols(i)/64 (rounded up) K-blocks of
+//    rows(i) 128-byte lines (64 halves, SWIZZLE_128B chunk order c ^ (r % 8)).
+template <int W>
+struct NetDims {
+    static_assert(W == 32 || W == 64 || W == 128, "hidden width 32, 64 or 128");
+    __host__ __device__ static constexpr int rows(int i) { return i < 5 ? W : kOutPad; }
+    __host__ __device__ static constexpr int cols(int i) { return i == 0 ? 64 : W; }
+    __host__ __device__ static constexpr int kblocks(int i) { return (cols(i) + 63) / 64; }
+    __host__ __device__ static constexpr int pad_off(int i) {
+        return i == 0 ? 0 : i <= 5 ? 64 * W + (i - 1) * W * W : 64 * W + 4 * W * W + kOutPad * W;
+    }
+    // sum over j < i of kblocks(j) rows(j) 128 (closed form: no recursion at run time)
+    __host__ __device__ static constexpr int img_off(int i) {
+        return i == 0 ? 0
+                      : i <= 5 ? W * 128 + (i - 1) * ((W + 63) / 64) * W * 128
+                               : W * 128 + 4 * ((W + 63) / 64) * W * 128 + ((W + 63) / 64) * kOutPad * 128;
+    }
+    static constexpr int kPadded = 64 * W + 4 * W * W + kOutPad * W;
+    static constexpr int kLogical = 64 * W + 4 * W * W + 3 * W;
+    static constexpr int kImg = img_off(6);
+    __host__ __device__ static constexpr uint32_t img_byte(int i, int r, int c) {
+        return uint32_t(img_off(i) + (c >> 6) * rows(i) * 128 + r * 128) +
+               ((uint32_t((c & 63) >> 3) ^ uint32_t(r & 7)) << 4) + uint32_t(c & 7) * 2u;
+    }
+};
+static_assert(NetDims<64>::kPadded == kParamPadded && NetDims<64>::kImg == kImgBytes, "W=64 layout");
 constexpr int kTileBytes = kTile * 128;               // 16 KB per 128x64 fp16 tile
 constexpr int kRecFloats = 16;                        // 64-B record
 

@@ -100,6 +100,18 @@ __global__ void nrc_image_kernel(const float* __restrict__ w, uint8_t* __restric
     *reinterpret_cast<__half*>(img + image_offset(layer, row, col)) = __float2half_rn(w[j]);
 }
 
+// fp32 padded array -> fp16 operand image at hidden width W (NetDims<W>).
+template <int W>
+__global__ void nrc_image_w_kernel(const float* __restrict__ w, uint8_t* __restrict__ img) {
+    using D = NetDims<W>;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= D::kPadded) return;
+    int i = 0;
+    while (i < 5 && j >= D::pad_off(i + 1)) ++i;
+    const int rel = j - D::pad_off(i), r = rel / D::cols(i), c = rel % D::cols(i);
+    *reinterpret_cast<__half*>(img + D::img_byte(i, r, c)) = __float2half_rn(w[j]);
+}
+
 // Sum the per-CTA partials in fixed order into a logical-layout gradient
 // (nrc_train_backward), plus the loss sum.
 // grid = kParamPadded / 32 blocks of kRedThreads (same order as Adam's sum).

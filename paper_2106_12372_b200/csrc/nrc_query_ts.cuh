@@ -18,17 +18,51 @@
 
 namespace nrc {
 
-constexpr int kTsMaxSlots = 5;
-
-template <int G, int S>
-__host__ __device__ constexpr int query_ts_smem_bytes() {
-    return 1024 + kImgBytes + G * kRecTileBytes + 8 * (1 + (S + 1) * G) + 16;
+// TMEM columns per in-flight tile at hidden width W: accumulator W + fp16 A
+// (the 64-wide input for layer 0, W wide after) max(64, W) / 2.
+template <int W>
+__host__ __device__ constexpr int ts_slot_cols() {
+    return W + (W > 64 ? W : 64) / 2;
+}
+template <int W>
+__host__ __device__ constexpr int ts_max_slots() {
+    return 512 / ts_slot_cols<W>();
 }
 
-// G independent 4-warp groups, S tiles in flight per group (G*S <= 5).
-template <int G, int S>
+template <int G, int S, int W = 64>
+__host__ __device__ constexpr int query_ts_smem_bytes() {
+    return 1024 + NetDims<W>::kImg + G * kRecTileBytes + 8 * (1 + (S + 1) * G) + 16;
+}
+
+// One layer's K chain (K/16 MMAs, A in TMEM at a + 8 k, B K-major blocks of
+// 64: b0 for k < 4, b1 for k >= 4), then a commit.  Elected lane only.
+template <int NK>
+__device__ __forceinline__ void umma_ta_chain_commit(uint32_t d, uint32_t a, uint64_t b0, uint64_t b1, uint32_t idesc,
+                                                     uint64_t* bar) {
+    static_assert(NK == 2 || NK == 4 || NK == 8, "K = 32, 64 or 128");
+    if (NK == 4) {
+        umma_chain4_ta_commit(d, a, b0, idesc, bar);
+        return;
+    }
+    umma_f16_ta(d, a, b0, idesc, 0u);
+    umma_f16_ta(d, a + 8, b0 + 2, idesc, 1u);
+    if (NK == 8) {
+        umma_f16_ta(d, a + 16, b0 + 4, idesc, 1u);
+        umma_f16_ta(d, a + 24, b0 + 6, idesc, 1u);
+        umma_f16_ta(d, a + 32, b1, idesc, 1u);
+        umma_f16_ta(d, a + 40, b1 + 2, idesc, 1u);
+        umma_f16_ta(d, a + 48, b1 + 4, idesc, 1u);
+        umma_f16_ta(d, a + 56, b1 + 6, idesc, 1u);
+    }
+    umma_commit(bar);
+}
+
+// G independent 4-warp groups, S tiles in flight per group, hidden width W.
+template <int G, int S, int W = 64>
 __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args) {
-    static_assert(G * S <= kTsMaxSlots, "TMEM holds 5 tiles");
+    static_assert(G * S <= ts_max_slots<W>(), "TMEM holds 512 columns");
+    using D = NetDims<W>;
+    constexpr uint32_t kACols = (W > 64 ? W : 64) / 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     const uint32_t tid = threadIdx.x;
@@ -38,8 +72,8 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     const bool issuer_warp = wq == (g & 3u);
     const bool issuer = r == 32u * (g & 3u);
     uint8_t* sW = smem;
-    const float* sRec = reinterpret_cast<const float*>(smem + kImgBytes + g * kRecTileBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kImgBytes + G * kRecTileBytes);
+    const float* sRec = reinterpret_cast<const float*>(smem + D::kImg + g * kRecTileBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + D::kImg + G * kRecTileBytes);
     uint64_t* wbar = &bars[0];
     uint64_t* mma_bar = &bars[1 + (S + 1) * g];  // [S]
     uint64_t* rec_bar = &bars[1 + (S + 1) * g + S];
@@ -58,8 +92,8 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (tid == 0) {
-        mbar_arrive_expect_tx(wbar, kImgBytes);
-        bulk_g2s(sW, args.wimg, kImgBytes, wbar);
+        mbar_arrive_expect_tx(wbar, D::kImg);
+        bulk_g2s(sW, args.wimg, D::kImg, wbar);
     }
 
     const uint64_t n = args.n;
@@ -81,16 +115,27 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
 
     const uint32_t sW_a = smem_u32(sW);
     const uint32_t lane_off = (wq * 32u) << 16;
-    auto d_col = [&](int s) -> uint32_t { return tmem_base + 64u * uint32_t(g * S + s); };
-    auto a_col = [&](int s) -> uint32_t { return tmem_base + 320u + 32u * uint32_t(g * S + s); };
+    // D regions first (W columns each), then the A regions
+    auto d_col = [&](int s) -> uint32_t { return tmem_base + uint32_t(W) * uint32_t(g * S + s); };
+    auto a_col = [&](int s) -> uint32_t {
+        return tmem_base + uint32_t(W * G * S) + kACols * uint32_t(g * S + s);
+    };
     // called by the whole issuer warp (converged)
     auto issue_layer = [&](int s, int L) {
-        const uint32_t wl = sW_a + layer_off(L) * 2;
-        const uint32_t idesc = (L < 5) ? make_idesc(128, 64, 0, 0) : make_idesc(128, 16, 0, 0);
+        const uint32_t wl = sW_a + uint32_t(D::img_off(L));
+        const uint32_t idesc = make_idesc(128, D::rows(L), 0, 0);
         const uint32_t d = warp_uniform(d_col(s)), a = warp_uniform(a_col(s));
-        const uint64_t b = warp_uniform(desc_kmajor(wl, 0));
+        const uint64_t b0 = warp_uniform(desc_kmajor(wl, 0));
+        const uint64_t b1 = warp_uniform(desc_kmajor(wl + uint32_t(D::rows(L)) * 128u, 0));
         tc_fence_after();
-        if (elect_one()) umma_chain4_ta_commit(d, a, b, idesc, &mma_bar[s]);
+        if (elect_one()) {
+            if (D::cols(L) == 32)
+                umma_ta_chain_commit<2>(d, a, b0, b1, idesc, &mma_bar[s]);
+            else if (D::cols(L) == 64)
+                umma_ta_chain_commit<4>(d, a, b0, b1, idesc, &mma_bar[s]);
+            else
+                umma_ta_chain_commit<8>(d, a, b0, b1, idesc, &mma_bar[s]);
+        }
         __syncwarp();
     };
 
@@ -182,14 +227,14 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
             if (layer[s] < 5) {
                 // h_{L+1} = relu(acc) -> fp16, written over h_L in the slot's TMEM A
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
+                for (int part = 0; part < W / 32; ++part) {
                     uint32_t v[32];
-                    tmem_ld32(t_d + 32 * half, v);
+                    tmem_ld32(t_d + 32 * part, v);
                     uint32_t hp[16];
 #pragma unroll
                     for (int q = 0; q < 16; ++q)
                         hp[q] = pack_h2_relu(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
-                    tmem_st16_nowait(a_col(s) + lane_off + 16 * half, hp);
+                    tmem_st16_nowait(a_col(s) + lane_off + 16 * part, hp);
                 }
                 tmem_wait_st();
 

@@ -116,6 +116,7 @@ class RadianceCache:
         if st != 0:
             raise NRCError(f"nrc_init failed: {self.L.nrc_status_string(st).decode()}")
         self.h = h
+        self.nparam = int(self.L.nrc_param_count(self.h))  # logical parameters at this hidden width
 
     # ------------------------------------------------------------------ helpers
     def _check(self, st: int, what: str):
@@ -220,15 +221,17 @@ class RadianceCache:
         return out
 
     def get_params(self, which: str = "train") -> np.ndarray:
-        out = np.zeros(NPARAM, np.float32)
-        self._check(self.L.nrc_get_params(self.h, _PARAM_SETS[which], out.ctypes.data, NPARAM), "nrc_get_params")
+        out = np.zeros(self.nparam, np.float32)
+        self._check(self.L.nrc_get_params(self.h, _PARAM_SETS[which], out.ctypes.data, self.nparam),
+                    "nrc_get_params")
         return out
 
     def set_params(self, values, which: str = "train"):
         v = np.ascontiguousarray(values, dtype=np.float32).reshape(-1)
-        if v.size != NPARAM:
-            raise NRCError(f"expected {NPARAM} parameters")
-        self._check(self.L.nrc_set_params(self.h, _PARAM_SETS[which], v.ctypes.data, NPARAM), "nrc_set_params")
+        if v.size != self.nparam:
+            raise NRCError(f"expected {self.nparam} parameters")
+        self._check(self.L.nrc_set_params(self.h, _PARAM_SETS[which], v.ctypes.data, self.nparam),
+                    "nrc_set_params")
 
     def stats(self) -> dict:
         a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
