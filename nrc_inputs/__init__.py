@@ -101,3 +101,37 @@ def train_frame(frame: int = 0, n: int = TRAIN_S * TRAIN_L, noise: float = 0.0):
 
 def query_batch(n: int = N_1080P, seed: int = SEED_QUERY) -> np.ndarray:
     return records(n, seed)
+
+
+SEED_PATHS = 0x5E1F
+
+
+def training_paths(n_vertices: int = TRAIN_S * TRAIN_L, seed: int = SEED_PATHS, u_inv: int = 16):
+    """Synthetic training-path buffers for self-training target assembly
+    (SURVEY 8(f) N1).  Path lengths are geometric
+    (mean ~3, the paper's short suffixes plus the training extension), cut so
+    the vertex count is exactly n_vertices.  Per vertex 9 floats [E N T]:
+    emission E (5 % of vertices are emitters, E ~ U[0, 4)), next-event estimate
+    N ~ U[0, 0.5), throughput T ~ U[0, 0.9) (energy conserving).  Every
+    u_inv-th path (index % u_inv == 0) is flagged unbiased (flag bit 0,
+    P:L341-343).  Returns (first, length, flags, vert [n, 9] f32, vertex
+    records [n, 16] f32, tail records [n_paths, 16] f32).  Data only: no
+    arithmetic of the method."""
+    rng = np.random.default_rng(seed)
+    lens = []
+    total = 0
+    while total < n_vertices:
+        k = int(min(rng.geometric(1.0 / 3.0), 12, n_vertices - total))
+        lens.append(k)
+        total += k
+    length = np.asarray(lens, np.uint32)
+    first = np.concatenate([[0], np.cumsum(length)[:-1]]).astype(np.uint32)
+    flags = (np.arange(length.size) % u_inv == 0).astype(np.uint32)
+    vert = np.zeros((n_vertices, 9), np.float32)
+    emit = rng.random(n_vertices) < 0.05
+    vert[:, 0:3] = np.where(emit[:, None], rng.uniform(0, 4, (n_vertices, 3)), 0.0)
+    vert[:, 3:6] = rng.uniform(0, 0.5, (n_vertices, 3))
+    vert[:, 6:9] = rng.uniform(0, 0.9, (n_vertices, 3))
+    vrec = records(n_vertices, seed=seed + 1)
+    trec = records(length.size, seed=seed + 2)
+    return first, length, flags, vert, vrec, trec

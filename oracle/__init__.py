@@ -82,6 +82,8 @@ def lib():
         L.orc_query_batch_w.restype = None
         L.orc_query_batch_w.argtypes = [ctypes.c_int, vp, vp, i64, vp, vp, ctypes.c_uint, vp]
         L.orc_init_weights_w.restype = None; L.orc_init_weights_w.argtypes = [ctypes.c_int, u64, vp]
+        L.orc_assemble_targets.restype = None
+        L.orc_assemble_targets.argtypes = [vp, vp, vp, i64, vp, vp, vp]
         L.orc_train_step.restype = d
         L.orc_train_step.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp, d, ctypes.c_uint,
                                      d, d, d, d, d, ctypes.c_int, vp, vp, vp]
@@ -179,6 +181,17 @@ def init_weights_w(hw: int, seed: int) -> np.ndarray:
     W = np.zeros(param_count_w(hw), np.float32)
     lib().orc_init_weights_w(int(hw), int(seed) & (2**64 - 1), W.ctypes.data)
     return W
+
+
+# ---------------------------------------------------------------- self-training targets (N1)
+def assemble_targets(first, length, flags, vert, tail) -> np.ndarray:
+    """Per-vertex targets [n_vertices, 3] (fp64) of orc_assemble_targets."""
+    first = _c(first, np.uint32); length = _c(length, np.uint32); flags = _c(flags, np.uint32)
+    vert = _c(vert, np.float32).reshape(-1, 9); tail = _c(tail, np.float32).reshape(-1, 3)
+    out = np.zeros((vert.shape[0], 3), np.float64)
+    lib().orc_assemble_targets(first.ctypes.data, length.ctypes.data, flags.ctypes.data, first.size,
+                               vert.ctypes.data, tail.ctypes.data, out.ctypes.data)
+    return out
 
 
 def loss(yhat, t, eps=0.01):

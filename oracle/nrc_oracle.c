@@ -23,6 +23,8 @@
  *       forms, SPEC worked examples, periodicity, integral of quartic = 1)
  *   orc_encode ............................................. pinned (golden
  *       vector tests/golden/encode_c0.txt, structural invariants)
+ *   orc_assemble_targets ................................... pinned (one-vertex
+ *       closed form, unbiased flag, hand-evaluated 3-vertex path, linearity)
  *   orc_forward_w / orc_query_batch_w / orc_init_weights_w . pinned (width
  *       embedding into the 64 net, numpy matmul chain, Glorot moments)
  *   orc_forward / orc_query ................................ pinned (zero net,
@@ -483,6 +485,33 @@ uint64_t orc_lcg_perm(uint64_t i, uint64_t n, uint64_t a, uint64_t c, uint64_t m
 void orc_lcg_permute(uint64_t n, uint64_t a, uint64_t c, uint64_t m, uint64_t* out)
 {
     for (uint64_t i = 0; i < n; ++i) out[i] = orc_lcg_perm(i, n, a, c, m);
+}
+
+/* ---- self-training targets.
+ * A training path has vertices v_0 .. v_{m-1} (camera side first).  Per vertex:
+ * emitted radiance E_i, next-event estimate N_i and the path throughput T_i
+ * (BSDF * cos / pdf) from v_i towards v_{i+1}, each RGB, stored as 9 floats
+ * [E N T].  The path's tail radiance L_tail is the cache's prediction at the
+ * terminal vertex (self-training) or 0 for the unbiased fraction
+ * u = 1/16 of paths terminated by Russian roulette only (flag bit
+ * 0).  The target of each vertex is the radiance transported back to it:
+ *   target(v_{m-1}) = E + N + T (.) L_tail
+ *   target(v_i)     = E_i + N_i + T_i (.) target(v_{i+1}),   i = m-2 .. 0. */
+void orc_assemble_targets(const uint32_t* first, const uint32_t* len, const uint32_t* flags, int64_t n_paths,
+                          const float* vert, const float* tail, double* targets)
+{
+    for (int64_t p = 0; p < n_paths; ++p) {
+        double acc[3];
+        for (int c = 0; c < 3; ++c) acc[c] = (flags[p] & 1u) ? 0.0 : (double)tail[3 * p + c];
+        for (int64_t k = (int64_t)len[p] - 1; k >= 0; --k) {
+            const int64_t v = (int64_t)first[p] + k;
+            const float* x = vert + 9 * v;
+            for (int c = 0; c < 3; ++c) {
+                acc[c] = (double)x[c] + (double)x[3 + c] + (double)x[6 + c] * acc[c];
+                targets[3 * v + c] = acc[c];
+            }
+        }
+    }
 }
 
 /* ---- initialisation (reading R16): Glorot-uniform from a
