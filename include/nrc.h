@@ -187,6 +187,21 @@ nrc_status nrc_lcg_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* c, u
  * order).  Same device function the fused kernels use. */
 nrc_status nrc_encode(nrc_handle* h, const nrc_record* d_rec, uint64_t n, uint16_t* d_out, void* stream);
 
+/* Self-training targets.  Training
+ * path p owns vertices d_first[p] .. d_first[p] + d_len[p] - 1 (camera side
+ * first); d_vert holds 9 fp32 per vertex: emitted radiance E, next-event
+ * estimate N and throughput T towards the next vertex (RGB each).  d_tail:
+ * 3 fp32 per path, the cache's radiance at the path's terminal vertex (e.g.
+ * from nrc_query on the tail records); ignored for paths with bit 0 of
+ * d_flags set (the unbiased fraction u = 1/16 terminated by Russian roulette
+ * only).  Writes d_targets (3 fp32 per vertex):
+ *   target(last) = E + N + T * tail,  target(v_i) = E_i + N_i + T_i * target(v_{i+1})
+ * in fp32 (fmaf).  All pointers device, 4-byte aligned; vertex ranges must lie
+ * in [0, n_vertices).  One kernel launch (one thread per path). */
+nrc_status nrc_assemble_targets(nrc_handle* h, const uint32_t* d_first, const uint32_t* d_len,
+                                const uint32_t* d_flags, uint32_t n_paths, const float* d_vert,
+                                const float* d_tail, float* d_targets, void* stream);
+
 /* Parameter I/O in the logical layout (nrc_param_count() fp32 host floats).
  * nrc_set_params(NRC_PARAMS_TRAIN) also refreshes the fp16 image of W;
  * nrc_set_params(NRC_PARAMS_EMA) refreshes the fp16 image of W-bar.

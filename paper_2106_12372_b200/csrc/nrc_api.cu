@@ -147,6 +147,8 @@ struct nrc_handle {
     unsigned long long gbar = 0;  // arrivals so far on the train kernel's grid-barrier counter
     bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
+    int query_ctas = 0;           // cap on the query grid (0: all SMs)
+    int train_ctas = 0;           // cap on the train grid (0: one CTA per tile up to all SMs)
     float* d_w() { return reinterpret_cast<float*>(state + L.w); }
     float* d_m() { return reinterpret_cast<float*>(state + L.m); }
     float* d_v() { return reinterpret_cast<float*>(state + L.v); }
@@ -371,6 +373,8 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     }
     h->query_cfg = 0;
     if (const char* e = std::getenv("NRC_COOP")) h->coop = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NRC_QUERY_CTAS")) h->query_ctas = std::atoi(e);
+    if (const char* e = std::getenv("NRC_TRAIN_CTAS")) h->train_ctas = std::atoi(e);
     if (const char* e = std::getenv("NRC_QUERY_CFG")) h->query_cfg = std::atoi(e);
     if (h->query_cfg < 0 || h->query_cfg >= kNumQueryCfgs) h->query_cfg = 0;
     for (int i = 0; i < kNumQueryCfgs; ++i)
@@ -447,7 +451,8 @@ nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* 
     const uint64_t ntiles = (n + kTile - 1) / kTile;
     const uint64_t G = uint64_t(qe.groups);
     const uint64_t ctas = (ntiles + G - 1) / G;  // one tile stream per group
-    const int grid = int(ctas < uint64_t(h->num_sms) ? ctas : uint64_t(h->num_sms));
+    const uint64_t cap = h->query_ctas > 0 && h->query_ctas < h->num_sms ? uint64_t(h->query_ctas) : uint64_t(h->num_sms);
+    const int grid = int(ctas < cap ? ctas : cap);
     qe.launch(grid, qa, static_cast<cudaStream_t>(stream));
     NRC_LAUNCHED(h, "nrc_query_kernel");
     return NRC_OK;
@@ -507,7 +512,8 @@ static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const flo
     ta.dbg = h->dbg;
     const uint32_t ntiles = (n + kTile - 1) / kTile;
     int grid = int(ntiles);
-    const int cap = h->num_sms < kMaxPartials ? h->num_sms : kMaxPartials;
+    int cap = h->num_sms < kMaxPartials ? h->num_sms : kMaxPartials;
+    if (h->train_ctas > 0 && h->train_ctas < cap) cap = h->train_ctas;
     if (grid > cap) grid = cap;
     *nparts = grid;
     if (nsteps == 0) {
@@ -704,6 +710,23 @@ nrc_status nrc_encode(nrc_handle* h, const nrc_record* d_rec, uint64_t n, uint16
     nrc_encode_kernel<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const float*>(d_rec), n,
                                                                               h->ep, reinterpret_cast<uint4*>(d_out));
     NRC_LAUNCHED(h, "nrc_encode_kernel");
+    return NRC_OK;
+}
+
+nrc_status nrc_assemble_targets(nrc_handle* h, const uint32_t* d_first, const uint32_t* d_len,
+                                const uint32_t* d_flags, uint32_t n_paths, const float* d_vert,
+                                const float* d_tail, float* d_targets, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n_paths == 0) return NRC_OK;
+    if (!d_first || !d_len || !d_flags || !d_vert || !d_tail || !d_targets || !aligned(d_first, 4) ||
+        !aligned(d_len, 4) || !aligned(d_flags, 4) || !aligned(d_vert, 4) || !aligned(d_tail, 4) ||
+        !aligned(d_targets, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_assemble_targets: NULL or misaligned pointer");
+    nrc_targets_kernel<<<(n_paths + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_first, d_len, d_flags, n_paths, d_vert, d_tail, d_targets);
+    NRC_LAUNCHED(h, "nrc_targets_kernel");
     return NRC_OK;
 }
 

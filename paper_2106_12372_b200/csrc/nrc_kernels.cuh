@@ -133,6 +133,30 @@ __global__ void __launch_bounds__(kRedThreads) nrc_reduce_kernel(const float* __
     if (li >= 0) grad[li] = g;
 }
 
+// Self-training targets (nrc_assemble_targets): one thread per training path,
+// back to front: acc = E + N + T * acc.
+__global__ void nrc_targets_kernel(const uint32_t* __restrict__ first, const uint32_t* __restrict__ len,
+                                   const uint32_t* __restrict__ flags, uint32_t n_paths,
+                                   const float* __restrict__ vert, const float* __restrict__ tail,
+                                   float* __restrict__ targets) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_paths) return;
+    const bool unbiased = (__ldg(flags + p) & 1u) != 0;
+    float acc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] = unbiased ? 0.0f : __ldg(tail + 3 * size_t(p) + c);
+    const uint32_t f = __ldg(first + p), m = __ldg(len + p);
+    for (uint32_t k = m; k-- > 0;) {
+        const float* x = vert + 9 * size_t(f + k);
+        float* t = targets + 3 * size_t(f + k);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            acc[c] = fmaf(__ldg(x + 6 + c), acc[c], __ldg(x + c) + __ldg(x + 3 + c));
+            t[c] = acc[c];
+        }
+    }
+}
+
 // Encoding only (nrc_encode): one thread per record, logical feature order.
 __global__ void nrc_encode_kernel(const float* __restrict__ rec, uint64_t n, EncodeParams ep, uint4* __restrict__ out) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -212,6 +212,33 @@ class RadianceCache:
                     "nrc_train_frame_backward")
         return grad, loss_sum
 
+    def assemble_targets(self, first: torch.Tensor, length: torch.Tensor, flags: torch.Tensor,
+                         vert: torch.Tensor, tail: torch.Tensor, targets: Optional[torch.Tensor] = None,
+                         stream=None) -> torch.Tensor:
+        """Self-training targets: per-vertex radiance transported
+        back from each training path's tail (see nrc_assemble_targets)."""
+        n_paths = first.shape[0]
+        for t, name in ((first, "first"), (length, "length"), (flags, "flags")):
+            if t.device != self.device or t.dtype != torch.int32 or tuple(t.shape) != (n_paths,) \
+                    or not t.is_contiguous():
+                raise NRCError(f"{name} must be a contiguous int32 [{n_paths}] tensor on the cache's device")
+        nv = vert.shape[0]
+        self._f32(vert, (nv, 9), "vert")
+        self._f32(tail, (n_paths, 3), "tail")
+        if targets is None:
+            targets = torch.empty((nv, 3), dtype=torch.float32, device=self.device)
+        self._f32(targets, (nv, 3), "targets")
+        self._check(self.L.nrc_assemble_targets(self.h, _ptr(first), _ptr(length), _ptr(flags), int(n_paths),
+                                                _ptr(vert), _ptr(tail), _ptr(targets), _stream(stream)),
+                    "nrc_assemble_targets")
+        return targets
+
+    def self_training_targets(self, first, length, flags, vert, tail_records, stream=None) -> torch.Tensor:
+        """Query the cache at every path's terminal vertex (nrc_query, the
+        ~1 % extra queries of P:L1030-1032), then assemble the targets."""
+        tail = self.query(tail_records, stream=stream)
+        return self.assemble_targets(first, length, flags, vert, tail, stream=stream)
+
     def encode(self, records: torch.Tensor, stream=None) -> torch.Tensor:
         """The 64-dim fp16 network input of each record (Table 1 + padding)."""
         records = self._rec(records)
