@@ -82,6 +82,8 @@ def lib():
         L.orc_query_batch_w.restype = None
         L.orc_query_batch_w.argtypes = [ctypes.c_int, vp, vp, i64, vp, vp, ctypes.c_uint, vp]
         L.orc_init_weights_w.restype = None; L.orc_init_weights_w.argtypes = [ctypes.c_int, u64, vp]
+        L.orc_query_accumulate.restype = None
+        L.orc_query_accumulate.argtypes = [vp, vp, i64, vp, vp, ctypes.c_uint, vp, vp, vp]
         L.orc_assemble_targets.restype = None
         L.orc_assemble_targets.argtypes = [vp, vp, vp, i64, vp, vp, vp]
         L.orc_train_step.restype = d
@@ -181,6 +183,20 @@ def init_weights_w(hw: int, seed: int) -> np.ndarray:
     W = np.zeros(param_count_w(hw), np.float32)
     lib().orc_init_weights_w(int(hw), int(seed) & (2**64 - 1), W.ctypes.data)
     return W
+
+
+# ---------------------------------------------------------------- pixel reconstruction (N2)
+def query_accumulate(W, recs, pix, thr, image, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1),
+                     flags=FACTORIZE | CLAMP_QUERY) -> np.ndarray:
+    """image [n_pixels, 3] fp64 (updated copy) += thr * query(recs) at pix."""
+    W = _c(W, np.float64)
+    recs = _c(recs, np.float32).reshape(-1, 16)
+    pix = _c(pix, np.uint32); thr = _c(thr, np.float32).reshape(-1, 3)
+    img = np.array(image, np.float64, copy=True, order="C")
+    lo, hi = _c(aabb_lo, np.float32), _c(aabb_hi, np.float32)
+    lib().orc_query_accumulate(W.ctypes.data, recs.ctypes.data, recs.shape[0], lo.ctypes.data, hi.ctypes.data,
+                               int(flags), pix.ctypes.data, thr.ctypes.data, img.ctypes.data)
+    return img
 
 
 # ---------------------------------------------------------------- self-training targets (N1)

@@ -23,6 +23,8 @@
  *       forms, SPEC worked examples, periodicity, integral of quartic = 1)
  *   orc_encode ............................................. pinned (golden
  *       vector tests/golden/encode_c0.txt, structural invariants)
+ *   orc_query_accumulate ................................... pinned (unit
+ *       throughput + identity pixels = query, permutation, accumulation)
  *   orc_assemble_targets ................................... pinned (one-vertex
  *       closed form, unbiased flag, hand-evaluated 3-vertex path, linearity)
  *   orc_forward_w / orc_query_batch_w / orc_init_weights_w . pinned (width
@@ -280,6 +282,20 @@ void orc_query_batch_w(int hw, const double* W, const float* recs, int64_t n, co
             q[3 * i + c] = v;
         }
     }
+}
+
+/* Pixel reconstruction from the cache: the
+ * rendering path of pixel pix[i] ends in cache query i; its radiance reaches
+ * the pixel through the path throughput T_i:  image[pix[i]] += T_i (.) q_i,
+ * q = orc_query_batch.  Sequential in i (the order of the adds is fixed). */
+void orc_query_accumulate(const double* W, const float* recs, int64_t n, const float* lo, const float* hi,
+                          unsigned flags, const uint32_t* pix, const float* thr, double* image)
+{
+    double* q = (double*)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+    orc_query_batch(W, recs, n, lo, hi, flags, q);
+    for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < 3; ++c) image[3 * (int64_t)pix[i] + c] += (double)thr[3 * i + c] * q[3 * i + c];
+    free(q);
 }
 
 /* ---- relative L2 loss, Eq.(5) ---------------------------------

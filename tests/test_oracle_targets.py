@@ -52,3 +52,24 @@ def test_linearity_in_tail(orc):
     for p in np.nonzero(flags)[0][:20]:
         s = slice(int(first[p]), int(first[p] + length[p]))
         np.testing.assert_array_equal(ta[s], zero[s])
+
+
+def test_query_accumulate_pins(orc):
+    """orc_query_accumulate: unit throughput on distinct pixels of
+    a zero image reproduces the query; a pixel permutation permutes the image;
+    two records on one pixel add; a zero throughput leaves the image."""
+    recs = nrc_inputs.records(200, seed=5)
+    W = orc.init_weights(3).astype(np.float64) * 1.3
+    q = orc.query(W, recs)
+    ones = np.ones((200, 3), np.float32)
+    img = orc.query_accumulate(W, recs, np.arange(200), ones, np.zeros((200, 3)))
+    np.testing.assert_array_equal(img, q)
+    perm = np.random.default_rng(0).permutation(200)
+    img_p = orc.query_accumulate(W, recs, perm, ones, np.zeros((200, 3)))
+    np.testing.assert_array_equal(img_p[perm], q)
+    both = orc.query_accumulate(W, recs[:2], np.array([7, 7]), np.full((2, 3), 0.5, np.float32),
+                                np.ones((10, 3)))
+    np.testing.assert_allclose(both[7], 1.0 + 0.5 * q[0] + 0.5 * q[1], rtol=1e-15)
+    np.testing.assert_array_equal(np.delete(both, 7, axis=0), 1.0)
+    z = orc.query_accumulate(W, recs, np.arange(200), np.zeros((200, 3), np.float32), np.full((200, 3), 2.0))
+    np.testing.assert_array_equal(z, 2.0)
