@@ -136,6 +136,16 @@ nrc_status nrc_destroy(nrc_handle* h);
  * kernel: encode -> 6 tcgen05 layers -> factorisation epilogue. */
 nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* d_rgb, void* stream);
 
+/* Query with the pixel reconstruction fused into the epilogue (
+ * SURVEY 8(f) N2): the rendering path of pixel d_pixel[i] ends in cache query
+ * i, whose radiance q_i (as nrc_query computes it) reaches the pixel through
+ * the path throughput d_thr[3i..3i+2]:  d_image[3 d_pixel[i] + c] += d_thr[3i + c] q_ic.
+ * d_image is an fp32 RGB image the caller owns and zeroes; the adds are
+ * atomic (deterministic when the pixel indices are distinct, the one-query-
+ * per-pixel case).  No radiance array is written. */
+nrc_status nrc_query_accumulate(nrc_handle* h, const nrc_record* d_rec, uint64_t n, const uint32_t* d_pixel,
+                                const float* d_thr, float* d_image, void* stream);
+
 /* One optimisation step on a batch: forward, relative
  * L2 loss (Eq. 5) of the factored prediction, backward, Adam on the batch-
  * mean gradient, EMA update.  d_rec: n records; d_tgt: 3n fp32 targets;

@@ -430,15 +430,9 @@ static nrc_status check_handle(nrc_handle* h) {
     return NRC_OK;
 }
 
-nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* d_rgb, void* stream) {
-    nrc_status s = check_handle(h);
-    if (s != NRC_OK) return s;
-    h->launches = 0;
-    if (n == 0) return NRC_OK;
-    if (!d_rec || !d_rgb || !aligned(d_rec, 16) || !aligned(d_rgb, 4))
-        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query: NULL or misaligned pointer");
-    if (n > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query: n > max_batch");
-    QueryArgs qa;
+static nrc_status query_impl(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* d_rgb, const uint32_t* d_pix,
+                             const float* d_thr, float* d_image, void* stream) {
+    QueryArgs qa{};
     qa.rec = reinterpret_cast<const float*>(d_rec);
     qa.out = d_rgb;
     qa.n = n;
@@ -447,7 +441,12 @@ nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* 
     qa.ep = h->ep;
     qa.flags = h->cfg.flags & (NRC_FACTORIZE | NRC_CLAMP_QUERY);
     qa.dbg = h->dbg;
-    const QueryEntry& qe = h->wi.W == 32 ? kQueryW32 : h->wi.W == 128 ? kQueryW128 : kQueryCfgs[h->query_cfg];
+    qa.pix = d_pix;
+    qa.thr = d_thr;
+    qa.image = d_image;
+    // the fused accumulate epilogue exists in the TMEM kernels only (entry 0 and the width kernels)
+    const int cfg = d_image ? 0 : h->query_cfg;
+    const QueryEntry& qe = h->wi.W == 32 ? kQueryW32 : h->wi.W == 128 ? kQueryW128 : kQueryCfgs[cfg];
     const uint64_t ntiles = (n + kTile - 1) / kTile;
     const uint64_t G = uint64_t(qe.groups);
     const uint64_t ctas = (ntiles + G - 1) / G;  // one tile stream per group
@@ -456,6 +455,30 @@ nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* 
     qe.launch(grid, qa, static_cast<cudaStream_t>(stream));
     NRC_LAUNCHED(h, "nrc_query_kernel");
     return NRC_OK;
+}
+
+nrc_status nrc_query(nrc_handle* h, const nrc_record* d_rec, uint64_t n, float* d_rgb, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n == 0) return NRC_OK;
+    if (!d_rec || !d_rgb || !aligned(d_rec, 16) || !aligned(d_rgb, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query: NULL or misaligned pointer");
+    if (n > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query: n > max_batch");
+    return query_impl(h, d_rec, n, d_rgb, nullptr, nullptr, nullptr, stream);
+}
+
+nrc_status nrc_query_accumulate(nrc_handle* h, const nrc_record* d_rec, uint64_t n, const uint32_t* d_pixel,
+                                const float* d_thr, float* d_image, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (n == 0) return NRC_OK;
+    if (!d_rec || !d_pixel || !d_thr || !d_image || !aligned(d_rec, 16) || !aligned(d_pixel, 4) ||
+        !aligned(d_thr, 4) || !aligned(d_image, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query_accumulate: NULL or misaligned pointer");
+    if (n > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query_accumulate: n > max_batch");
+    return query_impl(h, d_rec, n, nullptr, d_pixel, d_thr, d_image, stream);
 }
 
 struct Gather {

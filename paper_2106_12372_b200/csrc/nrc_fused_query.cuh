@@ -27,6 +27,11 @@ struct QueryArgs {
     EncodeParams ep;
     uint32_t flags;      // NRC_FACTORIZE | NRC_CLAMP_QUERY
     long long* dbg;      // per-round clock64 trace (builds with -DNRC_TRACE_QUERY only), else unused
+    // fused pixel reconstruction (nrc_query_accumulate, TMEM kernel only): if
+    // image != nullptr, image[3 pix[i] + c] += thr[3 i + c] * q_c instead of out
+    const uint32_t* pix;
+    const float* thr;
+    float* image;
 };
 
 constexpr int kRecTileBytes = kTile * kRecFloats * 4;  // 8 KB of records per tile

@@ -254,12 +254,21 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
                 tmem_ld4(t_d, v);
                 tc_fence_before();
                 if (row[s] < n) {
-                    float* o = args.out + row[s] * 3;
+                    float qv[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        float qv = __uint_as_float(v[c]) * fac[s][c];
-                        if (args.flags & 2u) qv = fmaxf(qv, 0.0f);
-                        o[c] = qv;
+                        qv[c] = __uint_as_float(v[c]) * fac[s][c];
+                        if (args.flags & 2u) qv[c] = fmaxf(qv[c], 0.0f);
+                    }
+                    if (args.image == nullptr) {
+                        float* o = args.out + row[s] * 3;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) o[c] = qv[c];
+                    } else {  // pixel += throughput * radiance
+                        float* px = args.image + size_t(__ldg(args.pix + row[s])) * 3;
+                        const float* th = args.thr + row[s] * 3;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) atomicAdd(px + c, __ldg(th + c) * qv[c]);
                     }
                 }
                 layer[s] = 0;

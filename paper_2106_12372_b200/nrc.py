@@ -212,6 +212,23 @@ class RadianceCache:
                     "nrc_train_frame_backward")
         return grad, loss_sum
 
+    def query_accumulate(self, records: torch.Tensor, pixel: torch.Tensor, throughput: torch.Tensor,
+                         image: torch.Tensor, stream=None) -> torch.Tensor:
+        """image[pixel[i]] += throughput[i] * radiance(records[i]) (P:L478-483),
+        fused into the query epilogue (nrc_query_accumulate)."""
+        records = self._rec(records)
+        n = records.shape[0]
+        if pixel.device != self.device or pixel.dtype != torch.int32 or tuple(pixel.shape) != (n,) \
+                or not pixel.is_contiguous():
+            raise NRCError(f"pixel must be a contiguous int32 [{n}] tensor on the cache's device")
+        self._f32(throughput, (n, 3), "throughput")
+        if image.device != self.device or image.dtype != torch.float32 or image.dim() != 2 or image.shape[1] != 3 \
+                or not image.is_contiguous():
+            raise NRCError("image must be a contiguous float32 [n_pixels, 3] tensor on the cache's device")
+        self._check(self.L.nrc_query_accumulate(self.h, _ptr(records), n, _ptr(pixel), _ptr(throughput), _ptr(image),
+                                                _stream(stream)), "nrc_query_accumulate")
+        return image
+
     def assemble_targets(self, first: torch.Tensor, length: torch.Tensor, flags: torch.Tensor,
                          vert: torch.Tensor, tail: torch.Tensor, targets: Optional[torch.Tensor] = None,
                          stream=None) -> torch.Tensor:

@@ -50,3 +50,32 @@ def test_self_training_targets_end_to_end(nrc, orc):
     # the targets train the cache: one frame on the self-trained records
     losses = c.train_frame(dev(vrec), torch.from_numpy(got).cuda(), 4, 4096, 5).cpu().numpy()
     assert np.all(np.isfinite(losses))
+
+
+def test_query_accumulate_parity(nrc, orc):
+    """nrc_query_accumulate vs the oracle: 1080p-sized
+    batch with one query per pixel in shuffled pixel order, throughputs in
+    [0, 1), accumulated onto a non-zero image."""
+    n = 300000
+    recs = nrc_inputs.records(n, seed=91)
+    rng = np.random.default_rng(2)
+    pix = rng.permutation(n).astype(np.int32)
+    thr = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    img0 = rng.uniform(0, 0.1, (n, 3)).astype(np.float32)
+    c = nrc.RadianceCache()
+    tr, tg = nrc_inputs.train_frame(0, n=16384)
+    c.train_frame(dev(tr), dev(tg), 4, 4096, 3)
+    image = dev(img0.copy())
+    c.query_accumulate(dev(recs), dev(pix), dev(thr), image)
+    got = image.cpu().numpy()
+    idx = np.linspace(0, n - 1, 6000).astype(np.int64)
+    ref = orc.query_accumulate(c.get_params("ema").astype(np.float64), recs[idx], pix[idx], thr[idx],
+                               img0.astype(np.float64))
+    # compare the touched pixels' increments against the radiance tolerance
+    touched = pix[idx]
+    assert max(radiance_err(got[touched] - img0[touched], ref[touched] - img0[touched])) <= TOL_RADIANCE
+    # bitwise consistency with the unfused path: image + thr * query
+    q = c.query(dev(recs)).cpu().numpy()
+    expect = img0.copy()
+    expect[pix] += thr * q
+    np.testing.assert_array_equal(got, expect)
