@@ -145,6 +145,7 @@ struct nrc_handle {
     int query_cfg;
     long long* dbg = nullptr;  // diagnostics only (nrc_debug_set_trace)
     unsigned long long gbar = 0;  // arrivals so far on the train kernel's grid-barrier counter
+    unsigned long long gbarA = 0; // arrivals so far on its phase-A (W3..W5 partials written) counter
     bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
@@ -565,12 +566,15 @@ static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const flo
     ta.losses = d_losses;
     ta.gbar = h->d_counters() + 2;
     ta.gbar_base = h->gbar;
+    ta.gbarA = h->d_counters() + 3;
+    ta.gbarA_base = h->gbarA;
     if (h->coop)
         NRC_CUDA(h, launch_coop(nrc_train_kernel, dim3(grid), dim3(kTrainBlock), kTrainSmemBytes, st, ta));
     else
         nrc_train_kernel<<<grid, kTrainBlock, kTrainSmemBytes, st>>>(ta);
     NRC_LAUNCHED(h, "nrc_train_kernel");
     h->gbar += 2ull * nsteps * uint64_t(grid);
+    h->gbarA += uint64_t(nsteps) * uint64_t(grid);
     h->step += nsteps;
     return NRC_OK;
 }

@@ -43,6 +43,8 @@ struct TrainArgs {
     float* losses;            // nsteps batch-mean losses (optional)
     unsigned long long* gbar; // grid-barrier counter (monotonic across launches)
     unsigned long long gbar_base;
+    unsigned long long* gbarA;  // arrivals of CTAs whose W3..W5 partials are written (phase A)
+    unsigned long long gbarA_base;
 };
 
 // SMEM: weight image | h0..h5 stash (6 tiles) | 3 rotating gradient tiles |
@@ -50,7 +52,10 @@ struct TrainArgs {
 // wgrad_i (which reads h_i and g_{i+1}) can still be in flight while the
 // epilogue of a later round writes another gradient buffer.  In fused mode
 // the stash + gradient tiles (144 KB) double as the optimiser's staging area.
-constexpr int kTrainSmemBytes = 1024 + kImgBytes + 10 * kTileBytes + 64 + 64;
+constexpr int kPhaseAScratch = 4096;  // helper-warp group sums (phase A)
+constexpr int kTrainSmemBytes = 1024 + kImgBytes + 10 * kTileBytes + 64 + 64 + kPhaseAScratch;
+constexpr int kHelpThreads = 224;      // warps 5..11
+constexpr int kChunkSplit = 3 * 4096 / 4;  // chunks of W0..W2 (phase B) | W3..W5 (phase A)
 constexpr uint32_t kTrainTmemCols = 512;  // acc 64 + 6 wgrad accumulators x 64
 constexpr int kTrainThreads = 160;        // tile threads: 4 row warps + 1 wgrad-issue warp
 constexpr int kTrainBlock = 384;          // + 7 warps that only join the fused optimiser
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     const uint32_t tid = threadIdx.x, r = tid, warp = tid >> 5, lane = tid & 31;
-    constexpr uint32_t kBarRows = 1, kBarDgrad = 2, kBarG1 = 3;  // named barriers
+    constexpr uint32_t kBarRows = 1, kBarDgrad = 2, kBarG1 = 3, kBarHelp = 4, kBarTile = 5;  // named barriers
     uint8_t* sW = smem;
     const uint32_t sW_a = smem_u32(sW);
     const uint32_t sH_a = sW_a + kImgBytes;              // h0..h5
@@ -210,6 +215,8 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
     uint64_t* wbar = &bars[0];     // weight image loads
     uint64_t* mma_bar = &bars[1];  // forward / dgrad commits (thread 0)
     uint64_t* wg_bar = &bars[2];   // wgrad commits (warp 4)
+    uint64_t* staged_bar = &bars[3];  // rows -> warp 5: a W3..W5 partial is staged in SMEM
+    float* sHelp = reinterpret_cast<float*>(smem + kImgBytes + 10 * kTileBytes + 128);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
     float* red = reinterpret_cast<float*>(bars + 5);    // 4 floats + 4 u32
 
@@ -217,6 +224,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         mbar_init(wbar, 1);
         mbar_init(mma_bar, 1);
         mbar_init(wg_bar, 1);
+        mbar_init(staged_bar, 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
     const uint32_t idesc_dgrad = make_idesc(128, 64, 0, 1);
     const uint32_t idesc_wgrad = make_idesc(64, 64, 1, 1);
 
-    uint32_t phase = 0, wg_phase = 0, w_phase = 0;
+    uint32_t phase = 0, wg_phase = 0, w_phase = 0, st_phase = 0;
     float loss_sum = 0.0f;
     uint32_t bad = 0;
     bool first = true;
@@ -337,8 +345,33 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         trc = 32u * step;
         NRC_GTRC(6);
 #pragma unroll 1
-        for (uint32_t tile = blockIdx.x; warp < 5 && tile < ntiles; tile += gridDim.x) {
+        for (uint32_t tile = blockIdx.x; warp < 6 && tile < ntiles; tile += gridDim.x) {
             const bool last = tile + gridDim.x >= ntiles;
+            if (warp == 5) {
+                // ---------------- partial-store warp: TMA-store G5, G4, G3 as the rows
+                // stage them, then (fused mode) announce that they are globally written
+                if (last) {
+#pragma unroll 1
+                    for (int i = 3; i >= 1; --i) {
+                        mbar_wait(staged_bar, st_phase);
+                        st_phase ^= 1;
+                        if (lane == 0) {
+                            bulk_s2g(part + layer_off(i + 2), hs(i + 2), uint32_t((i + 2 < 5 ? 64 : kOutPad) * 64 * 4));
+                            bulk_commit();
+                        }
+                        __syncwarp();
+                    }
+                    if (lane == 0) {
+                        bulk_wait_all();
+                        if (a.fused) {
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.gbarA) : "memory");
+                        }
+                    }
+                    __syncwarp();
+                }
+                continue;
+            }
             if (warp == 4) {
                 // ---------------- wgrad issue warp: G_{i+1} right after dgrad_i is queued
 #pragma unroll 1
@@ -466,7 +499,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
                 mma_wait();
                 mask_epilogue(i);
                 sync_rows();
-                if (last && i <= 3) store_partial(i + 2);
+                if (last && i <= 3 && tid == 0) mbar_arrive(staged_bar);  // warp 5 stores G_{i+2}
                 NRC_TRC(16 - i);
             }
             named_bar_arrive(kBarG1, kTrainThreads);  // warp 4 may queue wgrad_1, wgrad_0
@@ -485,6 +518,75 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
             }
             first = false;
         }
+        const unsigned long long G = gridDim.x;
+        const StepCoef sc = a.coef[step];
+        const OptParams op{a.lr, a.b1, a.b2, a.adam_eps, sc.inv_bc1, sc.inv_bc2, sc.ema_c1, sc.ema_c2};
+        // Deterministic reduction of partial chunks [cA, cB) over the G partials
+        // + Adam + EMA, by threads t < T of a thread set that syncs with sync().
+        // ng == 1: each thread owns whole chunks; else thread t sums chunk t % nch
+        // over partials p = z, z + ng, ... (z = t / nch) and the group sums are
+        // added in group order through scratch.  The order depends only on G.
+        auto reduce_apply = [&](int cA, int cB, int t, int T, float* scratch, auto&& sync) {
+            const int nch = cB - cA, per = 4 * nch;
+            const int ng = nch >= T ? 1 : T / nch;
+            const float4* P4 = reinterpret_cast<const float4*>(a.partials) + cA;
+            auto sum_chunk = [&](int c, int z) {
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+                for (int p = z; p < int(G); p += 16 * ng) {  // 16 loads in flight (predicated tail)
+                    float4 x[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        x[u] = (p + u * ng < int(G)) ? __ldcg(P4 + size_t(p + u * ng) * kParamChunks + c)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        acc.x += x[u].x;
+                        acc.y += x[u].y;
+                        acc.z += x[u].z;
+                        acc.w += x[u].w;
+                    }
+                }
+                return acc;
+            };
+            if (ng == 1) {
+                for (int c = t; c < nch; c += T) {
+                    const float4 g4 = sum_chunk(c, 0);
+                    const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        adam_ema_update(partial_to_param(4 * (cA + c) + e), g[e] * a.inv_n, op, a.w, a.m, a.v, a.ema,
+                                        a.wimg_out, a.eimg, a.bad_grads);
+                }
+                return;
+            }
+            // Adam state of the first two owned parameters, loaded under the partial loads
+            float st0[4] = {0.f, 0.f, 0.f, 0.f}, st1[4] = {0.f, 0.f, 0.f, 0.f};  // m, v, w, e
+            if (t < per) {
+                const int j = partial_to_param(4 * cA + t);
+                st0[0] = ld_global_f32(a.m + j), st0[1] = ld_global_f32(a.v + j);
+                st0[2] = ld_global_f32(a.w + j), st0[3] = ld_global_f32(a.ema + j);
+            }
+            if (t + T < per) {
+                const int j = partial_to_param(4 * cA + t + T);
+                st1[0] = ld_global_f32(a.m + j), st1[1] = ld_global_f32(a.v + j);
+                st1[2] = ld_global_f32(a.w + j), st1[3] = ld_global_f32(a.ema + j);
+            }
+            if (t < ng * nch) reinterpret_cast<float4*>(scratch)[t] = sum_chunk(t % nch, t / nch);
+            sync();
+            for (int q = t, u = 0; q < per; q += T, ++u) {
+                float g = 0.0f;
+                for (int z = 0; z < ng; ++z) g += scratch[z * per + q];
+                const int j = partial_to_param(4 * cA + q);
+                if (u < 2) {
+                    const float* stv = u == 0 ? st0 : st1;
+                    adam_ema_apply(j, g * a.inv_n, op, stv[0], stv[1], stv[2], stv[3], a.w, a.m, a.v, a.ema,
+                                   a.wimg_out, a.eimg, a.bad_grads);
+                } else {
+                    adam_ema_update(j, g * a.inv_n, op, a.w, a.m, a.v, a.ema, a.wimg_out, a.eimg, a.bad_grads);
+                }
+            }
+        };
         if (first && warp < 4) {  // no tile for this CTA: contribute zeros
             pdl_wait();
             for (int j = tid; j < kParamPadded; j += 128) part[j] = 0.0f;
@@ -504,7 +606,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
             reinterpret_cast<uint32_t*>(red + 4)[warp] = bad;
         }
         tc_fence_before();
-        __syncthreads();
+        if (warp < 5) named_bar_sync(kBarTile, kTrainThreads);  // rows + warp 4 (helpers are not involved)
         if (tid == 0) {
             a.loss_part[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
             const uint32_t* b = reinterpret_cast<const uint32_t*>(red + 4);
@@ -515,71 +617,44 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         bad = 0;
         if (!a.fused) break;
 
-        // ---------------- optimiser (fused mode): every partial is in global memory
-        const unsigned long long G = gridDim.x;
-        grid_sync(a.gbar, a.gbar_base + G * (2 * step + 1));
+        // ---------------- optimiser (fused mode).  Grid barrier 1: thread 0
+        // arrives once this CTA's partials and loss are written; the helper
+        // warps meanwhile reduce W3..W5 (phase A) and join before phase B.
+        if (warp >= 5) {
+            // ---------------- phase A (helper warps): W3..W5 as soon as every CTA
+            // has written them, overlapping the rows' last backward round
+            if (tid == 160) {
+                const unsigned long long target = a.gbarA_base + G * (step + 1);
+                unsigned long long v = 0;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.gbarA) : "memory");
+                } while (v < target);
+            }
+            named_bar_sync(kBarHelp, kHelpThreads);
+            const int n_a = kParamChunks - kChunkSplit;
+            reduce_apply(kChunkSplit + int(blockIdx.x * uint32_t(n_a) / uint32_t(G)),
+                         kChunkSplit + int((blockIdx.x + 1) * uint32_t(n_a) / uint32_t(G)), int(tid) - 160,
+                         kHelpThreads, sHelp, [&]() { named_bar_sync(kBarHelp, kHelpThreads); });
+        }
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.gbar) : "memory");
+            const unsigned long long target = a.gbar_base + G * (2 * step + 1);
+            unsigned long long v = 0;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.gbar) : "memory");
+            } while (v < target);
+        }
+        __syncthreads();
         NRC_TRC(17);
         NRC_GTRC(2);
         {
-            // This CTA's slice: 16-byte chunks [c0, c1) of the partial layout
-            // (balanced over the grid).  Thread t sums chunk c0 + t % nch over the
-            // partials p = z, z + ng, ... (z = t / nch) with L2 loads (the
-            // partials were written by other SMs); the ng group sums are then
-            // added in group order.  The order depends only on the grid size, so
-            // the result is deterministic.
-            const int c0 = int(blockIdx.x * uint32_t(kParamChunks) / uint32_t(G));
-            const int c1 = int((blockIdx.x + 1) * uint32_t(kParamChunks) / uint32_t(G));
-            const int nch = c1 - c0, per = 4 * nch;
-            const int ng = nch >= kTrainBlock ? 1 : kTrainBlock / nch;
-            const StepCoef sc = a.coef[step];
-            const OptParams op{a.lr, a.b1, a.b2, a.adam_eps, sc.inv_bc1, sc.inv_bc2, sc.ema_c1, sc.ema_c2};
-            // Adam state of the first two owned parameters, loaded before the partials
-            float st0[4] = {0.f, 0.f, 0.f, 0.f}, st1[4] = {0.f, 0.f, 0.f, 0.f};  // m, v, w, e
-            if (int(tid) < per) {
-                const int j = partial_to_param(4 * c0 + int(tid));
-                st0[0] = ld_global_f32(a.m + j), st0[1] = ld_global_f32(a.v + j);
-                st0[2] = ld_global_f32(a.w + j), st0[3] = ld_global_f32(a.ema + j);
-            }
-            if (int(tid) + kTrainBlock < per) {
-                const int j = partial_to_param(4 * c0 + int(tid) + kTrainBlock);
-                st1[0] = ld_global_f32(a.m + j), st1[1] = ld_global_f32(a.v + j);
-                st1[2] = ld_global_f32(a.w + j), st1[3] = ld_global_f32(a.ema + j);
-            }
-            const float4* P4 = reinterpret_cast<const float4*>(a.partials) + c0;
-            for (int t = int(tid); t < ng * nch; t += kTrainBlock) {  // ng > 1: one task per thread
-                const int c = t % nch, z = t / nch;
-                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-                for (int p = z; p < int(G); p += 16 * ng) {  // 16 loads in flight (predicated tail)
-                    float4 x[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u)
-                        x[u] = (p + u * ng < int(G)) ? __ldcg(P4 + size_t(p + u * ng) * kParamChunks + c)
-                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        acc.x += x[u].x;
-                        acc.y += x[u].y;
-                        acc.z += x[u].z;
-                        acc.w += x[u].w;
-                    }
-                }
-                reinterpret_cast<float4*>(sOpt)[z * nch + c] = acc;
-            }
-            __syncthreads();
+            // phase B: W0..W2, this CTA's balanced slice of chunks [0, kChunkSplit),
+            // all 384 threads, group sums staged in the (now free) stash
+            reduce_apply(int(blockIdx.x * uint32_t(kChunkSplit) / uint32_t(G)),
+                         int((blockIdx.x + 1) * uint32_t(kChunkSplit) / uint32_t(G)), int(tid), kTrainBlock, sOpt,
+                         [&]() { __syncthreads(); });
             NRC_TRC(18);
-            for (int q = int(tid), u = 0; q < per; q += kTrainBlock, ++u) {
-                float g = 0.0f;
-                for (int z = 0; z < ng; ++z) g += sOpt[z * per + q];
-                const int j = partial_to_param(4 * c0 + q);
-                if (u < 2) {
-                    const float* st = u == 0 ? st0 : st1;
-                    adam_ema_apply(j, g * a.inv_n, op, st[0], st[1], st[2], st[3], a.w, a.m, a.v, a.ema, a.wimg_out,
-                                   a.eimg, a.bad_grads);
-                } else {
-                    adam_ema_update(j, g * a.inv_n, op, a.w, a.m, a.v, a.ema, a.wimg_out, a.eimg, a.bad_grads);
-                }
-            }
             if (blockIdx.x == 0 && warp == 4 && a.losses != nullptr) {
                 float x[8];  // G <= 256 partials, all loads in flight
 #pragma unroll
