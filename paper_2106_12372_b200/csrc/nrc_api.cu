@@ -150,6 +150,22 @@ struct nrc_handle {
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
     int train_ctas = 0;           // cap on the train grid (0: one CTA per tile up to all SMs)
+    // nrc_frame_host pipelining: host->device and device->host copy streams and events
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    std::vector<cudaEvent_t> events;
+    ~nrc_handle() {
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+        if (copy_in) cudaStreamDestroy(copy_in);
+        if (copy_out) cudaStreamDestroy(copy_out);
+    }
+    cudaEvent_t event(size_t i) {  // lazily created, reused across frames
+        while (events.size() <= i) {
+            cudaEvent_t e = nullptr;
+            cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            events.push_back(e);
+        }
+        return events[i];
+    }
     float* d_w() { return reinterpret_cast<float*>(state + L.w); }
     float* d_m() { return reinterpret_cast<float*>(state + L.m); }
     float* d_v() { return reinterpret_cast<float*>(state + L.v); }
@@ -843,18 +859,52 @@ nrc_status nrc_frame_host(nrc_handle* h, const nrc_record* h_query, uint64_t n_q
     p += align_up(size_t(n_train) * 3 * sizeof(float), 256);
     float* dloss = reinterpret_cast<float*>(p);  // up to 64 losses
     if (s_ > 64) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_frame_host: s > 64");
+    // Pipelined: the query batch moves in chunks; chunk k's
+    // host->device copy (stream copy_in) overlaps the query of chunk k-1 (the
+    // caller's stream) and the device->host copy of chunk k-2's RGB (stream
+    // copy_out).  The training data (small) goes first; training runs after
+    // the last query chunk, so queries see the EMA weights of the previous
+    // frame as in the unpipelined order.  The caller's stream finally waits
+    // for copy_out, so synchronising it covers every copy.
+    if (!h->copy_in) NRC_CUDA(h, cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
+    if (!h->copy_out) NRC_CUDA(h, cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
+    constexpr uint64_t kChunk = 262144;  // records per chunk (16.8 MB in, 3.1 MB out)
+    const uint64_t nchunks = (n_query + kChunk - 1) / kChunk;
     uint32_t launches = 0;
-    if (n_query) NRC_CUDA(h, cudaMemcpyAsync(dq, h_query, n_query * sizeof(nrc_record), cudaMemcpyHostToDevice, st));
+    size_t ev = 0;
+    cudaEvent_t e_start = h->event(ev++);
+    NRC_CUDA(h, cudaEventRecord(e_start, st));  // earlier work on the caller's stream (scratch reuse)
+    NRC_CUDA(h, cudaStreamWaitEvent(h->copy_in, e_start, 0));
+    NRC_CUDA(h, cudaStreamWaitEvent(h->copy_out, e_start, 0));
+    cudaEvent_t e_train = h->event(ev++);
     if (n_train) {
-        NRC_CUDA(h, cudaMemcpyAsync(dt, h_train, size_t(n_train) * sizeof(nrc_record), cudaMemcpyHostToDevice, st));
-        NRC_CUDA(h, cudaMemcpyAsync(dtg, h_tgt, size_t(n_train) * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+        NRC_CUDA(h, cudaMemcpyAsync(dt, h_train, size_t(n_train) * sizeof(nrc_record), cudaMemcpyHostToDevice,
+                                    h->copy_in));
+        NRC_CUDA(h, cudaMemcpyAsync(dtg, h_tgt, size_t(n_train) * 3 * sizeof(float), cudaMemcpyHostToDevice,
+                                    h->copy_in));
     }
-    if ((s = nrc_query(h, dq, n_query, drgb, stream)) != NRC_OK) return s;
-    launches += h->launches;
+    NRC_CUDA(h, cudaEventRecord(e_train, h->copy_in));
+    for (uint64_t k = 0; k < nchunks; ++k) {
+        const uint64_t r0 = k * kChunk, nr = (n_query - r0) < kChunk ? (n_query - r0) : kChunk;
+        cudaEvent_t e_in = h->event(ev++), e_q = h->event(ev++);
+        NRC_CUDA(h, cudaMemcpyAsync(dq + r0, h_query + r0, nr * sizeof(nrc_record), cudaMemcpyHostToDevice,
+                                    h->copy_in));
+        NRC_CUDA(h, cudaEventRecord(e_in, h->copy_in));
+        NRC_CUDA(h, cudaStreamWaitEvent(st, e_in, 0));
+        if ((s = nrc_query(h, dq + r0, nr, drgb + 3 * r0, stream)) != NRC_OK) return s;
+        launches += h->launches;
+        NRC_CUDA(h, cudaEventRecord(e_q, st));
+        NRC_CUDA(h, cudaStreamWaitEvent(h->copy_out, e_q, 0));
+        NRC_CUDA(h, cudaMemcpyAsync(h_rgb + 3 * r0, drgb + 3 * r0, nr * 3 * sizeof(float), cudaMemcpyDeviceToHost,
+                                    h->copy_out));
+    }
+    NRC_CUDA(h, cudaStreamWaitEvent(st, e_train, 0));
     if ((s = nrc_train_frame(h, dt, dtg, n_train, s_, l, shuffle_seed, dloss, stream)) != NRC_OK) return s;
     launches += h->launches;
-    if (n_query) NRC_CUDA(h, cudaMemcpyAsync(h_rgb, drgb, n_query * 3 * sizeof(float), cudaMemcpyDeviceToHost, st));
     if (h_losses && s_) NRC_CUDA(h, cudaMemcpyAsync(h_losses, dloss, s_ * sizeof(float), cudaMemcpyDeviceToHost, st));
+    cudaEvent_t e_out = h->event(ev++);
+    NRC_CUDA(h, cudaEventRecord(e_out, h->copy_out));
+    NRC_CUDA(h, cudaStreamWaitEvent(st, e_out, 0));
     h->launches = launches;
     return NRC_OK;
 }

@@ -294,3 +294,28 @@ def test_init_matches_oracle_init(nrc, orc):
         c = nrc.RadianceCache(nrc.Config(seed=seed))
         np.testing.assert_array_equal(c.get_params("train"), orc.init_weights(seed))
         np.testing.assert_array_equal(c.get_params("ema"), orc.init_weights(seed))
+
+
+def test_frame_host_equals_device_calls(nrc):
+    """nrc_frame_host (pinned host buffers, chunked copies overlapped with the
+    query) gives the same bits as nrc_query + nrc_train_frame on device data,
+    over two consecutive frames (scratch and event reuse)."""
+    nq, s, l = 600_001, 4, 2048
+    q = nrc_inputs.records(nq, seed=61)
+    tr, tg = nrc_inputs.train_frame(4, n=s * l)
+    a, b = nrc.RadianceCache(), nrc.RadianceCache()
+    hq = torch.from_numpy(q).pin_memory()
+    ht, htg = torch.from_numpy(tr).pin_memory(), torch.from_numpy(tg).pin_memory()
+    hrgb = torch.empty((nq, 3), dtype=torch.float32).pin_memory()
+    hl = torch.empty(64, dtype=torch.float32).pin_memory()
+    scratch = torch.empty(a.frame_scratch_bytes(nq, s * l) + 256, dtype=torch.uint8, device="cuda")
+    scratch = scratch[(-scratch.data_ptr()) % 256:]
+    for frame in range(2):
+        a.frame_host(hq.numpy(), hrgb.numpy(), ht.numpy(), htg.numpy(), s, l, 9 + frame, hl.numpy(), scratch)
+        torch.cuda.synchronize()
+        rgb_b = b.query(dev(q)).cpu().numpy()
+        lb = b.train_frame(dev(tr), dev(tg), s, l, 9 + frame).cpu().numpy()
+        np.testing.assert_array_equal(hrgb.numpy(), rgb_b)
+        np.testing.assert_array_equal(hl.numpy()[:s], lb)
+    np.testing.assert_array_equal(a.get_params("train"), b.get_params("train"))
+    np.testing.assert_array_equal(a.get_params("ema"), b.get_params("ema"))
