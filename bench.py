@@ -131,9 +131,9 @@ def oracle_frame_estimate(q_sample: int, t_sample: int, reps: int = 1):
     return ms, sample, tq, tt
 
 
-def frame_config(world: int) -> dict:
+def frame_config(world: int, train_mode: str = "dp") -> dict:
     return {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
-            "parallelism": f"dp{world}" if world > 1 else "single",
+            "parallelism": (f"dp{world}" if train_mode == "dp" else f"replicated{world}") if world > 1 else "single",
             "l2": "flushed (256 MB write) between timed steps"}
 
 
@@ -175,7 +175,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong" if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (nrc_inputs seeded records)",
-        "config": frame_config(args.gpus),
+        "config": frame_config(args.gpus, args.train_mode),
         "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": omp_threads(), "kind": "oracle", "sample": sample},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -239,6 +239,11 @@ def run_nrc(args):
         if world == 1:
             cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
             launches += cache.last_launch_count
+        elif args.train_mode == "replicated":
+            # N3 (i): this rank's screen-region records, one all-gather, replicated training
+            lo, hi = nrc.shard(N_TRAIN, rank, world)
+            dpf.train_frame_replicated(d_r[lo:hi], d_t[lo:hi], TRAIN_S, TRAIN_L, 1000 + fi % 2)
+            launches += dpf.last_launch_count
         else:
             # this rank's rows of every shuffled batch, gathered in-kernel
             dpf.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
@@ -308,7 +313,7 @@ def run_nrc(args):
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 Adam/EMA)", "data": "synthetic (nrc_inputs)",
-        "config": frame_config(world),
+        "config": frame_config(world, args.train_mode),
         "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
         "query_ms": q_ms, "train_ms": ms - q_ms,
         "gpu_launches": launches,
@@ -340,6 +345,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["nrc", "reference"], default="nrc")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--train-mode", choices=["dp", "replicated"], default="dp",
+                    help="N > 1 training: data-parallel with one all-reduce per step (dp), or one all-gather "
+                         "of the frame's records per frame and replicated training (replicated, SURVEY N3)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -66,6 +66,24 @@ class DataParallelFrame:
         """This rank's rows of the frame's query (no communication)."""
         return self.cache.query(records_local, out, stream=stream)
 
+    def train_frame_replicated(self, records_local: torch.Tensor, targets_local: torch.Tensor, s: int, l: int,
+                               shuffle_seed: int, losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+        """SURVEY 8(f) N3 variant (i): each rank owns the training records of its
+        screen region; one all-gather per frame (rank order) assembles the
+        frame's records on every rank, then every rank runs the whole frame's
+        training (fused nrc_train_frame) on identical data -- bitwise-identical
+        replicas with no per-step collective (the kernels are deterministic).
+        Every rank must pass the same number of records."""
+        n_loc = int(records_local.shape[0])
+        rec = torch.empty((n_loc * self.world, records_local.shape[1]), dtype=records_local.dtype,
+                          device=records_local.device)
+        tgt = torch.empty((n_loc * self.world, 3), dtype=targets_local.dtype, device=targets_local.device)
+        dist.all_gather_into_tensor(rec, records_local.contiguous(), group=self.group)
+        dist.all_gather_into_tensor(tgt, targets_local.contiguous(), group=self.group)
+        out = self.cache.train_frame(rec, tgt, s, l, shuffle_seed, losses)
+        self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
+        return out
+
     def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
                     losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
         """All s steps of the frame's training on the full (replicated) record

@@ -60,6 +60,18 @@ class OracleShard:
         oracle.adam(oc.w, oc.m, oc.v, grad_sum.numpy().astype(np.float64) / n, oc.t)
         oracle.ema(oc.wbar, oc.w, oc.t)
 
+    def train_frame(self, records, targets, s, l, seed, losses=None):
+        recs, tg = records.numpy(), targets.numpy()
+        s, l = dp.frame_batches(recs.shape[0], s, l)
+        a, c, m = oracle.lcg_params(recs.shape[0], seed)
+        perm = oracle.lcg_permute(recs.shape[0], a, c, m).astype(np.int64)
+        for j in range(s):
+            idx = perm[j * l:(j + 1) * l]
+            lj = self.oc.train_step(recs[idx], tg[idx])
+            if losses is not None:
+                losses[j] = lj
+        return losses
+
     def query(self, records, out, stream=None):
         out.copy_(torch.from_numpy(self.oc.query(records.numpy())))
         return out
@@ -82,6 +94,21 @@ def _worker(rank, world, port, out_dir):
         frame.query(torch.from_numpy(q[q0:q1].copy()), rgb)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), w=shard_cache.oc.w, wbar=shard_cache.oc.wbar,
                  losses=losses.numpy(), rgb=rgb.numpy(), q0=q0, q1=q1)
+    finally:
+        dist.destroy_process_group()
+
+
+def _worker_replicated(rank, world, port, out_dir, n_total):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        recs, tgts = nrc_inputs.train_frame(0, n=n_total, noise=0.3)
+        lo, hi = dp.shard(n_total, rank, world)  # this rank's screen region's records
+        shard_cache = OracleShard(seed=5)
+        frame = dp.DataParallelFrame(shard_cache, dtype=torch.float64)
+        losses = torch.zeros(S, dtype=torch.float64)
+        frame.train_frame_replicated(torch.from_numpy(recs[lo:hi].copy()), torch.from_numpy(tgts[lo:hi].copy()),
+                                     S, L, SEED, losses)
+        np.savez(os.path.join(out_dir, f"rep{rank}.npz"), w=shard_cache.oc.w, losses=losses.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -118,3 +145,20 @@ def test_data_parallel_frame_equals_single_process(tmp_path):
     full = ref.query(q)
     got = np.concatenate([res[0]["rgb"], res[1]["rgb"]])
     np.testing.assert_allclose(got, full, rtol=1e-9, atol=1e-12)
+
+
+def test_replicated_frame_after_allgather(tmp_path):
+    """N3 variant (i): one all-gather of the frame's records per frame, then
+    replicated training: every rank ends bitwise identical and equal to the
+    single-process training on the gathered (rank-ordered) records."""
+    world = 2
+    N = 3 * 1000 + 6  # divisible by the world size
+    mp.spawn(_worker_replicated, args=(world, _free_port(), str(tmp_path), N), nprocs=world, join=True)
+    res = [np.load(tmp_path / f"rep{r}.npz") for r in range(world)]
+    np.testing.assert_array_equal(res[0]["w"], res[1]["w"])
+    recs, tgts = nrc_inputs.train_frame(0, n=N, noise=0.3)
+    ref = OracleShard(seed=5)
+    ref_losses = torch.zeros(S, dtype=torch.float64)
+    ref.train_frame(torch.from_numpy(recs), torch.from_numpy(tgts), S, L, SEED, ref_losses)
+    np.testing.assert_array_equal(res[0]["w"], ref.oc.w)
+    np.testing.assert_array_equal(res[0]["losses"], ref_losses.numpy())

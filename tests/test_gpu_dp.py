@@ -59,3 +59,21 @@ def test_dp_frame_world1_matches_fused_frame_and_oracle(group, orc):
         lo.append(ref.train_step(recs[idx], tg[idx]))
     np.testing.assert_allclose(ld, lo, rtol=1e-2)
     assert max(radiance_err(cache.query(q).cpu().numpy(), ref.query(q.cpu().numpy()))) <= TOL_RADIANCE
+
+
+def test_replicated_frame_world1_equals_train_frame(group):
+    """N3 variant (i) through NCCL (world size 1: the all-gather is a copy):
+    bitwise equal to nrc_train_frame on the same records."""
+    import paper_2106_12372_b200 as nrc
+    n, s, l, seed = 8192, 4, 2048, 23
+    recs, tg = nrc_inputs.train_frame(3, n=n, noise=0.3)
+    d_r = torch.from_numpy(recs).cuda()
+    d_t = torch.from_numpy(tg).cuda()
+    a, b = nrc.RadianceCache(), nrc.RadianceCache()
+    la = a.train_frame(d_r, d_t, s, l, seed).cpu().numpy()
+    frame = nrc.DataParallelFrame(b, device=torch.device("cuda", 0))
+    lb = torch.zeros(s, dtype=torch.float32, device="cuda")
+    frame.train_frame_replicated(d_r, d_t, s, l, seed, lb)
+    np.testing.assert_array_equal(lb.cpu().numpy(), la)
+    np.testing.assert_array_equal(b.get_params("train"), a.get_params("train"))
+    np.testing.assert_array_equal(b.get_params("ema"), a.get_params("ema"))
