@@ -339,6 +339,26 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         }
     };
 
+    // record + target of batch row `row` of step `step` (zeros past the batch)
+    auto gather_row = [&](uint32_t step_, uint32_t row, float (&rec)[16], float (&tg)[3]) {
+        if (row < a.n) {
+            const uint64_t k = uint64_t(step_) * a.n + row;
+            const uint64_t idx = a.gather ? lcg_perm(a.offset + k, a.lcg_n, a.lcg_a, a.lcg_c, a.lcg_m) : k;
+            load_record_global(a.rec + idx * kRecFloats, rec);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) tg[c] = __ldg(a.tgt + idx * 3 + c);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) rec[i] = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) tg[c] = 0.0f;
+        }
+    };
+    // fused mode: the rows gather and encode the next step's first tile while
+    // the grid waits at barrier 2 (the records do not depend on the weights)
+    bool have_next = false;
+    float rec_n[16], tg_n[3];
+
 #pragma unroll 1
     for (uint32_t step = 0; step < a.nsteps; ++step) {
         first = true;
@@ -389,18 +409,16 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
             const bool valid = row < a.n;
             float rec[16];
             float tg[3] = {0.f, 0.f, 0.f};
-            if (valid) {
-                const uint64_t k = uint64_t(step) * a.n + row;
-                const uint64_t idx = a.gather ? lcg_perm(a.offset + k, a.lcg_n, a.lcg_a, a.lcg_c, a.lcg_m) : k;
-                load_record_global(a.rec + idx * kRecFloats, rec);
+            if (have_next && tile == blockIdx.x) {
+                // gathered and encoded into h0 during the previous step's barrier wait
 #pragma unroll
-                for (int c = 0; c < 3; ++c) tg[c] = __ldg(a.tgt + idx * 3 + c);
+                for (int i = 0; i < 16; ++i) rec[i] = rec_n[i];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) tg[c] = tg_n[c];
+                have_next = false;
             } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) rec[i] = 0.0f;
-            }
-            NRC_TRC(2);
-            {
+                gather_row(step, row, rec, tg);
+                NRC_TRC(2);
                 uint32_t h[32];
                 encode_record(rec, a.ep, h);
                 store_row_swz(hs(0), r, h);
@@ -652,7 +670,8 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
             // phase B: W0..W2, this CTA's balanced slice of chunks [0, kChunkSplit),
             // all 384 threads, group sums staged in the (now free) stash
             reduce_apply(int(blockIdx.x * uint32_t(kChunkSplit) / uint32_t(G)),
-                         int((blockIdx.x + 1) * uint32_t(kChunkSplit) / uint32_t(G)), int(tid), kTrainBlock, sOpt,
+                         int((blockIdx.x + 1) * uint32_t(kChunkSplit) / uint32_t(G)), int(tid), kTrainBlock,
+                         sOpt + 4 * kTileBytes / 4,  // stash slot 4 (slot 0 takes the next h0)
                          [&]() { __syncthreads(); });
             NRC_TRC(18);
             if (blockIdx.x == 0 && warp == 4 && a.losses != nullptr) {
@@ -669,7 +688,28 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         }
         NRC_TRC(19);
         NRC_GTRC(3);
-        grid_sync(a.gbar, a.gbar_base + G * (2 * step + 2));
+        // grid barrier 2: arrive, gather + encode the next step's first tile
+        // while the other CTAs finish their slices, then wait
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.gbar) : "memory");
+        }
+        if (step + 1 < a.nsteps && warp < 4 && blockIdx.x < ntiles) {
+            gather_row(step + 1, blockIdx.x * kTile + r, rec_n, tg_n);
+            uint32_t h[32];
+            encode_record(rec_n, a.ep, h);
+            store_row_swz(hs(0), r, h);
+            fence_async_smem();
+            have_next = true;
+        }
+        if (tid == 0) {
+            const unsigned long long target = a.gbar_base + G * (2 * step + 2);
+            unsigned long long v = 0;
+            do {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.gbar) : "memory");
+            } while (v < target);
+        }
+        __syncthreads();
         NRC_TRC(20);
         NRC_GTRC(4);
         if (step + 1 < a.nsteps) load_weights();  // W_{t+1}
