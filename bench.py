@@ -345,10 +345,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["nrc", "reference"], default="nrc")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
+                    help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
+                         "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
     ap.add_argument("--train-mode", choices=["dp", "replicated"], default="dp",
                     help="N > 1 training: data-parallel with one all-reduce per step (dp), or one all-gather "
                          "of the frame's records per frame and replicated training (replicated, SURVEY N3)")
     args = ap.parse_args()
+    if args.workload == "4k":
+        global N_QUERY, METRIC, CONFIG_NAME
+        N_QUERY = 3840 * 2160
+        METRIC = "NRC frame ms (4K: 8.29M queries + 4\u00d716384 train); queries/s, records/s"
+        CONFIG_NAME = "4K frame: 8,294,400 queries + 4x16384 train, width 64, 5 hidden layers"
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
