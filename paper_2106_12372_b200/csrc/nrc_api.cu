@@ -50,7 +50,8 @@ struct QueryLauncherTS {
 // Entry 0 (activations in TMEM, 5 groups x 1 tile) is the default; the
 // shared-memory-activation variants are kept for comparison.
 const QueryEntry kQueryCfgs[] = {NRC_QCFG_TS(5, 1), NRC_QCFG(4, 2), NRC_QCFG(3, 2), NRC_QCFG(2, 4),
-                                 NRC_QCFG(6, 1),    NRC_QCFG_TS(2, 2), NRC_QCFG_TS(1, 5)};
+                                 NRC_QCFG(6, 1),    NRC_QCFG_TS(2, 2), NRC_QCFG_TS(1, 5), NRC_QCFG_TS(4, 1),
+                                 NRC_QCFG_TS(3, 1)};
 #undef NRC_QCFG
 #undef NRC_QCFG_TS
 constexpr int kNumQueryCfgs = int(sizeof(kQueryCfgs) / sizeof(kQueryCfgs[0]));

@@ -121,7 +121,7 @@ def test_query_parity_4k_sampled_and_all_configs(nrc, orc):
     w = cache.get_params("train")
     small = d_recs[:50000]
     base = cache.query(small).cpu().numpy()
-    for cfg in range(7):
+    for cfg in range(9):
         os.environ["NRC_QUERY_CFG"] = str(cfg)
         try:
             c2 = nrc.RadianceCache()
