@@ -79,36 +79,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-// Non-blocking probe: true once the phase with the given parity has completed.
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-// Four probes issued back to back (their ~150-cycle latencies overlap);
-// bit i of the result is set when barrier i's phase with parity p_i completed.
-__device__ __forceinline__ uint32_t mbar_test4(uint32_t a0, uint32_t p0, uint32_t a1, uint32_t p1, uint32_t a2,
-                                               uint32_t p2, uint32_t a3, uint32_t p3) {
-    uint32_t m;
-    asm volatile(
-        "{\n\t.reg .pred q0, q1, q2, q3;\n\t.reg .b32 t0, t1, t2, t3;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %2;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 q1, [%3], %4;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 q2, [%5], %6;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 q3, [%7], %8;\n\t"
-        "selp.b32 t0, 1, 0, q0;\n\tselp.b32 t1, 2, 0, q1;\n\tselp.b32 t2, 4, 0, q2;\n\tselp.b32 t3, 8, 0, q3;\n\t"
-        "or.b32 t0, t0, t1;\n\tor.b32 t2, t2, t3;\n\tor.b32 %0, t0, t2;\n}"
-        : "=r"(m)
-        : "r"(a0), "r"(p0), "r"(a1), "r"(p1), "r"(a2), "r"(p2), "r"(a3), "r"(p3)
-        : "memory");
-    return m;
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -232,22 +202,6 @@ __device__ __forceinline__ void umma_chain4_ta_commit(uint32_t d_tmem, uint32_t 
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n\t"
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(smem_u32(bar))
-        : "memory");
-}
-// Same with A a K-major SWIZZLE_128B smem tile.
-__device__ __forceinline__ void umma_chain4_ss_commit(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                                      uint32_t idesc, uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .pred f, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
-        "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
-        "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t"
-        "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t"
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(smem_u32(bar))
         : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread

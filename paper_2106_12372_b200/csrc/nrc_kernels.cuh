@@ -91,15 +91,6 @@ __global__ void __launch_bounds__(kRedThreads) nrc_adam_kernel(AdamArgs a) {
     adam_ema_update(j, g * a.inv_n, op, a.w, a.m, a.v, a.ema, a.wimg, a.eimg, a.bad_grads);
 }
 
-// Rebuild an fp16 operand image from an fp32 padded array.
-__global__ void nrc_image_kernel(const float* __restrict__ w, uint8_t* __restrict__ img) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= kParamPadded) return;
-    int layer, row, col;
-    padded_coords(j, layer, row, col);
-    *reinterpret_cast<__half*>(img + image_offset(layer, row, col)) = __float2half_rn(w[j]);
-}
-
 // fp32 padded array -> fp16 operand image at hidden width W (NetDims<W>).
 template <int W>
 __global__ void nrc_image_w_kernel(const float* __restrict__ w, uint8_t* __restrict__ img) {

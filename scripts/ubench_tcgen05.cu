@@ -8,11 +8,6 @@
 
 using namespace nrc;
 
-__device__ __forceinline__ bool elect_one() {
-    uint32_t p = 0;
-    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n}" : "=r"(p));
-    return p != 0;
-}
 __global__ void __launch_bounds__(128, 1) ubench(int mode, int iters, long long* out) {
     long long issue_sum = 0;
     __shared__ __align__(1024) uint8_t sA[kTileBytes];
