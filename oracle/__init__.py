@@ -82,6 +82,12 @@ def lib():
         L.orc_query_batch_w.restype = None
         L.orc_query_batch_w.argtypes = [ctypes.c_int, vp, vp, i64, vp, vp, ctypes.c_uint, vp]
         L.orc_init_weights_w.restype = None; L.orc_init_weights_w.argtypes = [ctypes.c_int, u64, vp]
+        L.orc_gauss.restype = d; L.orc_gauss.argtypes = [d]
+        L.orc_freq_sin.restype = None; L.orc_freq_sin.argtypes = [d, vp]
+        L.orc_one_blob_gauss.restype = None; L.orc_one_blob_gauss.argtypes = [d, ctypes.c_int, vp]
+        L.orc_encode_batch_exact.restype = None; L.orc_encode_batch_exact.argtypes = [vp, i64, vp, vp, vp]
+        L.orc_query_batch_exact.restype = None
+        L.orc_query_batch_exact.argtypes = [vp, vp, i64, vp, vp, ctypes.c_uint, vp]
         L.orc_query_accumulate.restype = None
         L.orc_query_accumulate.argtypes = [vp, vp, i64, vp, vp, ctypes.c_uint, vp, vp, vp]
         L.orc_assemble_targets.restype = None
@@ -183,6 +189,41 @@ def init_weights_w(hw: int, seed: int) -> np.ndarray:
     W = np.zeros(param_count_w(hw), np.float32)
     lib().orc_init_weights_w(int(hw), int(seed) & (2**64 - 1), W.ctypes.data)
     return W
+
+
+# ---------------------------------------------------------------- exact encodings (N4)
+def gauss(x: float) -> float:
+    return lib().orc_gauss(float(x))
+
+
+def freq_sin(v: float) -> np.ndarray:
+    out = np.zeros(12, np.float64)
+    lib().orc_freq_sin(float(v), out.ctypes.data)
+    return out
+
+
+def one_blob_gauss(s: float, k: int = 4) -> np.ndarray:
+    out = np.zeros(k, np.float64)
+    lib().orc_one_blob_gauss(float(s), int(k), out.ctypes.data)
+    return out
+
+
+def encode_exact(recs, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1)) -> np.ndarray:
+    recs = _c(recs, np.float32).reshape(-1, 16)
+    lo, hi = _c(aabb_lo, np.float32), _c(aabb_hi, np.float32)
+    out = np.zeros((recs.shape[0], 64), np.float64)
+    lib().orc_encode_batch_exact(recs.ctypes.data, recs.shape[0], lo.ctypes.data, hi.ctypes.data, out.ctypes.data)
+    return out
+
+
+def query_exact(W, recs, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), flags=FACTORIZE | CLAMP_QUERY) -> np.ndarray:
+    W = _c(W, np.float64)
+    recs = _c(recs, np.float32).reshape(-1, 16)
+    lo, hi = _c(aabb_lo, np.float32), _c(aabb_hi, np.float32)
+    q = np.zeros((recs.shape[0], 3), np.float64)
+    lib().orc_query_batch_exact(W.ctypes.data, recs.ctypes.data, recs.shape[0], lo.ctypes.data, hi.ctypes.data,
+                                int(flags), q.ctypes.data)
+    return q
 
 
 # ---------------------------------------------------------------- pixel reconstruction (N2)

@@ -23,6 +23,8 @@
  *       forms, SPEC worked examples, periodicity, integral of quartic = 1)
  *   orc_encode ............................................. pinned (golden
  *       vector tests/golden/encode_c0.txt, structural invariants)
+ *   orc_freq_sin / orc_gauss / orc_encode_exact (N4) ....... pinned (sin at
+ *       dyadic points, Gaussian closed forms, layout shared with orc_encode)
  *   orc_query_accumulate ................................... pinned (unit
  *       throughput + identity pixels = query, permutation, accumulation)
  *   orc_assemble_targets ................................... pinned (one-vertex
@@ -172,6 +174,60 @@ int orc_encode(const float* rec, const float* aabb_lo, const float* aabb_hi, dou
     return degenerate;
 }
 
+/* ---- exact encodings: the primitives the cheap ones replace
+ * (fig:cheap_primitives).  Reading R21: the frequency
+ * entry d is sin(pi 2^d v) (NeRF's form, the paper's "12 sine functions, each
+ * with frequency 2^d").  Reading R22: the one-blob kernel is the
+ * Gaussian of the one-blob encoding [Mueller et al. 2019] with sigma = 1/k,
+ * i.e. sigma = 1 in bin units: g(x) = exp(-x^2/2) / sqrt(2 pi), evaluated at
+ * the bin centres, no truncation. */
+double orc_gauss(double x) { return exp(-0.5 * x * x) / sqrt(2.0 * M_PI); }
+
+void orc_freq_sin(double v, double* out12)
+{
+    for (int d = 0; d < 12; ++d) out12[d] = sin(M_PI * ldexp(v, d));
+}
+
+void orc_one_blob_gauss(double s, int k, double* out)
+{
+    if (s < 0.0) s = 0.0;
+    if (s > 1.0) s = 1.0;
+    for (int i = 0; i < k; ++i) out[i] = orc_gauss((s - (i + 0.5) / k) * k);
+}
+
+/* orc_encode with the exact primitives (same layout, readings R3-R7). */
+int orc_encode_exact(const float* rec, const float* aabb_lo, const float* aabb_hi, double* e)
+{
+    int degenerate = 0;
+    for (int a = 0; a < 3; ++a) {
+        float v = orc_normalize_pos(rec[a], aabb_lo[a], aabb_hi[a]);
+        orc_freq_sin((double)v, e + 12 * a);
+    }
+    double u[3], sp[2];
+    u[0] = rec[3]; u[1] = rec[4]; u[2] = rec[5];
+    degenerate += orc_sph(u, sp);
+    orc_one_blob_gauss(sp[0], 4, e + 36);
+    orc_one_blob_gauss(sp[1], 4, e + 40);
+    u[0] = rec[6]; u[1] = rec[7]; u[2] = rec[8];
+    degenerate += orc_sph(u, sp);
+    orc_one_blob_gauss(sp[0], 4, e + 44);
+    orc_one_blob_gauss(sp[1], 4, e + 48);
+    double r = rec[9];
+    if (r < 0.0) r = 0.0;
+    orc_one_blob_gauss(1.0 - exp(-r), 4, e + 52);
+    for (int c = 0; c < 3; ++c) e[56 + c] = rec[10 + c];
+    for (int c = 0; c < 3; ++c) e[59 + c] = rec[13 + c];
+    e[62] = 1.0;
+    e[63] = 1.0;
+    return degenerate;
+}
+
+void orc_encode_batch_exact(const float* recs, int64_t n, const float* lo, const float* hi, double* E)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) orc_encode_exact(recs + 16 * i, lo, hi, E + 64 * i);
+}
+
 void orc_encode_batch(const float* recs, int64_t n, const float* lo, const float* hi, double* E)
 {
 #pragma omp parallel for schedule(static)
@@ -275,6 +331,25 @@ void orc_query_batch_w(int hw, const double* W, const float* recs, int64_t n, co
         const float* rec = recs + 16 * i;
         orc_encode(rec, lo, hi, e);
         orc_forward_w(hw, W, e, y);
+        for (int c = 0; c < 3; ++c) {
+            double v = y[c];
+            if (flags & ORC_FACTORIZE) v *= (double)rec[10 + c] + (double)rec[13 + c];
+            if ((flags & ORC_CLAMP_QUERY) && v < 0.0) v = 0.0;
+            q[3 * i + c] = v;
+        }
+    }
+}
+
+/* orc_query_batch with the exact encoding (N4). */
+void orc_query_batch_exact(const double* W, const float* recs, int64_t n, const float* lo, const float* hi,
+                           unsigned flags, double* q)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double e[64], H[6 * 64], y[3];
+        const float* rec = recs + 16 * i;
+        orc_encode_exact(rec, lo, hi, e);
+        orc_forward(W, e, H, y);
         for (int c = 0; c < 3; ++c) {
             double v = y[c];
             if (flags & ORC_FACTORIZE) v *= (double)rec[10 + c] + (double)rec[13 + c];
