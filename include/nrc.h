@@ -84,7 +84,10 @@ enum {
     NRC_FACTORIZE = 1u,         /* multiply the output by alpha+beta       */
     NRC_CLAMP_QUERY = 2u,       /* clamp query radiance at 0 (R2)                        */
     NRC_EMA_PRINTED_FORM = 4u,  /* Eq.(2) exactly as printed instead of R12's form      */
-    NRC_QUERY_RAW_WEIGHTS = 8u  /* queries read W_t instead of W-bar_t                  */
+    NRC_QUERY_RAW_WEIGHTS = 8u, /* queries read W_t instead of W-bar_t                  */
+    NRC_EXACT_ENCODING = 16u    /* sin / Gaussian encoding primitives instead of the
+                                 * cheap tri / quartic ones (
+                                 * readings R21, R22)                       */
 };
 
 typedef struct nrc_config {

@@ -66,6 +66,17 @@ struct QueryLauncherW {
         nrc_query_ts_kernel<G, S, W><<<grid, 128 * G, query_ts_smem_bytes<G, S, W>(), st>>>(qa);
     }
 };
+template <int G, int S, int W>
+struct QueryLauncherExact {
+    static cudaError_t set_smem() {
+        return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    query_ts_smem_bytes<G, S, W>());
+    }
+    static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
+        nrc_query_ts_kernel<G, S, W, true><<<grid, 128 * G, query_ts_smem_bytes<G, S, W>(), st>>>(qa);
+    }
+};
+const QueryEntry kQueryExact = {&QueryLauncherExact<5, 1, 64>::set_smem, &QueryLauncherExact<5, 1, 64>::launch, 5};
 const QueryEntry kQueryW32 = {&QueryLauncherW<5, 1, 32>::set_smem, &QueryLauncherW<5, 1, 32>::launch, 5};
 const QueryEntry kQueryW128 = {&QueryLauncherW<2, 1, 128>::set_smem, &QueryLauncherW<2, 1, 128>::launch, 2};
 constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
@@ -275,6 +286,10 @@ static nrc_status validate_config(const nrc_config* c, std::string* why) {
         *why = "ABI version mismatch";
         return NRC_ERR_UNSUPPORTED;
     }
+    if ((c->flags & NRC_EXACT_ENCODING) && c->hidden_width != 64) {
+        *why = "NRC_EXACT_ENCODING is built for hidden_width 64";
+        return NRC_ERR_UNSUPPORTED;
+    }
     if (!width_supported(c->hidden_width) || c->n_hidden_layers != 5) {
         *why = "hidden_width must be 32, 64 (P:L694) or 128 (width ablation) with 5 hidden layers";
         return NRC_ERR_UNSUPPORTED;
@@ -374,6 +389,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
         h->ep.lo[i] = cfg->aabb_min[i];
         h->ep.inv[i] = inv;
     }
+    h->ep.exact = (cfg->flags & NRC_EXACT_ENCODING) ? 1u : 0u;
     auto bail = [&](nrc_status st) {
         std::fprintf(stderr, "nrc_init: %s\n", h->err.c_str());
         delete h;
@@ -399,9 +415,14 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
         if ((s = cuda_check(h, kQueryCfgs[i].set_smem(), "cudaFuncSetAttribute(query)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW32.set_smem(), "cudaFuncSetAttribute(query w32)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW128.set_smem(), "cudaFuncSetAttribute(query w128)")) != NRC_OK) return bail(s);
-    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((s = cuda_check(h, kQueryExact.set_smem(), "cudaFuncSetAttribute(query exact)")) != NRC_OK) return bail(s);
+    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 kTrainSmemBytes),
                         "cudaFuncSetAttribute(train)")) != NRC_OK)
+        return bail(s);
+    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kTrainSmemBytes),
+                        "cudaFuncSetAttribute(train exact)")) != NRC_OK)
         return bail(s);
 
     // Glorot-uniform init from the counter-based splitmix64 stream (R16):
@@ -464,7 +485,10 @@ static nrc_status query_impl(nrc_handle* h, const nrc_record* d_rec, uint64_t n,
     qa.image = d_image;
     // the fused accumulate epilogue exists in the TMEM kernels only (entry 0 and the width kernels)
     const int cfg = d_image ? 0 : h->query_cfg;
-    const QueryEntry& qe = h->wi.W == 32 ? kQueryW32 : h->wi.W == 128 ? kQueryW128 : kQueryCfgs[cfg];
+    const QueryEntry& qe = h->ep.exact        ? kQueryExact
+                           : h->wi.W == 32   ? kQueryW32
+                           : h->wi.W == 128  ? kQueryW128
+                                             : kQueryCfgs[cfg];
     const uint64_t ntiles = (n + kTile - 1) / kTile;
     const uint64_t G = uint64_t(qe.groups);
     const uint64_t ctas = (ntiles + G - 1) / G;  // one tile stream per group
@@ -560,7 +584,8 @@ static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const flo
     if (nsteps == 0) {
         ta.fused = 0;
         ta.nsteps = 1;
-        NRC_CUDA(h, launch_pdl(nrc_train_kernel, dim3(grid), dim3(kTrainBlock), kTrainSmemBytes, st, ta));
+        NRC_CUDA(h, launch_pdl(h->ep.exact ? nrc_train_kernel<true> : nrc_train_kernel<false>, dim3(grid),
+                               dim3(kTrainBlock), kTrainSmemBytes, st, ta));
         NRC_LAUNCHED(h, "nrc_train_kernel");
         return NRC_OK;
     }
@@ -586,9 +611,12 @@ static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const flo
     ta.gbarA = h->d_counters() + 3;
     ta.gbarA_base = h->gbarA;
     if (h->coop)
-        NRC_CUDA(h, launch_coop(nrc_train_kernel, dim3(grid), dim3(kTrainBlock), kTrainSmemBytes, st, ta));
+        NRC_CUDA(h, launch_coop(h->ep.exact ? nrc_train_kernel<true> : nrc_train_kernel<false>, dim3(grid),
+                                dim3(kTrainBlock), kTrainSmemBytes, st, ta));
+    else if (h->ep.exact)
+        nrc_train_kernel<true><<<grid, kTrainBlock, kTrainSmemBytes, st>>>(ta);
     else
-        nrc_train_kernel<<<grid, kTrainBlock, kTrainSmemBytes, st>>>(ta);
+        nrc_train_kernel<false><<<grid, kTrainBlock, kTrainSmemBytes, st>>>(ta);
     NRC_LAUNCHED(h, "nrc_train_kernel");
     h->gbar += 2ull * nsteps * uint64_t(grid);
     h->gbarA += uint64_t(nsteps) * uint64_t(grid);
@@ -751,8 +779,12 @@ nrc_status nrc_encode(nrc_handle* h, const nrc_record* d_rec, uint64_t n, uint16
     if (!d_rec || !d_out || !aligned(d_rec, 16) || !aligned(d_out, 16))
         return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_encode: NULL or misaligned pointer");
     const unsigned blocks = unsigned((n + 127) / 128);
-    nrc_encode_kernel<<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const float*>(d_rec), n,
-                                                                              h->ep, reinterpret_cast<uint4*>(d_out));
+    if (h->ep.exact)
+        nrc_encode_kernel<true><<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+            reinterpret_cast<const float*>(d_rec), n, h->ep, reinterpret_cast<uint4*>(d_out));
+    else
+        nrc_encode_kernel<false><<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+            reinterpret_cast<const float*>(d_rec), n, h->ep, reinterpret_cast<uint4*>(d_out));
     NRC_LAUNCHED(h, "nrc_encode_kernel");
     return NRC_OK;
 }

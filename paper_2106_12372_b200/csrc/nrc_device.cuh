@@ -321,6 +321,7 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t saddr) {
 struct EncodeParams {
     float lo[3];
     float inv[3];
+    uint32_t exact;  // 1: sin / Gaussian primitives (NRC_EXACT_ENCODING, N4) instead of tri / quartic
 };
 
 // quartic(x) = 15/16 (1 - x^2)^2 on |x| <= 1, else 0: clamping
@@ -406,7 +407,50 @@ __device__ __forceinline__ void sph_f(float x, float y, float z, float& th, floa
 // Encodes one record into 64 fp16 features packed as 32 f16x2 words, in the
 // order of reading R5 / Table 1: freq(x) 36 | ob(sph(w)) 8 | ob(sph(n)) 8 |
 // ob(1-e^-r) 4 | alpha 3 | beta 3 | 1, 1.
+// Exact primitives (readings R21/R22): sin(pi 2^d v) with
+// sinpif's exact range reduction (2^d v is exact in fp32), and the Gaussian
+// one-blob exp(-x^2/2)/sqrt(2 pi) at the bin centres.
+__device__ __forceinline__ void encode_record_exact(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
+    float e[64];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float v = __fmul_rn(__fsub_rn(rec[a], ep.lo[a]), ep.inv[a]);
+#pragma unroll
+        for (int d = 0; d < 12; ++d) e[12 * a + d] = sinpif(ldexpf(v, d));
+    }
+    auto ob = [](float s, float* o) {
+        s = fminf(fmaxf(s, 0.0f), 1.0f);
+        const float x = 4.0f * s;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float t = x - (float(i) + 0.5f);
+            o[i] = 0.3989422804014327f * __expf(-0.5f * t * t);
+        }
+    };
+    float th, ph;
+    sph_f(rec[3], rec[4], rec[5], th, ph);
+    ob(th, e + 36);
+    ob(ph, e + 40);
+    sph_f(rec[6], rec[7], rec[8], th, ph);
+    ob(th, e + 44);
+    ob(ph, e + 48);
+    ob(1.0f - ex2_approx(-1.44269504088896341f * fmaxf(rec[9], 0.0f)), e + 52);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) e[56 + c] = rec[10 + c];
+    e[62] = 1.0f;
+    e[63] = 1.0f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) h[j] = pack_h2(e[2 * j], e[2 * j + 1]);
+}
+
+// EXACT selects the primitives at compile time (kernels are instantiated per
+// variant, so the cheap path carries no trace of the exact one).
+template <bool EXACT = false>
 __device__ __forceinline__ void encode_record(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
+    if (EXACT) {
+        encode_record_exact(rec, ep, h);
+        return;
+    }
     float e[64];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {

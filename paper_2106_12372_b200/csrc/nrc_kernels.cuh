@@ -149,13 +149,14 @@ __global__ void nrc_targets_kernel(const uint32_t* __restrict__ first, const uin
 }
 
 // Encoding only (nrc_encode): one thread per record, logical feature order.
+template <bool EXACT>
 __global__ void nrc_encode_kernel(const float* __restrict__ rec, uint64_t n, EncodeParams ep, uint4* __restrict__ out) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float r[16];
     load_record_global(rec + i * kRecFloats, r);
     uint32_t h[32];
-    encode_record(r, ep, h);
+    encode_record<EXACT>(r, ep, h);
 #pragma unroll
     for (int c = 0; c < 8; ++c) out[i * 8 + c] = make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
 }

@@ -57,8 +57,9 @@ __device__ __forceinline__ void umma_ta_chain_commit(uint32_t d, uint32_t a, uin
     umma_commit(bar);
 }
 
-// G independent 4-warp groups, S tiles in flight per group, hidden width W.
-template <int G, int S, int W = 64>
+// G independent 4-warp groups, S tiles in flight per group, hidden width W,
+// EXACT: sin / Gaussian encoding primitives (N4).
+template <int G, int S, int W = 64, bool EXACT = false>
 __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args) {
     static_assert(G * S <= ts_max_slots<W>(), "TMEM holds 512 columns");
     using D = NetDims<W>;
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
         for (int c = 0; c < 3; ++c) fac[s][c] = (args.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
         {
             uint32_t h[32];
-            encode_record(rec, args.ep, h);
+            encode_record<EXACT>(rec, args.ep, h);
             tmem_st32(a_col(s) + lane_off, h);  // includes tcgen05.wait::st
         }
         fence_async_smem();  // record reads before the next TMA overwrite

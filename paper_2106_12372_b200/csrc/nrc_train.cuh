@@ -198,6 +198,7 @@ __device__ __forceinline__ void warp_issue(uint32_t d, uint64_t a, uint64_t b, u
 // partials -> [barrier] -> each CTA reduces its slice of parameter rows over
 // all partials in fixed CTA order and applies Adam + EMA -> [barrier] ->
 // reload the new weight image.
+template <bool EXACT>
 __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) {
     uint32_t trc = 0;  // trace slot base: 32 per step
     NRC_TRC(0);
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
                 gather_row(step, row, rec, tg);
                 NRC_TRC(2);
                 uint32_t h[32];
-                encode_record(rec, a.ep, h);
+                encode_record<EXACT>(rec, a.ep, h);
                 store_row_swz(hs(0), r, h);
             }
             if (!weights_ready) {
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         if (step + 1 < a.nsteps && warp < 4 && blockIdx.x < ntiles) {
             gather_row(step + 1, blockIdx.x * kTile + r, rec_n, tg_n);
             uint32_t h[32];
-            encode_record(rec_n, a.ep, h);
+            encode_record<EXACT>(rec_n, a.ep, h);
             store_row_swz(hs(0), r, h);
             fence_async_smem();
             have_next = true;

@@ -28,6 +28,7 @@ FACTORIZE = 1
 CLAMP_QUERY = 2
 EMA_PRINTED_FORM = 4
 QUERY_RAW_WEIGHTS = 8
+EXACT_ENCODING = 16
 
 PARAMS_TRAIN, PARAMS_EMA, ADAM_M, ADAM_V = 0, 1, 2, 3
 _PARAM_SETS = {"train": PARAMS_TRAIN, "ema": PARAMS_EMA, "adam_m": ADAM_M, "adam_v": ADAM_V}

@@ -1,0 +1,59 @@
+"""Exact encodings (NRC_EXACT_ENCODING; readings R21, R22) on
+the GPU against the fp64 oracle: encoding within one fp16 ulp and query
+parity."""
+import numpy as np
+import pytest
+import torch
+
+import nrc_inputs
+from parity import TOL_RADIANCE, fp16_ulp, radiance_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nrc():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    import paper_2106_12372_b200 as p
+    return p
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("n", [1, 1000])
+def test_exact_encode_within_one_fp16_ulp(nrc, orc, n):
+    recs = nrc_inputs.records(n, seed=500 + n)
+    c = nrc.RadianceCache(nrc.Config(flags=nrc.FACTORIZE | nrc.CLAMP_QUERY | nrc.EXACT_ENCODING))
+    got = c.encode(dev(recs)).cpu().numpy().astype(np.float64)
+    ref16 = orc.encode_exact(recs).astype(np.float16).astype(np.float64)
+    err = np.abs(got - ref16)
+    assert np.all(err <= fp16_ulp(ref16) * 1.0001), float(err.max())
+
+
+def test_exact_query_parity(nrc, orc):
+    recs = nrc_inputs.records(20000, seed=501)
+    c = nrc.RadianceCache(nrc.Config(flags=nrc.FACTORIZE | nrc.CLAMP_QUERY | nrc.EXACT_ENCODING))
+    w = orc.init_weights(7) * 1.4
+    c.set_params(w, "ema")
+    q = c.query(dev(recs)).cpu().numpy()
+    ref = orc.query_exact(c.get_params("ema").astype(np.float64), recs)
+    assert max(radiance_err(q, ref)) <= TOL_RADIANCE
+    # and it is a different function from the cheap encoding's
+    cheap = orc.query(c.get_params("ema").astype(np.float64), recs)
+    assert max(radiance_err(cheap, ref)) > 10 * TOL_RADIANCE
+
+
+def test_exact_training_runs(nrc):
+    c = nrc.RadianceCache(nrc.Config(flags=nrc.FACTORIZE | nrc.CLAMP_QUERY | nrc.EXACT_ENCODING))
+    tr, tg = nrc_inputs.train_frame(0, n=16384)
+    losses = [c.train_frame(dev(tr), dev(tg), 4, 4096, j).cpu().numpy() for j in range(20)]
+    assert np.all(np.isfinite(losses))
+    assert np.mean(losses[-1]) < np.mean(losses[0])
+
+
+def test_exact_requires_width_64(nrc):
+    with pytest.raises(nrc.NRCError):
+        nrc.RadianceCache(nrc.Config(hidden_width=32, flags=nrc.EXACT_ENCODING))
