@@ -443,14 +443,18 @@ __device__ __forceinline__ void encode_record_exact(const float* rec, const Enco
     for (int j = 0; j < 32; ++j) h[j] = pack_h2(e[2 * j], e[2 * j + 1]);
 }
 
+__device__ __forceinline__ void encode_record_cheap(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]);
 // EXACT selects the primitives at compile time (kernels are instantiated per
 // variant, so the cheap path carries no trace of the exact one).
 template <bool EXACT = false>
 __device__ __forceinline__ void encode_record(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
-    if (EXACT) {
+    if constexpr (EXACT) {
         encode_record_exact(rec, ep, h);
-        return;
+    } else {
+        encode_record_cheap(rec, ep, h);
     }
+}
+__device__ __forceinline__ void encode_record_cheap(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
     float e[64];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
