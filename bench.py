@@ -280,7 +280,7 @@ def run_nrc(args):
 
     # ---- end to end through the C ABI with host buffers (N = 1 path; for N > 1 rank-local)
     e2e = None
-    if world == 1:
+    if world == 1 and not args.no_e2e:
         hq = torch.from_numpy(recs_q_all).pin_memory()
         ht = torch.from_numpy(frames[0][2]).pin_memory()
         htg = torch.from_numpy(frames[0][3]).pin_memory()
@@ -345,6 +345,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["nrc", "reference"], default="nrc")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer (e2e) leg (profiling runs)")
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")

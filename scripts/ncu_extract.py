@@ -35,7 +35,7 @@ def main(tag, d):
             per[r[ki]].append(float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1))
     ours = {k: v for k, v in per.items() if k.startswith("nrc::") or "nrc_" in k}
     frame = sum(sum(v) for v in ours.values())
-    lines = [f"# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline`",
+    lines = [f"# ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e`",
              f"# (--metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised)",
              f"{'kernel':60s} {'launches':>8s} {'mean_us':>10s} {'share_of_nrc_time':>18s}"]
     for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
