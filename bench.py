@@ -10,10 +10,12 @@ forward / relative-L2 / backward step followed by Adam + EMA.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nrc|reference]
 
 N > 1 (launched with torch.distributed.run, one rank per GPU, NCCL): the same
-1080p frame is split across ranks -- query rows sharded with no
-communication, training data-parallel (each rank takes l/N rows of every
-batch, one NCCL all-reduce of the 20,672-float gradient per step, identical
-Adam on every rank) -- strong scaling, max-over-ranks device time.
+frame is split across ranks -- query rows sharded with no communication;
+training either replicated after one all-gather of the frame's records
+(--train-mode replicated, the default) or data-parallel (--train-mode dp:
+each rank takes l/N rows of every batch, one NCCL all-reduce of the gradient
+per step, identical Adam on every rank) -- strong scaling, max-over-ranks
+device time.
 
 --impl reference: the fp64 CPU oracle (oracle/, as it stands) on the host
 cores, timed on a bounded sample of the same frame and scaled to the frame.
@@ -349,9 +351,11 @@ def main():
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
-    ap.add_argument("--train-mode", choices=["dp", "replicated"], default="dp",
-                    help="N > 1 training: data-parallel with one all-reduce per step (dp), or one all-gather "
-                         "of the frame's records per frame and replicated training (replicated, SURVEY N3)")
+    ap.add_argument("--train-mode", choices=["dp", "replicated"], default="replicated",
+                    help="N > 1 training: one all-gather of the frame's records per frame and replicated "
+                         "training (replicated, SURVEY N3 (i); default: the training step is latency-bound, so "
+                         "fewer rows per GPU do not shorten it while per-step collectives add up), or "
+                         "data-parallel with one all-reduce per step (dp, north_star's description)")
     args = ap.parse_args()
     if args.workload == "4k":
         global N_QUERY, METRIC, CONFIG_NAME
