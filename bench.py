@@ -199,9 +199,17 @@ def run_nrc(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    # NRC_BENCH_SHARED_GPU=1 (code-path test only, timings meaningless): every rank
+    # uses cuda:0 and gloo, so the N > 1 path can run on a one-GPU box
+    shared = os.environ.get("NRC_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     def barrier():

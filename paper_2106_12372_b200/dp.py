@@ -78,8 +78,12 @@ class DataParallelFrame:
         rec = torch.empty((n_loc * self.world, records_local.shape[1]), dtype=records_local.dtype,
                           device=records_local.device)
         tgt = torch.empty((n_loc * self.world, 3), dtype=targets_local.dtype, device=targets_local.device)
-        dist.all_gather_into_tensor(rec, records_local.contiguous(), group=self.group)
-        dist.all_gather_into_tensor(tgt, targets_local.contiguous(), group=self.group)
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(rec, records_local.contiguous(), group=self.group)
+            dist.all_gather_into_tensor(tgt, targets_local.contiguous(), group=self.group)
+        else:  # gloo (CPU tests): list form
+            dist.all_gather(list(rec.chunk(self.world)), records_local.contiguous(), group=self.group)
+            dist.all_gather(list(tgt.chunk(self.world)), targets_local.contiguous(), group=self.group)
         out = self.cache.train_frame(rec, tgt, s, l, shuffle_seed, losses)
         self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
         return out
