@@ -319,3 +319,42 @@ def test_frame_host_equals_device_calls(nrc):
         np.testing.assert_array_equal(hl.numpy()[:s], lb)
     np.testing.assert_array_equal(a.get_params("train"), b.get_params("train"))
     np.testing.assert_array_equal(a.get_params("ema"), b.get_params("ema"))
+
+
+def test_multi_tile_ctas_gradient_and_fused_step(nrc, orc):
+    """Batches larger than one tile per SM (40,000 rows = 313 tiles on <= 148
+    CTAs): the partials-only path (train_backward) and the fused step
+    (train_step: several tiles per CTA, phase A / phase B optimiser) against
+    the oracle's gradient and post-Adam weights."""
+    n = 40_000
+    recs, tg = nrc_inputs.train_frame(8, n=n, noise=0.3)
+    cache = nrc.RadianceCache()
+    oc = orc.OracleCache(W32=cache.get_params("train"))
+    g_gpu, ls = cache.train_backward(dev(recs), dev(tg))
+    g_gpu = g_gpu.cpu().numpy()
+    g_ref, l_ref, _ = orc.grad_batch(oc.w, recs, tg)
+    assert max(per_matrix_err(g_gpu, g_ref)) <= TOL_GRAD
+    assert float(ls.item()) == pytest.approx(l_ref, rel=1e-2)
+    loss = cache.train_step(dev(recs), dev(tg)).item()
+    l1, G1 = oc.train_step(recs, tg, return_grad=True)
+    assert loss == pytest.approx(l1, rel=1e-2)
+    errs, flip_frac, worst = post_adam_err(cache.get_params("train"), oc.w, g_gpu / n, G1)
+    assert max(errs) <= TOL_PARAM, errs
+    assert flip_frac <= 0.01 and worst <= 3e-2, (flip_frac, worst)
+
+
+def test_train_frame_more_than_eight_steps(nrc):
+    """s = 11 steps run as two fused launches (8 + 3): bitwise equal to 11
+    single steps on the gathered batches, losses included."""
+    n, s, l, seed = 11 * 1024, 11, 1024, 5
+    recs, tg = nrc_inputs.train_frame(6, n=n)
+    a, b = nrc.RadianceCache(), nrc.RadianceCache()
+    la = a.train_frame(dev(recs), dev(tg), s, l, seed).cpu().numpy()
+    pa, pc, pm = nrc.lcg_params(n, seed)
+    import oracle
+    perm = oracle.lcg_permute(n, pa, pc, pm).astype(np.int64)
+    lb = [b.train_step(dev(recs[perm[j * l:(j + 1) * l]]), dev(tg[perm[j * l:(j + 1) * l]])).item()
+          for j in range(s)]
+    np.testing.assert_array_equal(la, np.array(lb, np.float32))
+    np.testing.assert_array_equal(a.get_params("train"), b.get_params("train"))
+    assert a.stats()["step"] == s
