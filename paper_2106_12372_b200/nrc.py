@@ -85,6 +85,33 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+# Volume queries: "undefined parameters (surface roughness,
+# normal, albedo, and specular coefficients) are simply set to default
+# constants".  Reading R23: n = (0, 0, 1), r = 1, alpha = (1, 1, 1),
+# beta = (0, 0, 0), so the reflectance factorisation (alpha + beta = 1) leaves
+# the network output unchanged.
+VOLUME_DEFAULTS = {"normal": (0.0, 0.0, 1.0), "roughness": 1.0, "albedo": (1.0, 1.0, 1.0),
+                   "specular": (0.0, 0.0, 0.0)}
+
+
+def volume_records(positions: torch.Tensor, directions: torch.Tensor) -> torch.Tensor:
+    """Cache records [n, 16] for volume (in-medium) vertices: position and
+    direction from the caller, the surface fields at VOLUME_DEFAULTS (R23).
+    Data assembly only (torch ops on the caller's device)."""
+    n = positions.shape[0]
+    if positions.shape != (n, 3) or directions.shape != (n, 3):
+        raise NRCError("positions and directions must be [n, 3]")
+    rec = torch.empty((n, REC_FLOATS), dtype=torch.float32, device=positions.device)
+    rec[:, 0:3] = positions
+    rec[:, 3:6] = directions
+    d = VOLUME_DEFAULTS
+    rec[:, 6:9] = torch.tensor(d["normal"], dtype=torch.float32, device=positions.device)
+    rec[:, 9] = d["roughness"]
+    rec[:, 10:13] = torch.tensor(d["albedo"], dtype=torch.float32, device=positions.device)
+    rec[:, 13:16] = torch.tensor(d["specular"], dtype=torch.float32, device=positions.device)
+    return rec
+
+
 def lcg_params(n: int, seed: int):
     """LCG constants (a, c, m) of reading R15, from the C ABI."""
     L = _lib.load()

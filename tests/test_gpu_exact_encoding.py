@@ -57,3 +57,21 @@ def test_exact_training_runs(nrc):
 def test_exact_requires_width_64(nrc):
     with pytest.raises(nrc.NRCError):
         nrc.RadianceCache(nrc.Config(hidden_width=32, flags=nrc.EXACT_ENCODING))
+
+
+def test_volume_records_query(nrc, orc):
+    """Volume queries (reading R23): records assembled with the
+    default surface constants query like any record (oracle parity), and the
+    factorisation is the identity for them."""
+    rng = np.random.default_rng(4)
+    pos = torch.from_numpy(rng.random((3000, 3)).astype(np.float32)).cuda()
+    d = rng.normal(size=(3000, 3)).astype(np.float32)
+    dirs = torch.from_numpy(d / np.linalg.norm(d, axis=1, keepdims=True)).cuda()
+    recs = nrc.volume_records(pos, dirs)
+    r_np = recs.cpu().numpy()
+    assert np.all(r_np[:, 10:13] + r_np[:, 13:16] == 1.0)
+    c = nrc.RadianceCache()
+    c.set_params(orc.init_weights(2) * 1.3, "ema")
+    q = c.query(recs).cpu().numpy()
+    ref = orc.query(c.get_params("ema").astype(np.float64), r_np)
+    assert max(radiance_err(q, ref)) <= TOL_RADIANCE
