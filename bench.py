@@ -135,7 +135,7 @@ def oracle_frame_estimate(q_sample: int, t_sample: int, reps: int = 1):
 
 def frame_config(world: int, train_mode: str = "dp") -> dict:
     return {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
-            "parallelism": (f"dp{world}" if train_mode == "dp" else f"replicated{world}") if world > 1 else "single",
+            "parallelism": f"{train_mode}{world}" if world > 1 else "single",
             "l2": "flushed (256 MB write) between timed steps"}
 
 
@@ -249,6 +249,12 @@ def run_nrc(args):
         if world == 1:
             cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
             launches += cache.last_launch_count
+        elif args.train_mode == "peer":
+            # N3, all-gather fused into the kernel: rows gathered from the owners' memory
+            # (CUDA IPC / NVLink); the frame buffers are static and synchronised at setup
+            lo, hi = nrc.shard(N_TRAIN, rank, world)
+            dpf.train_frame_peer(d_r[lo:hi], d_t[lo:hi], TRAIN_S, TRAIN_L, 1000 + fi % 2, parts_ready=True)
+            launches += dpf.last_launch_count
         elif args.train_mode == "replicated":
             # N3 (i): this rank's screen-region records, one all-gather, replicated training
             lo, hi = nrc.shard(N_TRAIN, rank, world)
@@ -260,6 +266,8 @@ def run_nrc(args):
             launches += dpf.last_launch_count
         return launches
 
+    torch.cuda.synchronize()
+    barrier()  # every rank's frame buffers are on the device (peer mode reads them remotely)
     for i in range(args.warmup):
         frame(i)
     torch.cuda.synchronize()
@@ -359,11 +367,12 @@ def main():
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
-    ap.add_argument("--train-mode", choices=["dp", "replicated"], default="replicated",
+    ap.add_argument("--train-mode", choices=["dp", "replicated", "peer"], default="replicated",
                     help="N > 1 training: one all-gather of the frame's records per frame and replicated "
                          "training (replicated, SURVEY N3 (i); default: the training step is latency-bound, so "
                          "fewer rows per GPU do not shorten it while per-step collectives add up), or "
-                         "data-parallel with one all-reduce per step (dp, north_star's description)")
+                         "data-parallel with one all-reduce per step (dp, north_star's description), or the "
+                         "all-gather fused into the training kernel over peer memory (peer)")
     args = ap.parse_args()
     if args.workload == "4k":
         global N_QUERY, METRIC, CONFIG_NAME

@@ -191,6 +191,30 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
                                     uint32_t l, uint64_t shuffle_seed, uint32_t j, uint32_t row_begin,
                                     uint32_t row_end, float* d_grad, float* d_loss_sum, void* stream);
 
+/* Replicated frame training over peer memory: the frame's
+ * n_parts x n_per_part training records live on n_parts ranks (part p holds
+ * records [p n_per_part, (p+1) n_per_part), e.g. each rank's screen region;
+ * rec_parts / tgt_parts are HOST arrays of the parts' DEVICE pointers, peers'
+ * opened with nrc_ipc_import).  The training kernel gathers every shuffled
+ * batch row straight from its owner's buffer -- NVLink loads on a multi-GPU
+ * box -- so the frame's record all-gather happens inside the kernel and no
+ * collective runs.  Bitwise identical to nrc_train_frame on the concatenated
+ * records, so every rank ends with the same state.  n_parts <= 8.  The caller
+ * guarantees the parts are complete before the call and are not overwritten
+ * until it has finished (e.g. a barrier per frame). */
+nrc_status nrc_train_frame_parts(nrc_handle* h, const nrc_record* const* rec_parts, const float* const* tgt_parts,
+                                 uint32_t n_parts, uint32_t n_per_part, uint32_t s, uint32_t l,
+                                 uint64_t shuffle_seed, float* d_losses, void* stream);
+
+/* CUDA IPC for nrc_train_frame_parts.  nrc_ipc_export: the 64-byte handle of
+ * the device allocation that contains d_ptr and d_ptr's offset in it;
+ * nrc_ipc_import (another process): maps it, *d_ptr = mapped base + offset;
+ * nrc_ipc_close: unmaps (pass the imported pointer and its offset).  A
+ * process cannot import its own handle. */
+nrc_status nrc_ipc_export(const void* d_ptr, uint8_t* handle, uint64_t* offset);
+nrc_status nrc_ipc_import(const uint8_t* handle, uint64_t offset, void** d_ptr);
+nrc_status nrc_ipc_close(void* d_ptr, uint64_t offset);
+
 /* Host helper: the LCG constants of reading R15 (m = 2^ceil(log2 n), a = 1
  * mod 4, c odd, from the splitmix64 stream of seed). */
 nrc_status nrc_lcg_params(uint64_t n, uint64_t seed, uint64_t* a, uint64_t* c, uint64_t* m);

@@ -1,6 +1,7 @@
 // nrc_api.cu -- host side of libnrc: the C ABI declared in include/nrc.h.
 // Argument validation, state-arena layout, launch configuration.  All
 // arithmetic of the method runs in the kernels of nrc_kernels.cuh.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -526,6 +527,9 @@ nrc_status nrc_query_accumulate(nrc_handle* h, const nrc_record* d_rec, uint64_t
 struct Gather {
     bool on;
     uint64_t a, c, m, n, offset;
+    uint32_t n_parts = 0, part_n = 0;  // peer mode
+    const float* rec_parts[kMaxParts] = {};
+    const float* tgt_parts[kMaxParts] = {};
 };
 
 // Adam bias corrections and EMA coefficients of optimisation step t >= 1
@@ -567,6 +571,12 @@ static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const flo
     ta.lcg_m = gth.m;
     ta.lcg_n = gth.n;
     ta.offset = gth.offset;
+    ta.n_parts = gth.n_parts;
+    ta.part_n = gth.part_n;
+    for (int p = 0; p < kMaxParts; ++p) {
+        ta.rec_parts[p] = gth.rec_parts[p];
+        ta.tgt_parts[p] = gth.tgt_parts[p];
+    }
     ta.wimg = h->d_wimg();
     ta.ep = h->ep;
     ta.flags = h->cfg.flags & NRC_FACTORIZE;
@@ -743,21 +753,16 @@ nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_gl
     return NRC_OK;
 }
 
-nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s_,
-                           uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream) {
-    nrc_status s = check_handle(h);
-    if (s != NRC_OK) return s;
-    if ((s = check_train_width(h)) != NRC_OK) return s;
-    h->launches = 0;
-    if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
-    if (!d_rec || !d_tgt || !aligned(d_rec, 16) || !aligned(d_tgt, 4))
-        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: NULL or misaligned pointer");
+static nrc_status train_frame_impl(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
+                                   uint32_t s_, uint32_t l, uint64_t shuffle_seed, float* d_losses, Gather g,
+                                   cudaStream_t st) {
+    nrc_status s = NRC_OK;
     if (uint64_t(s_) * l > n_total) l = n_total / s_;  // batches shrink proportionally
     if (l == 0) return NRC_OK;
     if (l > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: l > max_batch");
-    Gather g{true, 0, 0, 0, n_total, 0};
+    g.on = true;
+    g.n = n_total;
     nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint32_t total = 0;
     for (uint32_t j = 0; j < s_; j += kMaxFusedSteps) {  // one launch per <= 8 steps
         const uint32_t k = (s_ - j) < uint32_t(kMaxFusedSteps) ? (s_ - j) : uint32_t(kMaxFusedSteps);
@@ -769,6 +774,84 @@ nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* 
     }
     h->launches = total;
     return NRC_OK;
+}
+
+nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s_,
+                           uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
+    h->launches = 0;
+    if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
+    if (!d_rec || !d_tgt || !aligned(d_rec, 16) || !aligned(d_tgt, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: NULL or misaligned pointer");
+    Gather g{true, 0, 0, 0, n_total, 0};
+    return train_frame_impl(h, d_rec, d_tgt, n_total, s_, l, shuffle_seed, d_losses, g,
+                            static_cast<cudaStream_t>(stream));
+}
+
+nrc_status nrc_train_frame_parts(nrc_handle* h, const nrc_record* const* rec_parts, const float* const* tgt_parts,
+                                 uint32_t n_parts, uint32_t n_per_part, uint32_t s_, uint32_t l,
+                                 uint64_t shuffle_seed, float* d_losses, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
+    h->launches = 0;
+    if (!rec_parts || !tgt_parts || n_parts == 0 || n_parts > uint32_t(kMaxParts))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_parts: 1..8 parts required");
+    const uint64_t n_total = uint64_t(n_parts) * n_per_part;
+    if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
+    if (n_total > 0xFFFFFFFFull) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_parts: too many records");
+    Gather g{true, 0, 0, 0, n_total, 0};
+    g.n_parts = n_parts;
+    g.part_n = n_per_part;
+    for (uint32_t p = 0; p < n_parts; ++p) {
+        if (!rec_parts[p] || !tgt_parts[p] || !aligned(rec_parts[p], 16) || !aligned(tgt_parts[p], 4))
+            return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_parts: NULL or misaligned part pointer");
+        g.rec_parts[p] = reinterpret_cast<const float*>(rec_parts[p]);
+        g.tgt_parts[p] = tgt_parts[p];
+    }
+    // d_rec / d_tgt are unused in peer mode (every row resolves to a part)
+    return train_frame_impl(h, rec_parts[0], tgt_parts[0], uint32_t(n_total), s_, l, shuffle_seed, d_losses, g,
+                            static_cast<cudaStream_t>(stream));
+}
+
+nrc_status nrc_ipc_export(const void* d_ptr, uint8_t* handle, uint64_t* offset) {
+    if (!d_ptr || !handle || !offset) return NRC_ERR_INVALID_ARGUMENT;
+    // driver entry point through the runtime (no link-time libcuda dependency)
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return NRC_ERR_CUDA;
+        get_range = reinterpret_cast<GetRange>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS) return NRC_ERR_CUDA;
+    cudaIpcMemHandle_t hd;
+    if (cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base)) != cudaSuccess) return NRC_ERR_CUDA;
+    std::memcpy(handle, &hd, sizeof(hd));
+    *offset = uint64_t(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+    return NRC_OK;
+}
+
+nrc_status nrc_ipc_import(const uint8_t* handle, uint64_t offset, void** d_ptr) {
+    if (!handle || !d_ptr) return NRC_ERR_INVALID_ARGUMENT;
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    void* base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return NRC_ERR_CUDA;
+    *d_ptr = static_cast<uint8_t*>(base) + offset;
+    return NRC_OK;
+}
+
+nrc_status nrc_ipc_close(void* d_ptr, uint64_t offset) {
+    if (!d_ptr) return NRC_ERR_INVALID_ARGUMENT;
+    return cudaIpcCloseMemHandle(static_cast<uint8_t*>(d_ptr) - offset) == cudaSuccess ? NRC_OK : NRC_ERR_CUDA;
 }
 
 nrc_status nrc_encode(nrc_handle* h, const nrc_record* d_rec, uint64_t n, uint16_t* d_out, void* stream) {

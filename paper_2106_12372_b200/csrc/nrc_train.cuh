@@ -13,6 +13,7 @@
 namespace nrc {
 
 constexpr int kMaxFusedSteps = 8;
+constexpr int kMaxParts = 8;  // ranks of one box
 struct StepCoef {
     float inv_bc1, inv_bc2;  // Adam bias corrections 1/(1-b^t)
     float ema_c1, ema_c2;    // W-bar = c1 W + c2 W-bar (Eq. 2 / R12)
@@ -20,6 +21,11 @@ struct StepCoef {
 
 struct TrainArgs {
     const float* rec;      // records (indexed through the gather below)
+    // peer mode (nrc_train_frame_parts): record i lives in part i / part_n at
+    // row i % part_n of rec_parts / tgt_parts (peer pointers), if n_parts > 0
+    const float* rec_parts[kMaxParts];
+    const float* tgt_parts[kMaxParts];
+    uint32_t n_parts, part_n;
     const float* tgt;      // targets, 3 fp32 per record
     uint32_t n;            // rows per step
     uint32_t gather;       // 1: row k of step j reads record lcg_perm(offset + j n + k); 0: record j n + k
@@ -345,9 +351,17 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         if (row < a.n) {
             const uint64_t k = uint64_t(step_) * a.n + row;
             const uint64_t idx = a.gather ? lcg_perm(a.offset + k, a.lcg_n, a.lcg_a, a.lcg_c, a.lcg_m) : k;
-            load_record_global(a.rec + idx * kRecFloats, rec);
+            const float* rsrc = a.rec + idx * kRecFloats;
+            const float* tsrc = a.tgt + idx * 3;
+            if (a.n_parts > 0) {  // the owner's buffer (a peer GPU's memory over NVLink)
+                const uint32_t p = uint32_t(idx / a.part_n);
+                const uint64_t o = idx - uint64_t(p) * a.part_n;
+                rsrc = a.rec_parts[p] + o * kRecFloats;
+                tsrc = a.tgt_parts[p] + o * 3;
+            }
+            load_record_global(rsrc, rec);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) tg[c] = __ldg(a.tgt + idx * 3 + c);
+            for (int c = 0; c < 3; ++c) tg[c] = __ldg(tsrc + c);
         } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) rec[i] = 0.0f;

@@ -88,6 +88,48 @@ class DataParallelFrame:
         self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
         return out
 
+    def train_frame_peer(self, records_local: torch.Tensor, targets_local: torch.Tensor, s: int, l: int,
+                         shuffle_seed: int, losses: Optional[torch.Tensor] = None,
+                         parts_ready: bool = False) -> Optional[torch.Tensor]:
+        """SURVEY 8(f) N3, the all-gather fused into the training kernel: every
+        rank exports its record / target buffers once (CUDA IPC handles over
+        the process group), maps the peers', and nrc_train_frame_parts reads
+        each shuffled batch row from its owner's memory (NVLink loads).  No
+        collective per frame; bitwise the same result as train_frame_replicated.
+        The caller keeps the local buffers alive and unchanged across the call
+        on every rank (here: a barrier before the kernel, skipped with
+        parts_ready=True when the caller already knows every part is final,
+        e.g. buffers written once and synchronised at setup)."""
+        from .nrc import ipc_export, ipc_import
+        key = (records_local.data_ptr(), targets_local.data_ptr(), int(records_local.shape[0]))
+        self._peer_cache = getattr(self, "_peer_cache", {})
+        if key not in self._peer_cache:
+            mine = (ipc_export(records_local), ipc_export(targets_local), int(records_local.shape[0]))
+            everyone = [None] * self.world
+            dist.all_gather_object(everyone, mine, group=self.group)
+            if any(e[2] != mine[2] for e in everyone):
+                raise ValueError("every rank must hold the same number of records")
+            self._peer_maps = getattr(self, "_peer_maps", {})
+            rec_ptrs, tgt_ptrs = [], []
+            for r, (rh, th, _) in enumerate(everyone):
+                if r == self.rank:
+                    rec_ptrs.append(records_local.data_ptr())
+                    tgt_ptrs.append(targets_local.data_ptr())
+                    continue
+                for hnd, lst in ((rh, rec_ptrs), (th, tgt_ptrs)):
+                    if hnd not in self._peer_maps:
+                        self._peer_maps[hnd] = ipc_import(*hnd)
+                    lst.append(self._peer_maps[hnd])
+            self._peer_cache[key] = (rec_ptrs, tgt_ptrs)
+        if not parts_ready:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)  # every part is complete
+        rec_ptrs, tgt_ptrs = self._peer_cache[key]
+        out = self.cache.train_frame_parts(rec_ptrs, tgt_ptrs, int(records_local.shape[0]), s, l, shuffle_seed,
+                                           losses)
+        self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
+        return out
+
     def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
                     losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
         """All s steps of the frame's training on the full (replicated) record

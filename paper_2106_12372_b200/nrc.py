@@ -112,6 +112,33 @@ def volume_records(positions: torch.Tensor, directions: torch.Tensor) -> torch.T
     return rec
 
 
+def ipc_export(t: torch.Tensor):
+    """(64-byte handle, offset) of a device tensor's allocation (CUDA IPC)."""
+    L = _lib.load()
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_uint64()
+    st = L.nrc_ipc_export(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off))
+    if st != 0:
+        raise NRCError(f"nrc_ipc_export: {L.nrc_status_string(st).decode()}")
+    return bytes(h), off.value
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device pointer (int) to another process's allocation + offset."""
+    L = _lib.load()
+    hb = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    p = ctypes.c_void_p()
+    st = L.nrc_ipc_import(hb, int(offset), ctypes.byref(p))
+    if st != 0:
+        raise NRCError(f"nrc_ipc_import: {L.nrc_status_string(st).decode()}")
+    return int(p.value)
+
+
+def ipc_close(ptr: int, offset: int):
+    L = _lib.load()
+    L.nrc_ipc_close(ctypes.c_void_p(ptr), int(offset))
+
+
 def lcg_params(n: int, seed: int):
     """LCG constants (a, c, m) of reading R15, from the C ABI."""
     L = _lib.load()
@@ -220,6 +247,22 @@ class RadianceCache:
         self._check(self.L.nrc_train_frame(self.h, _ptr(records), _ptr(targets), n, int(s), int(l),
                                            int(shuffle_seed) & (2 ** 64 - 1), _ptr(losses), _stream(stream)),
                     "nrc_train_frame")
+        return losses
+
+    def train_frame_parts(self, rec_ptrs, tgt_ptrs, n_per_part: int, s: int = 4, l: int = 16384,
+                          shuffle_seed: int = 0, losses: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """nrc_train_frame over records split into parts that may live in peer
+        GPUs' memory (device pointers as ints; see DataParallelFrame)."""
+        n = len(rec_ptrs)
+        if n != len(tgt_ptrs) or not 1 <= n <= 8:
+            raise NRCError("1..8 record / target parts required")
+        rp = (ctypes.c_void_p * n)(*rec_ptrs)
+        tp = (ctypes.c_void_p * n)(*tgt_ptrs)
+        if losses is None:
+            losses = torch.zeros(max(int(s), 1), dtype=torch.float32, device=self.device)
+        self._check(self.L.nrc_train_frame_parts(self.h, rp, tp, n, int(n_per_part), int(s), int(l),
+                                                 int(shuffle_seed) & (2 ** 64 - 1), _ptr(losses), _stream(stream)),
+                    "nrc_train_frame_parts")
         return losses
 
     def train_frame_backward(self, records: torch.Tensor, targets: torch.Tensor, l: int, shuffle_seed: int, j: int,
