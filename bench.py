@@ -163,8 +163,15 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    q_sample, t_sample = 32768, 4096
-    oracle_frame_estimate(1024, 256)  # warm-up (build, page-in)
+    # bounded samples: size each step so that warm-up + timed steps take about
+    # REF_BUDGET_S of host time in total, from the oracle's measured per-record cost
+    budget = float(os.environ.get("NRC_REF_BUDGET_S", "120"))
+    _, _, tq, tt = oracle_frame_estimate(4096, 512)  # warm-up (build, page-in) + calibration
+    per_step = budget / max(1, args.steps + args.warmup)
+    per_q, per_t = tq / 4096, tt / 512
+    scale = per_step / max(per_q * 32768 + per_t * 4096, 1e-9)
+    q_sample = int(min(32768, max(1024, 32768 * scale)))
+    t_sample = int(min(4096, max(256, 4096 * scale)))
     times = []
     for _ in range(args.warmup):
         oracle_frame_estimate(q_sample, t_sample)
