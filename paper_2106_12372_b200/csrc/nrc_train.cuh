@@ -187,6 +187,19 @@ __device__ __forceinline__ void warp_issue(uint32_t d, uint64_t a, uint64_t b, u
     __syncwarp();
 }
 
+// Spin until *ctr >= target: relaxed polls with a short back-off (acquire
+// polls hammer L2 and the SM's memory pipe while other warps compute), then
+// one acquire fence.
+__device__ __forceinline__ void wait_counter(unsigned long long* ctr, unsigned long long target) {
+    unsigned long long v = 0;
+    while (true) {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        if (v >= target) break;
+        __nanosleep(64);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 #define NRC_TRC(i)                                                                          \
     do {                                                                                    \
         if (a.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.dbg[trc + (i)] = clock64(); \
@@ -656,13 +669,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         if (warp >= 5) {
             // ---------------- phase A (helper warps): W3..W5 as soon as every CTA
             // has written them, overlapping the rows' last backward round
-            if (tid == 160) {
-                const unsigned long long target = a.gbarA_base + G * (step + 1);
-                unsigned long long v = 0;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.gbarA) : "memory");
-                } while (v < target);
-            }
+            if (tid == 160) wait_counter(a.gbarA, a.gbarA_base + G * (step + 1));
             named_bar_sync(kBarHelp, kHelpThreads);
             const int n_a = kParamChunks - kChunkSplit;
             reduce_apply(kChunkSplit + int(blockIdx.x * uint32_t(n_a) / uint32_t(G)),
@@ -672,11 +679,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
         if (tid == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");
             asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.gbar) : "memory");
-            const unsigned long long target = a.gbar_base + G * (2 * step + 1);
-            unsigned long long v = 0;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.gbar) : "memory");
-            } while (v < target);
+            wait_counter(a.gbar, a.gbar_base + G * (2 * step + 1));
         }
         __syncthreads();
         NRC_TRC(17);
@@ -718,11 +721,7 @@ __global__ void __launch_bounds__(kTrainBlock, 1) nrc_train_kernel(TrainArgs a) 
             have_next = true;
         }
         if (tid == 0) {
-            const unsigned long long target = a.gbar_base + G * (2 * step + 2);
-            unsigned long long v = 0;
-            do {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.gbar) : "memory");
-            } while (v < target);
+            wait_counter(a.gbar, a.gbar_base + G * (2 * step + 2));
         }
         __syncthreads();
         NRC_TRC(20);
