@@ -78,7 +78,11 @@ struct QueryLauncherExact {
     }
 };
 const QueryEntry kQueryExact = {&QueryLauncherExact<5, 1, 64>::set_smem, &QueryLauncherExact<5, 1, 64>::launch, 5};
-const QueryEntry kQueryW32 = {&QueryLauncherW<5, 1, 32>::set_smem, &QueryLauncherW<5, 1, 32>::launch, 5};
+#ifndef NRC_W32_G
+#define NRC_W32_G 7  // 7 groups: 82 us vs 90 us with 5 at 1080p (scripts/try_w32.sh)
+#endif
+const QueryEntry kQueryW32 = {&QueryLauncherW<NRC_W32_G, 1, 32>::set_smem, &QueryLauncherW<NRC_W32_G, 1, 32>::launch,
+                              NRC_W32_G};
 const QueryEntry kQueryW128 = {&QueryLauncherW<2, 1, 128>::set_smem, &QueryLauncherW<2, 1, 128>::launch, 2};
 constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
 
