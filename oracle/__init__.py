@@ -82,6 +82,13 @@ def lib():
         L.orc_query_batch_w.restype = None
         L.orc_query_batch_w.argtypes = [ctypes.c_int, vp, vp, i64, vp, vp, ctypes.c_uint, vp]
         L.orc_init_weights_w.restype = None; L.orc_init_weights_w.argtypes = [ctypes.c_int, u64, vp]
+        L.orc_forward_stash_w.restype = None; L.orc_forward_stash_w.argtypes = [ctypes.c_int, vp, vp, vp, vp]
+        L.orc_backward_w.restype = None; L.orc_backward_w.argtypes = [ctypes.c_int, vp, vp, vp, vp]
+        L.orc_grad_batch_w.restype = None
+        L.orc_grad_batch_w.argtypes = [ctypes.c_int, vp, vp, vp, i64, vp, vp, d, ctypes.c_uint, vp, vp, vp]
+        L.orc_train_step_w.restype = d
+        L.orc_train_step_w.argtypes = [ctypes.c_int, vp, vp, vp, vp, i64, vp, vp, i64, vp, vp, d, ctypes.c_uint,
+                                       d, d, d, d, d, ctypes.c_int, vp, vp, vp]
         L.orc_gauss.restype = d; L.orc_gauss.argtypes = [d]
         L.orc_freq_sin.restype = None; L.orc_freq_sin.argtypes = [d, vp]
         L.orc_one_blob_gauss.restype = None; L.orc_one_blob_gauss.argtypes = [d, ctypes.c_int, vp]
@@ -189,6 +196,37 @@ def init_weights_w(hw: int, seed: int) -> np.ndarray:
     W = np.zeros(param_count_w(hw), np.float32)
     lib().orc_init_weights_w(int(hw), int(seed) & (2**64 - 1), W.ctypes.data)
     return W
+
+
+def forward_stash_w(hw, W, e):
+    """(H = [h0 (64) | h1..h5 (hw each)], y [3]) for one encoded input at width hw."""
+    W = _c(W, np.float64); e = _c(e, np.float64)
+    H = np.zeros(64 + 5 * hw, np.float64); y = np.zeros(3, np.float64)
+    lib().orc_forward_stash_w(int(hw), W.ctypes.data, e.ctypes.data, H.ctypes.data, y.ctypes.data)
+    return H, y
+
+
+def backward_w(hw, W, H, dy):
+    W = _c(W, np.float64); H = _c(H, np.float64); dy = _c(dy, np.float64)
+    G = np.zeros(param_count_w(hw), np.float64)
+    lib().orc_backward_w(int(hw), W.ctypes.data, H.ctypes.data, dy.ctypes.data, G.ctypes.data)
+    return G
+
+
+def grad_batch_w(hw, W, recs, tgts, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), eps=0.01, flags=FACTORIZE):
+    """grad_batch at hidden width hw (C4): un-normalised gradient sum, loss sum, #bad targets."""
+    W = _c(W, np.float64)
+    assert W.size == param_count_w(hw)
+    recs = _c(recs, np.float32).reshape(-1, 16)
+    tgts = _c(tgts, np.float32).reshape(-1, 3)
+    lo, hi = _c(aabb_lo, np.float32), _c(aabb_hi, np.float32)
+    G = np.zeros(param_count_w(hw), np.float64)
+    ls = np.zeros(1, np.float64)
+    nb = np.zeros(1, np.int64)
+    lib().orc_grad_batch_w(int(hw), W.ctypes.data, recs.ctypes.data, tgts.ctypes.data, recs.shape[0],
+                           lo.ctypes.data, hi.ctypes.data, float(eps), int(flags), G.ctypes.data, ls.ctypes.data,
+                           nb.ctypes.data)
+    return G, float(ls[0]), int(nb[0])
 
 
 # ---------------------------------------------------------------- exact encodings (N4)
@@ -323,10 +361,15 @@ class OracleCache:
 
     def __init__(self, W32=None, seed=1, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), lr=1e-2, b1=0.9, b2=0.99,
                  adam_eps=1e-8, loss_eps=0.01, ema_alpha=0.99, flags=FACTORIZE | CLAMP_QUERY,
-                 ema_printed=False):
-        W32 = init_weights(seed) if W32 is None else np.asarray(W32, np.float32)
+                 ema_printed=False, hidden_width=64):
+        self.hw = int(hidden_width)
+        if W32 is None:
+            W32 = init_weights(seed) if self.hw == 64 else init_weights_w(self.hw, seed)
+        W32 = np.asarray(W32, np.float32)
+        self.P = NPARAM if self.hw == 64 else param_count_w(self.hw)
+        assert W32.size == self.P
         self.w = W32.astype(np.float64)
-        self.m = np.zeros(NPARAM); self.v = np.zeros(NPARAM)
+        self.m = np.zeros(self.P); self.v = np.zeros(self.P)
         self.wbar = self.w.copy()
         self.t = 0
         self.lo = _c(aabb_lo, np.float32); self.hi = _c(aabb_hi, np.float32)
@@ -342,8 +385,17 @@ class OracleCache:
         if n == 0:
             return 0.0
         self.t += 1
-        G = np.zeros(NPARAM, np.float64)
+        G = np.zeros(self.P, np.float64)
         bg = np.zeros(1, np.int64); bt = np.zeros(1, np.int64)
+        if self.hw != 64:
+            l = lib().orc_train_step_w(self.hw, self.w.ctypes.data, self.m.ctypes.data, self.v.ctypes.data,
+                                       self.wbar.ctypes.data, self.t, recs.ctypes.data, tgts.ctypes.data, n,
+                                       self.lo.ctypes.data, self.hi.ctypes.data, self.loss_eps,
+                                       int(self.flags & FACTORIZE), self.lr, self.b1, self.b2, self.adam_eps,
+                                       self.ema_alpha, int(self.ema_printed), G.ctypes.data, bg.ctypes.data,
+                                       bt.ctypes.data)
+            self.bad_grads += int(bg[0]); self.bad_targets += int(bt[0])
+            return (l, G) if return_grad else l
         l = lib().orc_train_step(self.w.ctypes.data, self.m.ctypes.data, self.v.ctypes.data, self.wbar.ctypes.data,
                                  self.t, recs.ctypes.data, tgts.ctypes.data, n, self.lo.ctypes.data,
                                  self.hi.ctypes.data, self.loss_eps, int(self.flags & FACTORIZE), self.lr, self.b1,
@@ -354,4 +406,6 @@ class OracleCache:
 
     def query(self, recs, use_ema=True):
         W = self.wbar if (use_ema and self.ema_alpha > 0) else self.w
+        if self.hw != 64:
+            return query_w(self.hw, W, recs, self.lo, self.hi, self.flags)
         return query(W, recs, self.lo, self.hi, self.flags)

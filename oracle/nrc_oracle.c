@@ -31,6 +31,9 @@
  *       closed form, unbiased flag, hand-evaluated 3-vertex path, linearity)
  *   orc_forward_w / orc_query_batch_w / orc_init_weights_w . pinned (width
  *       embedding into the 64 net, numpy matmul chain, Glorot moments)
+ *   orc_backward_w / orc_grad_batch_w / orc_train_step_w ... pinned (exact
+ *       zero-padding embeddings 32 -> 64 and 64 -> 128 against the pinned
+ *       width-64 functions, central finite differences at hw = 32 and 128)
  *   orc_forward / orc_query ................................ pinned (zero net,
  *       constant net via pad channel, linear chain, homogeneity, permutation)
  *   orc_loss ............................................... pinned (S:L193-195
@@ -656,5 +659,144 @@ double orc_train_step(double* w, double* m, double* v, double* wbar, int64_t t, 
     int64_t bad = orc_adam(w, m, v, G, ORC_NPARAM, t, lr, b1, b2, adam_eps);
     if (bad_grads) *bad_grads = bad;
     orc_ema(wbar, w, ORC_NPARAM, t, ema_a, ema_printed);
+    return lsum / (double)n;
+}
+
+/* ---- width ablation, training (BASELINE.json configs[3]: "32/64/128-neuron
+ * hidden layers at 1080p query+train").  The same definitions as
+ * orc_forward / orc_backward / orc_grad_batch / orc_train_step (P:L662-667,
+ * Eq.(5), Eq.(2)) with hidden width hw: logical layout
+ * of orc_forward_w, P(hw) = orc_param_count_w(hw) parameters.
+ * H holds h_0 (64 values, the encoding) then h_1..h_5 (hw values each). */
+void orc_forward_stash_w(int hw, const double* W, const double* e, double* H, double* y)
+{
+    for (int k = 0; k < ORC_IN; ++k) H[k] = e[k];
+    for (int i = 0; i < 5; ++i) {
+        const int in = i == 0 ? ORC_IN : hw;
+        const double* Wi = W + orc_mat_off_w(hw, i);
+        const double* hin = i == 0 ? H : H + ORC_IN + (int64_t)(i - 1) * hw;
+        double* hout = H + ORC_IN + (int64_t)i * hw;
+        for (int o = 0; o < hw; ++o) {
+            double acc = 0.0;
+            for (int k = 0; k < in; ++k) acc += Wi[(int64_t)in * o + k] * hin[k];
+            hout[o] = acc > 0.0 ? acc : 0.0;
+        }
+    }
+    const double* W5 = W + orc_mat_off_w(hw, 5);
+    const double* h5 = H + ORC_IN + 4 * (int64_t)hw;
+    for (int o = 0; o < 3; ++o) {
+        double acc = 0.0;
+        for (int k = 0; k < hw; ++k) acc += W5[(int64_t)hw * o + k] * h5[k];
+        y[o] = acc;
+    }
+}
+
+/* Reverse mode at width hw (cf. orc_backward): G5 += dy h5^T; delta5 = W5^T dy;
+ * for i = 4..0: g = delta_{i+1} * 1[h_{i+1} > 0] (R17); G_i += g h_i^T;
+ * delta_i = W_i^T g (i > 0). */
+void orc_backward_w(int hw, const double* W, const double* H, const double* dy, double* G)
+{
+    double delta[128], g[128];
+    const double* W5 = W + orc_mat_off_w(hw, 5);
+    double* G5 = G + orc_mat_off_w(hw, 5);
+    const double* h5 = H + ORC_IN + 4 * (int64_t)hw;
+    for (int o = 0; o < 3; ++o)
+        for (int k = 0; k < hw; ++k) G5[(int64_t)hw * o + k] += dy[o] * h5[k];
+    for (int k = 0; k < hw; ++k) {
+        double acc = 0.0;
+        for (int o = 0; o < 3; ++o) acc += W5[(int64_t)hw * o + k] * dy[o];
+        delta[k] = acc;
+    }
+    for (int i = 4; i >= 0; --i) {
+        const int in = i == 0 ? ORC_IN : hw;
+        const double* Wi = W + orc_mat_off_w(hw, i);
+        double* Gi = G + orc_mat_off_w(hw, i);
+        const double* hout = H + ORC_IN + (int64_t)i * hw;
+        const double* hin = i == 0 ? H : H + ORC_IN + (int64_t)(i - 1) * hw;
+        for (int o = 0; o < hw; ++o) g[o] = hout[o] > 0.0 ? delta[o] : 0.0;
+        for (int o = 0; o < hw; ++o)
+            for (int k = 0; k < in; ++k) Gi[(int64_t)in * o + k] += g[o] * hin[k];
+        if (i > 0) {
+            for (int k = 0; k < in; ++k) {
+                double acc = 0.0;
+                for (int o = 0; o < hw; ++o) acc += Wi[(int64_t)in * o + k] * g[o];
+                delta[k] = acc;
+            }
+        }
+    }
+}
+
+/* orc_grad_batch at width hw: un-normalised gradient sum, loss sum, masked
+ * non-finite targets; the same fixed chunking (deterministic). */
+void orc_grad_batch_w(int hw, const double* W, const float* recs, const float* tgts, int64_t n, const float* lo,
+                      const float* hi, double eps, unsigned flags, double* G, double* loss_sum,
+                      int64_t* n_bad_targets)
+{
+    const int64_t P = orc_param_count_w(hw);
+    double* Gc = (double*)calloc((size_t)ORC_CHUNKS * (size_t)P, sizeof(double));
+    double lc[ORC_CHUNKS];
+    int64_t bc[ORC_CHUNKS];
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int ch = 0; ch < ORC_CHUNKS; ++ch) {
+        int64_t i0 = n * ch / ORC_CHUNKS, i1 = n * (ch + 1) / ORC_CHUNKS;
+        double* Gk = Gc + (size_t)ch * (size_t)P;
+        double lsum = 0.0;
+        int64_t nbad = 0;
+        for (int64_t i = i0; i < i1; ++i) {
+            const float* rec = recs + 16 * i;
+            const float* tg = tgts + 3 * i;
+            if (!(isfinite(tg[0]) && isfinite(tg[1]) && isfinite(tg[2]))) {
+                ++nbad;
+                continue;
+            }
+            double e[64], H[64 + 5 * 128], y[3], yhat[3], t[3], dyhat[3], dy[3];
+            orc_encode(rec, lo, hi, e);
+            orc_forward_stash_w(hw, W, e, H, y);
+            for (int c = 0; c < 3; ++c) {
+                double f = (flags & ORC_FACTORIZE) ? (double)rec[10 + c] + (double)rec[13 + c] : 1.0;
+                yhat[c] = y[c] * f;
+                t[c] = tg[c];
+            }
+            lsum += orc_loss(yhat, t, eps, dyhat);
+            for (int c = 0; c < 3; ++c) {
+                double f = (flags & ORC_FACTORIZE) ? (double)rec[10 + c] + (double)rec[13 + c] : 1.0;
+                dy[c] = dyhat[c] * f;
+            }
+            orc_backward_w(hw, W, H, dy, Gk);
+        }
+        lc[ch] = lsum;
+        bc[ch] = nbad;
+    }
+    memset(G, 0, sizeof(double) * (size_t)P);
+    double lsum = 0.0;
+    int64_t nbad = 0;
+    for (int ch = 0; ch < ORC_CHUNKS; ++ch) {
+        const double* Gk = Gc + (size_t)ch * (size_t)P;
+        for (int64_t j = 0; j < P; ++j) G[j] += Gk[j];
+        lsum += lc[ch];
+        nbad += bc[ch];
+    }
+    free(Gc);
+    if (loss_sum) *loss_sum = lsum;
+    if (n_bad_targets) *n_bad_targets = nbad;
+}
+
+/* orc_train_step at width hw (w, m, v, wbar: fp64 arrays of P(hw)). */
+double orc_train_step_w(int hw, double* w, double* m, double* v, double* wbar, int64_t t, const float* recs,
+                        const float* tgts, int64_t n, const float* lo, const float* hi, double loss_eps,
+                        unsigned flags, double lr, double b1, double b2, double adam_eps, double ema_a,
+                        int ema_printed, double* G_out, int64_t* bad_grads, int64_t* bad_targets)
+{
+    const int64_t P = orc_param_count_w(hw);
+    double lsum = 0.0;
+    if (n <= 0) return 0.0;
+    double* G = (double*)malloc(sizeof(double) * (size_t)P);
+    orc_grad_batch_w(hw, w, recs, tgts, n, lo, hi, loss_eps, flags, G, &lsum, bad_targets);
+    for (int64_t j = 0; j < P; ++j) G[j] /= (double)n;
+    if (G_out) memcpy(G_out, G, sizeof(double) * (size_t)P);
+    int64_t bad = orc_adam(w, m, v, G, P, t, lr, b1, b2, adam_eps);
+    if (bad_grads) *bad_grads = bad;
+    orc_ema(wbar, w, P, t, ema_a, ema_printed);
+    free(G);
     return lsum / (double)n;
 }
