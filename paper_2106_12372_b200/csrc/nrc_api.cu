@@ -133,8 +133,8 @@ StateLayout layout(int W) {
     L.ema = take(pf);
     L.wimg = take(size_t(wi.img));
     L.eimg = take(size_t(wi.img));
-    // training (hidden width 64 only) scratch
-    L.partials = take(W == 64 ? sizeof(float) * kParamPadded * kMaxPartials : 256);
+    // training scratch: per-CTA fp32 gradient partials (padded layout of the width)
+    L.partials = take(sizeof(float) * size_t(wi.padded) * kMaxPartials);
     L.loss_part = take(sizeof(float) * kMaxPartials);
     L.counters = take(sizeof(unsigned long long) * 4);
     L.total = o;
@@ -164,6 +164,7 @@ struct nrc_handle {
     unsigned long long gbar = 0;  // arrivals so far on the train kernel's grid-barrier counter
     unsigned long long gbarA = 0; // arrivals so far on its phase-A (W3..W5 partials written) counter
     bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
+    bool train_generic = false;   // width 64 through the width-generic kernels (NRC_TRAIN_GENERIC=1: cross-checks)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
     int train_ctas = 0;           // cap on the train grid (0: one CTA per tile up to all SMs)
@@ -412,6 +413,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     }
     h->query_cfg = 0;
     if (const char* e = std::getenv("NRC_COOP")) h->coop = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NRC_TRAIN_GENERIC")) h->train_generic = std::atoi(e) != 0;
     if (const char* e = std::getenv("NRC_QUERY_CTAS")) h->query_ctas = std::atoi(e);
     if (const char* e = std::getenv("NRC_TRAIN_CTAS")) h->train_ctas = std::atoi(e);
     if (const char* e = std::getenv("NRC_QUERY_CFG")) h->query_cfg = std::atoi(e);
@@ -428,6 +430,16 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 kTrainSmemBytes),
                         "cudaFuncSetAttribute(train exact)")) != NRC_OK)
+        return bail(s);
+    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TrainW<32>::kSmemBytes),
+                        "cudaFuncSetAttribute(train w32)")) != NRC_OK ||
+        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TrainW<64>::kSmemBytes),
+                        "cudaFuncSetAttribute(train w64)")) != NRC_OK ||
+        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TrainW<128>::kSmemBytes),
+                        "cudaFuncSetAttribute(train w128)")) != NRC_OK)
         return bail(s);
 
     // Glorot-uniform init from the counter-based splitmix64 stream (R16):
@@ -461,11 +473,13 @@ nrc_status nrc_destroy(nrc_handle* h) {
     return NRC_OK;
 }
 
-// training kernels are built for the paper's width only (the C4 ablation is query-only)
+// hidden width 64 trains through the fused persistent kernel; 32 and 128 (the
+// C4 width ablation) through the width-generic partials + Adam kernels
 static nrc_status check_train_width(nrc_handle* h) {
-    if (h->wi.W == 64) return NRC_OK;
-    return fail(h, NRC_ERR_UNSUPPORTED, "training is built for hidden_width 64 only (width ablation is query-only)");
+    if (width_supported(uint32_t(h->wi.W))) return NRC_OK;
+    return fail(h, NRC_ERR_UNSUPPORTED, "unsupported hidden width for training");
 }
+static bool train_generic(const nrc_handle* h) { return h->wi.W != 64 || h->train_generic; }
 static nrc_status check_handle(nrc_handle* h) {
     if (!h || !h->state) return NRC_ERR_STATE;
     int dev = -1;
@@ -562,9 +576,8 @@ static StepCoef step_coef(const nrc_config& c, uint64_t t) {
 // partials only (PDL launch; the caller reduces).  nsteps >= 1: fused
 // cooperative launch running nsteps optimisation steps (reduce + Adam + EMA
 // inside), batch-mean losses to d_losses[0..nsteps).  Returns #partials.
-static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
-                               const Gather& gth, cudaStream_t st, int* nparts, uint32_t nsteps = 0,
-                               float* d_losses = nullptr) {
+static TrainArgs train_args(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                            const Gather& gth) {
     TrainArgs ta{};
     ta.rec = reinterpret_cast<const float*>(d_rec);
     ta.tgt = d_tgt;
@@ -589,11 +602,70 @@ static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const flo
     ta.loss_part = h->d_loss_part();
     ta.bad_targets = h->d_counters() + 1;
     ta.dbg = h->dbg;
+    return ta;
+}
+static int train_grid(const nrc_handle* h, uint32_t n) {
     const uint32_t ntiles = (n + kTile - 1) / kTile;
     int grid = int(ntiles);
     int cap = h->num_sms < kMaxPartials ? h->num_sms : kMaxPartials;
     if (h->train_ctas > 0 && h->train_ctas < cap) cap = h->train_ctas;
-    if (grid > cap) grid = cap;
+    return grid > cap ? cap : grid;
+}
+// Width-generic partials kernel (nrc_train_w.cuh): one step over n rows.
+static nrc_status launch_train_w(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                                 const Gather& gth, cudaStream_t st, int* nparts) {
+    const TrainArgs ta = train_args(h, d_rec, d_tgt, n, gth);
+    const int grid = train_grid(h, n);
+    *nparts = grid;
+    if (h->wi.W == 32)
+        nrc_train_w_kernel<32><<<grid, 128, TrainW<32>::kSmemBytes, st>>>(ta);
+    else if (h->wi.W == 128)
+        nrc_train_w_kernel<128><<<grid, 128, TrainW<128>::kSmemBytes, st>>>(ta);
+    else
+        nrc_train_w_kernel<64><<<grid, 128, TrainW<64>::kSmemBytes, st>>>(ta);
+    NRC_LAUNCHED(h, "nrc_train_w_kernel");
+    return NRC_OK;
+}
+static AdamWArgs adam_w_args(nrc_handle* h) {
+    AdamWArgs aa{};
+    const nrc_config& c = h->cfg;
+    aa.w = h->d_w();
+    aa.m = h->d_m();
+    aa.v = h->d_v();
+    aa.ema = h->d_ema();
+    aa.wimg = h->d_wimg();
+    aa.eimg = h->d_eimg();
+    aa.lr = c.learning_rate;
+    aa.b1 = c.adam_beta1;
+    aa.b2 = c.adam_beta2;
+    aa.eps = c.adam_eps;
+    const StepCoef k = step_coef(c, h->step);  // already incremented
+    aa.inv_bc1 = k.inv_bc1;
+    aa.inv_bc2 = k.inv_bc2;
+    aa.ema_c1 = k.ema_c1;
+    aa.ema_c2 = k.ema_c2;
+    aa.bad_grads = h->d_counters() + 0;
+    aa.loss_part = h->d_loss_part();
+    return aa;
+}
+static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t st) {
+    const int blocks = (h->wi.padded + 255) / 256;
+    if (h->wi.W == 32)
+        nrc_adam_w_kernel<32><<<blocks, 256, 0, st>>>(aa);
+    else if (h->wi.W == 128)
+        nrc_adam_w_kernel<128><<<blocks, 256, 0, st>>>(aa);
+    else
+        nrc_adam_w_kernel<64><<<blocks, 256, 0, st>>>(aa);
+    NRC_LAUNCHED(h, "nrc_adam_w_kernel");
+    return NRC_OK;
+}
+
+static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                               const Gather& gth, cudaStream_t st, int* nparts, uint32_t nsteps = 0,
+                               float* d_losses = nullptr) {
+    if (train_generic(h) && nsteps == 0) return launch_train_w(h, d_rec, d_tgt, n, gth, st, nparts);
+    TrainArgs ta = train_args(h, d_rec, d_tgt, n, gth);
+    const int grid = train_grid(h, n);
     *nparts = grid;
     if (nsteps == 0) {
         ta.fused = 0;
@@ -663,7 +735,46 @@ static AdamArgs adam_args(nrc_handle* h) {
 static nrc_status train_step_impl(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
                                   const Gather& gth, float* d_losses, uint32_t nsteps, cudaStream_t st) {
     int np = 0;
-    return launch_train(h, d_rec, d_tgt, n, gth, st, &np, nsteps, d_losses);
+    if (!train_generic(h)) return launch_train(h, d_rec, d_tgt, n, gth, st, &np, nsteps, d_losses);
+    // width-generic: per step the partials kernel, then reduce + Adam + EMA
+    uint32_t launches = 0;
+    for (uint32_t k = 0; k < nsteps; ++k) {
+        Gather g = gth;
+        g.offset = gth.offset + uint64_t(k) * n;  // step k of the batch sequence
+        nrc_status s = launch_train_w(h, d_rec, d_tgt, n, g, st, &np);
+        if (s != NRC_OK) return s;
+        h->step += 1;
+        AdamWArgs aa = adam_w_args(h);
+        aa.partials = h->d_partials();
+        aa.np = np;
+        aa.apply = 1;
+        aa.inv_n = float(1.0 / double(n));
+        aa.nloss = np;
+        aa.loss_scale = aa.inv_n;
+        aa.loss_out = d_losses ? d_losses + k : nullptr;
+        if ((s = launch_adam_w(h, aa, st)) != NRC_OK) return s;
+        launches += 2;
+    }
+    h->launches = launches;
+    return NRC_OK;
+}
+// partials -> logical gradient sum + loss sum (multi-GPU backward)
+static nrc_status reduce_partials(nrc_handle* h, int np, float* d_grad, float* d_loss_sum, cudaStream_t st) {
+    if (train_generic(h)) {
+        AdamWArgs aa = adam_w_args(h);
+        aa.partials = h->d_partials();
+        aa.np = np;
+        aa.grad_out = d_grad;
+        aa.apply = 0;
+        aa.nloss = np;
+        aa.loss_scale = 1.0f;
+        aa.loss_out = d_loss_sum;
+        return launch_adam_w(h, aa, st);
+    }
+    nrc_reduce_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
+                                                                  d_loss_sum);
+    NRC_LAUNCHED(h, "nrc_reduce_kernel");
+    return NRC_OK;
 }
 
 static nrc_status check_train_args(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint64_t n,
@@ -696,7 +807,7 @@ nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const floa
     if (!d_grad || !aligned(d_grad, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_backward: bad d_grad");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (n_local == 0) {  // contributes a zero gradient to the all-reduce
-        NRC_CUDA(h, cudaMemsetAsync(d_grad, 0, sizeof(float) * kParamLogical, st));
+        NRC_CUDA(h, cudaMemsetAsync(d_grad, 0, sizeof(float) * size_t(h->wi.logical), st));
         if (d_loss_sum) NRC_CUDA(h, cudaMemsetAsync(d_loss_sum, 0, sizeof(float), st));
         return NRC_OK;
     }
@@ -704,10 +815,7 @@ nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const floa
     int np = 0;
     Gather g{false, 0, 0, 0, 0, 0};
     if ((s = launch_train(h, d_rec, d_tgt, n_local, g, st, &np)) != NRC_OK) return s;
-    nrc_reduce_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
-                                                                  d_loss_sum);
-    NRC_LAUNCHED(h, "nrc_reduce_kernel");
-    return NRC_OK;
+    return reduce_partials(h, np, d_grad, d_loss_sum, st);
 }
 
 nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
@@ -723,7 +831,7 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint32_t n = row_end - row_begin;
     if (n == 0) {
-        NRC_CUDA(h, cudaMemsetAsync(d_grad, 0, sizeof(float) * kParamLogical, st));
+        NRC_CUDA(h, cudaMemsetAsync(d_grad, 0, sizeof(float) * size_t(h->wi.logical), st));
         if (d_loss_sum) NRC_CUDA(h, cudaMemsetAsync(d_loss_sum, 0, sizeof(float), st));
         return NRC_OK;
     }
@@ -732,10 +840,7 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
     nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
     int np = 0;
     if ((s = launch_train(h, d_rec, d_tgt, n, g, st, &np)) != NRC_OK) return s;
-    nrc_reduce_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
-                                                                  d_loss_sum);
-    NRC_LAUNCHED(h, "nrc_reduce_kernel");
-    return NRC_OK;
+    return reduce_partials(h, np, d_grad, d_loss_sum, st);
 }
 
 nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, void* stream) {
@@ -746,6 +851,13 @@ nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_gl
     if (n_global == 0) return NRC_OK;
     if (!d_grad_sum || !aligned(d_grad_sum, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply: bad grad");
     h->step += 1;
+    if (train_generic(h)) {
+        AdamWArgs aw = adam_w_args(h);
+        aw.grad_logical = d_grad_sum;
+        aw.apply = 1;
+        aw.inv_n = float(1.0 / double(n_global));
+        return launch_adam_w(h, aw, static_cast<cudaStream_t>(stream));
+    }
     AdamArgs aa = adam_args(h);
     aa.src = d_grad_sum;
     aa.nsrc = 1;

@@ -14,6 +14,7 @@
 #include "nrc_fused_query.cuh"
 #include "nrc_query_ts.cuh"
 #include "nrc_train.cuh"
+#include "nrc_train_w.cuh"
 
 namespace nrc {
 

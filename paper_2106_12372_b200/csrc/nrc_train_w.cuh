@@ -1,0 +1,440 @@
+// nrc_train_w.cuh -- training at hidden width W in {32, 64, 128} (width
+// ablation, BASELINE.json configs[3] "32/64/128-neuron hidden layers at 1080p
+// query+train").  The same rows a0, a1, a4-a8 of SURVEY 8(a) as
+// nrc_train.cuh (LCG gather P:L487-491 -> encode -> forward with the stash in
+// SMEM -> Eq. 5 loss gradient P:L886-894 -> dgrad + wgrad on tcgen05,
+// P:L662-667), as one partials kernel per step followed by the reduce + Adam +
+// EMA kernel (Eq. 2).  The width-64 product path keeps its fused
+// persistent kernel; this one trades the grid barriers for width generality.
+//
+// Layout per CTA (one 128-row tile at a time, 4 row warps, warp 0 issues):
+//  * stash: h0 (128 x 64 fp16) and h1..h5 (128 x W fp16, W/64 blocks of
+//    128 lines of 128 B, SWIZZLE_128B; at W = 32 a line holds 32 values and
+//    its other half stays zero).  The gradient g_j = delta_j * 1[h_j > 0]
+//    overwrites h_j in place once dgrad_j and wgrad_j (the last readers of
+//    h_j) have completed, so no separate gradient tiles exist.
+//  * weights: W <= 64 keeps the whole fp16 image resident (one TMA load per
+//    launch); W = 128 (151 KB image + 176 KB stash > 227 KB) streams one
+//    layer (<= 32 KB) at a time into one buffer: W_{L+1} is fetched while
+//    the epilogue of layer L runs, and W5 serves the forward and dgrad_5.
+//  * TMEM: fwd / dgrad accumulator (max(W, 64) columns) + two wgrad
+//    accumulators used alternately: G_{j+1} is drained to the CTA's fp32
+//    partial while round j's MMAs run.
+// MMA shapes (M x N x K, A/B majors):
+//   forward L   128 x rows(L) x cols(L)      A = h_L K-major, B = W_L K-major
+//   dgrad j     128 x max(W,64) x rows(j)    A = g_{j+1} K-major, B = W_j MN-major
+//   wgrad j     M x N x 128 rows             A = g_{j+1}^T MN-major, B = h_j MN-major
+//               M = 128 (W = 128, j < 5) else 64 (rows beyond W / 16 are 0)
+//               N = 64 (j = 0) else max(W, 64) (columns beyond W are 0)
+#pragma once
+#include "nrc_train.cuh"
+
+namespace nrc {
+
+template <int W>
+struct TrainW {
+    using D = NetDims<W>;
+    static constexpr bool kStream = W > 64;        // per-layer weight streaming
+    static constexpr int kKB = (W + 63) / 64;      // 64-wide blocks of a hidden activation
+    static constexpr int kNW = W > 64 ? W : 64;    // dgrad N, wgrad N (j >= 1), accumulator columns
+    static constexpr int kWBytes = kStream ? kKB * W * 128 : (D::kImg + 1023) / 1024 * 1024;
+    static constexpr int kStashBytes = kTileBytes + 5 * kKB * kTileBytes;
+    static constexpr int kSmemBytes = 1024 + kWBytes + kStashBytes + kTileBytes + 64;
+    static constexpr uint32_t kTmemCols = 3 * kNW <= 256 ? 256u : 512u;
+    __host__ __device__ static constexpr int slot_off(int i) { return i == 0 ? 0 : kTileBytes + (i - 1) * kKB * kTileBytes; }
+    // wgrad_j's M: the out-neuron rows (M = 64 holds rows 16 w + lane of warp w, lane < 16)
+    __host__ __device__ static constexpr int wg_m(int j) { return (j < 5 && W > 64) ? 128 : 64; }
+    __host__ __device__ static constexpr int wg_n(int j) { return j == 0 ? 64 : kNW; }
+};
+static_assert(TrainW<128>::kSmemBytes <= 232448 && TrainW<64>::kSmemBytes <= 232448, "227 KB of SMEM per CTA");
+
+// SWIZZLE_128B descriptor with an explicit leading byte offset (the stride
+// between 64-wide MN blocks of an MN-major operand, SBO = 8 lines = 1024 B).
+__device__ __forceinline__ uint64_t desc_mn_lbo(uint32_t saddr, uint32_t lbo) { return make_sdesc(saddr, lbo, 1024u); }
+
+// record + target of batch row `row` (zeros past the batch; LCG gather or
+// peer parts as in nrc_train_kernel)
+__device__ __forceinline__ void train_gather_row(const TrainArgs& a, uint32_t row, float (&rec)[16], float (&tg)[3]) {
+    if (row < a.n) {
+        const uint64_t k = row;
+        const uint64_t idx = a.gather ? lcg_perm(a.offset + k, a.lcg_n, a.lcg_a, a.lcg_c, a.lcg_m) : k;
+        const float* rsrc = a.rec + idx * kRecFloats;
+        const float* tsrc = a.tgt + idx * 3;
+        if (a.n_parts > 0) {
+            const uint32_t p = uint32_t(idx / a.part_n);
+            const uint64_t o = idx - uint64_t(p) * a.part_n;
+            rsrc = a.rec_parts[p] + o * kRecFloats;
+            tsrc = a.tgt_parts[p] + o * 3;
+        }
+        load_record_global(rsrc, rec);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tg[c] = __ldg(tsrc + c);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) rec[i] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tg[c] = 0.0f;
+    }
+}
+
+// One training step's partials at width W: CTA c processes tiles c, c + grid,
+// ... and writes its un-normalised fp32 gradient sum (padded layout of
+// NetDims<W>) to partials[c] and its loss sum to loss_part[c].
+template <int W>
+__global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
+    using D = NetDims<W>;
+    using T = TrainW<W>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    const uint32_t tid = threadIdx.x, r = tid, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sW_a = smem_u32(smem);
+    const uint32_t sH_a = sW_a + T::kWBytes;
+    const uint32_t sG6_a = sH_a + T::kStashBytes;  // dL/dy tile (columns 0..2 used)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::kWBytes + T::kStashBytes + kTileBytes);
+    uint64_t* wbar = &bars[0];
+    uint64_t* mma_bar = &bars[1];
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+    float* red = reinterpret_cast<float*>(bars + 3);  // 4 floats + 4 u32
+
+    if (tid == 0) {
+        mbar_init(wbar, 1);
+        mbar_init(mma_bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc(tmem_slot, T::kTmemCols);
+        tmem_relinquish();
+    }
+    // zero the dL/dy tile (only chunk 0 of a line is rewritten per tile) and, at
+    // W < 64, the hidden slots (the upper half of each line is never written)
+    {
+        const uint32_t z0 = W < 64 ? sH_a + kTileBytes : sG6_a;
+        for (uint32_t off = z0 + tid * 16; off < sG6_a + kTileBytes; off += 128 * 16) st_shared_v4(off, 0, 0, 0, 0);
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t lane_off = (warp * 32u) << 16;
+    const uint32_t t_acc = tmem_base;
+    auto t_g = [&](int j) -> uint32_t { return tmem_base + uint32_t(T::kNW) * (1u + uint32_t(j & 1)); };
+    auto slot = [&](int i) -> uint32_t { return sH_a + uint32_t(T::slot_off(i)); };
+    auto wl = [&](int L) -> uint32_t { return T::kStream ? sW_a : sW_a + uint32_t(D::img_off(L)); };
+
+    uint32_t phase = 0, w_phase = 0;
+    // weight bytes of layer L (streamed) or the whole image (resident), issued by thread 0
+    auto fetch = [&](int L) {
+        const uint32_t off = T::kStream ? uint32_t(D::img_off(L)) : 0u;
+        const uint32_t bytes = T::kStream ? uint32_t(D::img_off(L + 1) - D::img_off(L)) : uint32_t(D::kImg);
+        mbar_arrive_expect_tx(wbar, bytes);
+        for (uint32_t o = 0; o < bytes; o += 8192u) {
+            const uint32_t b = bytes - o < 8192u ? bytes - o : 8192u;
+            bulk_g2s(smem + o, a.wimg + off + o, b, wbar);
+        }
+    };
+    auto wwait = [&]() {  // warp 0 only (the MMA issuer reads the weights)
+        mbar_wait(wbar, w_phase);
+        w_phase ^= 1;
+    };
+    auto mma_wait = [&]() {
+        mbar_wait(mma_bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+    };
+    auto sync_rows = [&]() {
+        tc_fence_before();
+        fence_async_smem();
+        __syncthreads();
+        tc_fence_after();
+    };
+    // forward layer L (whole warp 0, converged; one elected lane issues + commits)
+    auto issue_fwd = [&](int L) {
+        const uint32_t idesc = warp_uniform(make_idesc(128, D::rows(L), 0, 0));
+        const uint64_t a0 = warp_uniform(desc_kmajor(slot(L), 0));
+        const uint64_t a1 = warp_uniform(desc_kmajor(slot(L) + kTileBytes, 0));
+        const uint64_t b0 = warp_uniform(desc_kmajor(wl(L), 0));
+        const uint64_t b1 = warp_uniform(desc_kmajor(wl(L) + uint32_t(D::rows(L)) * 128u, 0));
+        const uint32_t d = warp_uniform(t_acc);
+        tc_fence_after();
+        if (elect_one()) {
+            if (D::cols(L) == 32) {
+                umma_f16(d, a0, b0, idesc, 0u);
+                umma_f16(d, a0 + 2, b0 + 2, idesc, 1u);
+            } else {
+                umma_ss4<kKmajStep, kKmajStep>(d, a0, b0, idesc, 0u);
+                if (D::cols(L) == 128) umma_ss4<kKmajStep, kKmajStep>(d, a1, b1, idesc, 1u);
+            }
+            umma_commit(mma_bar);
+        }
+        __syncwarp();
+    };
+    // round j of the backward pass: dgrad_j (j >= 1) and wgrad_j, one commit
+    auto issue_bwd = [&](int j) {
+        const uint32_t gsrc = j == 5 ? sG6_a : slot(j + 1);  // g_{j+1}
+        const uint32_t d_acc = warp_uniform(t_acc), d_g = warp_uniform(t_g(j));
+        // dgrad: delta_j = g_{j+1} W_j (K = rows(j) out-neurons)
+        const uint32_t id_d = warp_uniform(make_idesc(128, T::kNW, 0, 1));
+        const uint64_t da0 = warp_uniform(desc_kmajor(gsrc, 0));
+        const uint64_t da1 = warp_uniform(desc_kmajor(gsrc + kTileBytes, 0));
+        const uint64_t db = warp_uniform(desc_mn_lbo(wl(j), uint32_t(D::rows(j)) * 128u));
+        // wgrad: G_j += g_{j+1}^T h_j (K = 128 rows)
+        const uint32_t id_w = warp_uniform(make_idesc(T::wg_m(j), T::wg_n(j), 1, 1));
+        const uint64_t wa = warp_uniform(desc_mn_lbo(gsrc, kTileBytes));
+        const uint64_t wb = warp_uniform(desc_mn_lbo(slot(j), kTileBytes));
+        tc_fence_after();
+        if (elect_one()) {
+            if (j >= 1) {
+                if (j == 5) {
+                    umma_f16(d_acc, da0, db, id_d, 0u);  // K = 16 (W5 padded rows)
+                } else if (W == 32) {
+                    umma_f16(d_acc, da0, db, id_d, 0u);
+                    umma_f16(d_acc, da0 + kKmajStep, db + kMNmajStep, id_d, 1u);
+                } else {
+                    umma_ss4<kKmajStep, kMNmajStep>(d_acc, da0, db, id_d, 0u);
+                    if (W == 128) umma_ss4<kKmajStep, kMNmajStep>(d_acc, da1, db + 4 * kMNmajStep, id_d, 1u);
+                }
+            }
+            umma_ss8<kMNmajStep, kMNmajStep>(d_g, wa, wb, id_w, 0u);
+            umma_commit(mma_bar);
+        }
+        __syncwarp();
+    };
+    float* part = a.partials + size_t(blockIdx.x) * D::kPadded;
+    // drain G_j (TMEM) into this CTA's partial (plain store on the first tile, else add)
+    auto flush_g = [&](int j, bool first) {
+        const int M = T::wg_m(j);
+        const int o = M == 128 ? int(r) : int(warp) * 16 + int(lane);
+        const int rows_pad = j < 5 ? W : kOutPad;
+        const bool valid = (M == 128 || lane < 16) && o < rows_pad;
+        constexpr int kMaxParts32 = (W > 64 ? W : 64) / 32;
+#pragma unroll
+        for (int p = 0; p < kMaxParts32; ++p) {
+            if (32 * p >= D::cols(j)) break;
+            uint32_t v[32];
+            tmem_ld32(t_g(j) + lane_off + 32u * p, v);
+            if (valid) {
+                float4* dst = reinterpret_cast<float4*>(part + D::pad_off(j) + o * D::cols(j) + 32 * p);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float4 x = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                           __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                    if (!first) {
+                        const float4 y = dst[q];
+                        x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
+                    }
+                    dst[q] = x;
+                }
+            }
+        }
+    };
+    // g_j = delta_j * 1[h_j > 0] written over h_j (ReLU'(0) = 0, R17)
+    auto mask_epilogue = [&](int j) {
+#pragma unroll
+        for (int p = 0; p < W / 32; ++p) {
+            uint32_t v[32];
+            tmem_ld32(t_acc + lane_off + 32u * p, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t off = slot(j) + uint32_t(p >> 1) * kTileBytes + swz(r, uint32_t((p & 1) * 4 + q));
+                const uint4 hv = ld_shared_v4(off);
+                const float* f = reinterpret_cast<const float*>(v) + 8 * q;
+                st_shared_v4(off, pack_h2(f[0], f[1]) & relu_mask(hv.x), pack_h2(f[2], f[3]) & relu_mask(hv.y),
+                             pack_h2(f[4], f[5]) & relu_mask(hv.z), pack_h2(f[6], f[7]) & relu_mask(hv.w));
+            }
+        }
+    };
+
+    float loss_sum = 0.0f;
+    uint32_t bad = 0;
+    const uint32_t ntiles = (a.n + kTile - 1) / kTile;
+    if (tid == 0 && blockIdx.x < ntiles) fetch(0);  // W0 (streamed) or the whole image
+    bool first = true;
+#pragma unroll 1
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const bool more = tile + gridDim.x < ntiles;
+        const uint32_t row = tile * kTile + r;
+        const bool valid = row < a.n;
+        float rec[16], tg[3];
+        train_gather_row(a, row, rec, tg);
+        {
+            uint32_t h[32];
+            encode_record<false>(rec, a.ep, h);
+            store_row_swz(slot(0), r, h);
+        }
+        sync_rows();
+        // ---------------- forward: h_{L+1} = relu(W_L h_L), y = W5 h5
+#pragma unroll 1
+        for (int L = 0; L < 6; ++L) {
+            if (warp == 0) {
+                if (T::kStream || (L == 0 && first)) wwait();
+                issue_fwd(L);
+            }
+            mma_wait();
+            if (T::kStream && L < 5 && tid == 0) fetch(L + 1);  // the buffer is free
+            if (L == 5) break;
+#pragma unroll
+            for (int p = 0; p < W / 32; ++p) {
+                uint32_t v[32];
+                tmem_ld32(t_acc + lane_off + 32u * p, v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float* f = reinterpret_cast<const float*>(v) + 8 * q;
+                    st_shared_v4(slot(L + 1) + uint32_t(p >> 1) * kTileBytes + swz(r, uint32_t((p & 1) * 4 + q)),
+                                 pack_h2_relu(f[0], f[1]), pack_h2_relu(f[2], f[3]), pack_h2_relu(f[4], f[5]),
+                                 pack_h2_relu(f[6], f[7]));
+                }
+            }
+            sync_rows();
+        }
+        // ---------------- relative L2 loss, Eq.(5) (R8-R10, R13)
+        {
+            uint32_t v[4];
+            tmem_ld4(t_acc + lane_off, v);
+            const bool use = valid && isfinite(tg[0]) && isfinite(tg[1]) && isfinite(tg[2]);
+            if (valid && !use) ++bad;
+            float yh[3], f[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                f[c] = (a.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
+                yh[c] = __uint_as_float(v[c]) * f[c];
+            }
+            const float lam = 0.2126f * yh[0] + 0.7152f * yh[1] + 0.0722f * yh[2];
+            const float den = lam * lam + a.loss_eps;
+            const float inv3den = 1.0f / (3.0f * den);
+            float gy[3], l = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float d = yh[c] - tg[c];
+                l += d * d;
+                gy[c] = use ? 2.0f * d * f[c] * inv3den : 0.0f;
+            }
+            if (use) loss_sum += l * inv3den;
+            st_shared_v4(sG6_a + swz(r, 0), pack_h2(gy[0], gy[1]), pack_h2(gy[2], 0.0f), 0u, 0u);
+        }
+        sync_rows();
+        // ---------------- backward: round j = dgrad_j + wgrad_j, then
+        // G_{j+1} drains while they run; g_j overwrites h_j after both complete
+#pragma unroll 1
+        for (int j = 5; j >= 1; --j) {
+            if (warp == 0) {
+                if (T::kStream && j < 5) wwait();  // W_j (W5 is still resident from the forward)
+                issue_bwd(j);
+            }
+            if (j < 5) flush_g(j + 1, first);
+            mma_wait();
+            if (T::kStream && tid == 0) {
+                if (j > 1)
+                    fetch(j - 1);
+                else if (more)
+                    fetch(0);  // the next tile's W0
+            }
+            mask_epilogue(j);
+            sync_rows();
+        }
+        if (warp == 0) issue_bwd(0);  // G_0 += g_1^T h_0 (no gradient w.r.t. the encoding)
+        flush_g(1, first);
+        mma_wait();
+        flush_g(0, first);
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        first = false;
+    }
+    // ---------------- this CTA's loss sum (fixed order over the 4 row warps)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        loss_sum += __shfl_xor_sync(0xffffffffu, loss_sum, off);
+        bad += __shfl_xor_sync(0xffffffffu, bad, off);
+    }
+    if (lane == 0) {
+        red[warp] = loss_sum;
+        reinterpret_cast<uint32_t*>(red + 4)[warp] = bad;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+        a.loss_part[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+        const uint32_t* b = reinterpret_cast<const uint32_t*>(red + 4);
+        const uint32_t nb = b[0] + b[1] + b[2] + b[3];
+        if (nb) atomicAdd(a.bad_targets, (unsigned long long)nb);
+    }
+    if (warp == 0) tmem_dealloc(tmem_base, T::kTmemCols);
+}
+
+// Reduce + Adam + EMA at width W: thread j owns padded parameter j.
+//   partials != nullptr: g = sum over p < np of partials[p][j] (ascending p);
+//   else g = grad_logical[j] (logical layout = padded prefix; W5 pad rows 0).
+//   grad_out: the reduced sum in the logical layout (nrc_train_backward).
+//   apply: Adam (R11) + EMA (Eq. 2, R12) on g * inv_n, writing
+//   the fp32 state and both fp16 operand images.
+struct AdamWArgs {
+    const float* partials;
+    int np;
+    const float* grad_logical;
+    float* grad_out;
+    int apply;
+    float inv_n;
+    float *w, *m, *v, *ema;
+    uint8_t *wimg, *eimg;
+    float lr, b1, b2, eps, inv_bc1, inv_bc2, ema_c1, ema_c2;
+    unsigned long long* bad_grads;
+    const float* loss_part;  // optional: loss partial sums -> loss_out (x loss_scale)
+    int nloss;
+    float loss_scale;
+    float* loss_out;
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
+    using D = NetDims<W>;
+    const int j = int(blockIdx.x * blockDim.x + threadIdx.x);
+    if (blockIdx.x == 0 && threadIdx.x < 32 && a.loss_out != nullptr) {
+        float s = 0.0f;
+        for (int p = int(threadIdx.x); p < a.nloss; p += 32) s += a.loss_part[p];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (threadIdx.x == 0) *a.loss_out = s * a.loss_scale;
+    }
+    if (j >= D::kPadded) return;
+    float g = 0.0f;
+    if (a.partials != nullptr) {
+        const float* src = a.partials + j;
+        int p = 0;
+#pragma unroll 1
+        for (; p + 8 <= a.np; p += 8) {
+            float x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + size_t(p + u) * D::kPadded);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) g += x[u];
+        }
+        for (; p < a.np; ++p) g += __ldcg(src + size_t(p) * D::kPadded);
+    } else {
+        g = j < D::kLogical ? a.grad_logical[j] : 0.0f;
+    }
+    if (a.grad_out != nullptr && j < D::kLogical) a.grad_out[j] = g;
+    if (!a.apply) return;
+    g *= a.inv_n;
+    if (!isfinite(g)) {  // non-finite gradient entries are zeroed and counted
+        g = 0.0f;
+        atomicAdd(a.bad_grads, 1ull);
+    }
+    float m = a.m[j], v = a.v[j], w = a.w[j], e = a.ema[j];
+    m = a.b1 * m + (1.0f - a.b1) * g;
+    v = a.b2 * v + (1.0f - a.b2) * g * g;
+    w = w - a.lr * (m * a.inv_bc1) / (sqrtf(v * a.inv_bc2) + a.eps);
+    e = a.ema_c1 * w + a.ema_c2 * e;
+    a.m[j] = m;
+    a.v[j] = v;
+    a.w[j] = w;
+    a.ema[j] = e;
+    int i = 0;
+    while (i < 5 && j >= D::pad_off(i + 1)) ++i;
+    const int rel = j - D::pad_off(i), row = rel / D::cols(i), col = rel % D::cols(i);
+    const uint32_t off = D::img_byte(i, row, col);
+    *reinterpret_cast<__half*>(a.wimg + off) = __float2half_rn(w);
+    *reinterpret_cast<__half*>(a.eimg + off) = __float2half_rn(e);
+}
+
+}  // namespace nrc

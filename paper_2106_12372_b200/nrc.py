@@ -224,7 +224,7 @@ class RadianceCache:
         n = records.shape[0]
         self._f32(targets, (n, 3), "targets")
         if grad is None:
-            grad = torch.empty(NPARAM, dtype=torch.float32, device=self.device)
+            grad = torch.empty(self.nparam, dtype=torch.float32, device=self.device)
         if loss_sum is None:
             loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
         self._check(self.L.nrc_train_backward(self.h, _ptr(records), _ptr(targets), n, _ptr(grad), _ptr(loss_sum),
@@ -233,7 +233,7 @@ class RadianceCache:
 
     def train_apply(self, grad_sum: torch.Tensor, n_global: int, stream=None):
         """Adam + EMA with g = grad_sum / n_global (after an all-reduce)."""
-        self._f32(grad_sum, (NPARAM,), "grad_sum")
+        self._f32(grad_sum, (self.nparam,), "grad_sum")
         self._check(self.L.nrc_train_apply(self.h, _ptr(grad_sum), int(n_global), _stream(stream)), "nrc_train_apply")
 
     def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int = 4, l: int = 16384,
@@ -274,7 +274,7 @@ class RadianceCache:
         n = records.shape[0]
         self._f32(targets, (n, 3), "targets")
         if grad is None:
-            grad = torch.empty(NPARAM, dtype=torch.float32, device=self.device)
+            grad = torch.empty(self.nparam, dtype=torch.float32, device=self.device)
         if loss_sum is None:
             loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
         self._check(self.L.nrc_train_frame_backward(self.h, _ptr(records), _ptr(targets), n, int(l),

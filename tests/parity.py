@@ -14,14 +14,22 @@ TOL_GRAD = 3e-2
 TOL_PARAM = 3e-2
 
 
+def offsets_w(hw):
+    """Matrix offsets of the logical layout at hidden width hw (W0 hw x 64,
+    W1..W4 hw x hw, W5 3 x hw)."""
+    sizes = [hw * 64] + [hw * hw] * 4 + [3 * hw]
+    return [int(x) for x in np.concatenate([[0], np.cumsum(sizes)])]
+
+
 def radiance_err(q_gpu, q_ref):
     q_gpu = np.asarray(q_gpu, np.float64); q_ref = np.asarray(q_ref, np.float64)
     return [float(np.max(np.abs(q_gpu[:, c] - q_ref[:, c])) / max(np.max(np.abs(q_ref[:, c])), 1e-30))
             for c in range(3)]
 
 
-def per_matrix_err(a, b):
+def per_matrix_err(a, b, off=OFF):
     a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    OFF = off
     out = []
     for i in range(6):
         x, y = a[OFF[i]:OFF[i + 1]], b[OFF[i]:OFF[i + 1]]
@@ -29,11 +37,12 @@ def per_matrix_err(a, b):
     return out
 
 
-def post_adam_err(w_gpu, w_ref, g_gpu, g_ref):
+def post_adam_err(w_gpu, w_ref, g_gpu, g_ref, off=OFF):
     """Per-matrix post-Adam error over sign-agreeing entries, plus the sign-flip
     statistics (fraction, and worst |G_ref| / max|G_ref| among the flips)."""
     w_gpu = np.asarray(w_gpu, np.float64); w_ref = np.asarray(w_ref, np.float64)
     g_gpu = np.asarray(g_gpu, np.float64); g_ref = np.asarray(g_ref, np.float64)
+    OFF = off
     errs, flips, worst = [], 0, 0.0
     for i in range(6):
         s = slice(OFF[i], OFF[i + 1])

@@ -1,6 +1,6 @@
 """Width ablation (BASELINE.json configs[3]): the query at
 hidden width 32 and 128 (input 64, depth 5) against the width-general fp64
-oracle (oracle.query_w), plus init parity and the query-only scope."""
+oracle (oracle.query_w), plus init parity (training at these widths: tests/test_gpu_width_train.py)."""
 import numpy as np
 import pytest
 import torch
@@ -56,13 +56,3 @@ def test_width_query_1080p_sampled(nrc, orc, hw):
     ref = orc.query_w(hw, c.get_params("ema").astype(np.float64), recs[idx])
     assert max(radiance_err(q[idx], ref)) <= TOL_RADIANCE
     assert np.all(np.isfinite(q))
-
-
-@pytest.mark.parametrize("hw", [32, 128])
-def test_width_training_is_query_only(nrc, hw):
-    c = nrc.RadianceCache(nrc.Config(hidden_width=hw))
-    recs, tg = nrc_inputs.train_frame(0, n=1024)
-    with pytest.raises(nrc.NRCError, match="UNSUPPORTED"):
-        c.train_step(dev(recs), dev(tg))
-    with pytest.raises(nrc.NRCError, match="UNSUPPORTED"):
-        c.train_frame(dev(recs), dev(tg), 4, 256, 1)
