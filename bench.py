@@ -136,7 +136,9 @@ def oracle_frame_estimate(q_sample: int, t_sample: int, reps: int = 1):
 def frame_config(world: int, train_mode: str = "dp") -> dict:
     return {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
             "parallelism": f"{train_mode}{world}" if world > 1 else "single",
-            "l2": "flushed (256 MB write) between timed steps"}
+            "l2": "flushed (256 MB write) between timed steps",
+            "train_kernel": ("fused cooperative (NRC_TRAIN_FUSED=1)" if os.environ.get("NRC_TRAIN_FUSED", "0") != "0"
+                             else "per step: partials + reduce/Adam/EMA, PDL-chained")}
 
 
 def ncu_traffic(kernel: str):

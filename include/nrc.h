@@ -93,10 +93,10 @@ enum {
 typedef struct nrc_config {
     uint32_t abi_version;      /* must equal NRC_ABI_VERSION                          */
     uint32_t hidden_width;     /* 64 ("five hidden layers have 64 neurons");
-                                * 32 or 128 for the width ablation (BASELINE configs[3]):
-                                * query and parameter calls only, training calls return
-                                * NRC_ERR_UNSUPPORTED.  nrc_param_count() gives
-                                * 64 W + 4 W^2 + 3 W.                                   */
+                                * 32 or 128 for the width ablation (BASELINE configs[3]),
+                                * query and training alike.  nrc_param_count() gives
+                                * 64 W + 4 W^2 + 3 W (logical layout: W0 W x 64,
+                                * W1..W4 W x W, W5 3 x W, row-major [out][in]).        */
     uint32_t n_hidden_layers;  /* 5; fixed in ABI v1                         */
     uint32_t max_batch;        /* largest n accepted by query/train calls             */
     float aabb_min[3];         /* position normalisation domain (R3)           */
@@ -152,18 +152,20 @@ nrc_status nrc_query_accumulate(nrc_handle* h, const nrc_record* d_rec, uint64_t
 /* One optimisation step on a batch: forward, relative
  * L2 loss (Eq. 5) of the factored prediction, backward, Adam on the batch-
  * mean gradient, EMA update.  d_rec: n records; d_tgt: 3n fp32 targets;
- * d_loss (optional, 1 fp32): the batch-mean loss.  n <= max_batch.  One
- * cooperative kernel launch (the fused train kernel with its in-kernel
- * reduction + Adam + EMA); it occupies up to min(#SMs, ceil(n/128)) SMs and
- * must not share the device with a concurrently running kernel that holds
- * them (the launch fails with NRC_ERR_CUDA if co-residency is impossible). */
+ * d_loss (optional, 1 fp32): the batch-mean loss.  n <= max_batch.  Two
+ * kernel launches: the partials kernel (min(#SMs, ceil(n/128)) CTAs) and the
+ * reduce + Adam + EMA kernel, chained with programmatic dependent launch.
+ * With the environment variable NRC_TRAIN_FUSED=1 at nrc_init (width 64
+ * only) one cooperative launch of the fused kernel instead; that launch must
+ * not share the device with a concurrently running kernel holding its SMs
+ * (it fails with NRC_ERR_CUDA if co-residency is impossible). */
 nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n, float* d_loss,
                           void* stream);
 
 /* Multi-GPU split of nrc_train_step.  nrc_train_backward writes the UN-
  * normalised gradient sum over the n_local records into d_grad
- * (nrc_param_count() fp32, logical layout: W0..W4 64x64 then W5 3x64, row-
- * major [out][in]) and, if d_loss_sum != NULL, the loss sum (1 fp32).  The
+ * (nrc_param_count() fp32, logical layout: W0 Wx64, W1..W4 WxW, W5 3xW,
+ * row-major [out][in]) and, if d_loss_sum != NULL, the loss sum (1 fp32).  The
  * caller all-reduces (SUM) d_grad across ranks, then nrc_train_apply runs
  * Adam + EMA with g = d_grad_sum / n_global.  Deterministic: equal inputs
  * give bitwise-equal replicas on every rank. */
@@ -177,7 +179,8 @@ nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_gl
  * perm(j*l + k), k < l, gathered inside the kernel (nothing materialised).
  * If s*l > n_total, l shrinks to n_total / s.  d_losses: s fp32
  * (optional).  Equivalent (bitwise) to s nrc_train_step calls on the
- * gathered batches; runs as one cooperative launch per 8 steps. */
+ * gathered batches; two launches per step (one cooperative launch per 8
+ * steps with NRC_TRAIN_FUSED=1). */
 nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s,
                            uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream);
 

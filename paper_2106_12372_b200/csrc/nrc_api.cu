@@ -164,7 +164,7 @@ struct nrc_handle {
     unsigned long long gbar = 0;  // arrivals so far on the train kernel's grid-barrier counter
     unsigned long long gbarA = 0; // arrivals so far on its phase-A (W3..W5 partials written) counter
     bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
-    bool train_generic = false;   // width 64 through the width-generic kernels (NRC_TRAIN_GENERIC=1: cross-checks)
+    bool train_fused = false;     // width 64 through the fused cooperative kernel (NRC_TRAIN_FUSED=1, comparison)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
     int train_ctas = 0;           // cap on the train grid (0: one CTA per tile up to all SMs)
@@ -413,7 +413,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     }
     h->query_cfg = 0;
     if (const char* e = std::getenv("NRC_COOP")) h->coop = std::atoi(e) != 0;
-    if (const char* e = std::getenv("NRC_TRAIN_GENERIC")) h->train_generic = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NRC_TRAIN_FUSED")) h->train_fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("NRC_QUERY_CTAS")) h->query_ctas = std::atoi(e);
     if (const char* e = std::getenv("NRC_TRAIN_CTAS")) h->train_ctas = std::atoi(e);
     if (const char* e = std::getenv("NRC_QUERY_CFG")) h->query_cfg = std::atoi(e);
@@ -473,13 +473,15 @@ nrc_status nrc_destroy(nrc_handle* h) {
     return NRC_OK;
 }
 
-// hidden width 64 trains through the fused persistent kernel; 32 and 128 (the
-// C4 width ablation) through the width-generic partials + Adam kernels
+// Training runs as one partials kernel + one reduce/Adam/EMA kernel per step
+// (nrc_train_w.cuh, PDL-chained) at every width: measured faster than the
+// fused cooperative kernel at width 64 (68.6 vs 74.8 us per 4-step frame,
+// DESIGN.md 5.2), which stays selectable with NRC_TRAIN_FUSED=1.
 static nrc_status check_train_width(nrc_handle* h) {
     if (width_supported(uint32_t(h->wi.W))) return NRC_OK;
     return fail(h, NRC_ERR_UNSUPPORTED, "unsupported hidden width for training");
 }
-static bool train_generic(const nrc_handle* h) { return h->wi.W != 64 || h->train_generic; }
+static bool train_generic(const nrc_handle* h) { return h->wi.W != 64 || !h->train_fused; }
 static nrc_status check_handle(nrc_handle* h) {
     if (!h || !h->state) return NRC_ERR_STATE;
     int dev = -1;
@@ -618,11 +620,11 @@ static nrc_status launch_train_w(nrc_handle* h, const nrc_record* d_rec, const f
     const int grid = train_grid(h, n);
     *nparts = grid;
     if (h->wi.W == 32)
-        nrc_train_w_kernel<32><<<grid, 128, TrainW<32>::kSmemBytes, st>>>(ta);
+        NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::kSmemBytes, st, ta));
     else if (h->wi.W == 128)
-        nrc_train_w_kernel<128><<<grid, 128, TrainW<128>::kSmemBytes, st>>>(ta);
+        NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<128>, dim3(grid), dim3(128), TrainW<128>::kSmemBytes, st, ta));
     else
-        nrc_train_w_kernel<64><<<grid, 128, TrainW<64>::kSmemBytes, st>>>(ta);
+        NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta));
     NRC_LAUNCHED(h, "nrc_train_w_kernel");
     return NRC_OK;
 }
@@ -649,13 +651,13 @@ static AdamWArgs adam_w_args(nrc_handle* h) {
     return aa;
 }
 static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t st) {
-    const int blocks = (h->wi.padded + 255) / 256;
+    const dim3 grid(unsigned(h->wi.padded / 32)), block(256);
     if (h->wi.W == 32)
-        nrc_adam_w_kernel<32><<<blocks, 256, 0, st>>>(aa);
+        NRC_CUDA(h, launch_pdl(nrc_adam_w_kernel<32>, grid, block, 0, st, aa));
     else if (h->wi.W == 128)
-        nrc_adam_w_kernel<128><<<blocks, 256, 0, st>>>(aa);
+        NRC_CUDA(h, launch_pdl(nrc_adam_w_kernel<128>, grid, block, 0, st, aa));
     else
-        nrc_adam_w_kernel<64><<<blocks, 256, 0, st>>>(aa);
+        NRC_CUDA(h, launch_pdl(nrc_adam_w_kernel<64>, grid, block, 0, st, aa));
     NRC_LAUNCHED(h, "nrc_adam_w_kernel");
     return NRC_OK;
 }

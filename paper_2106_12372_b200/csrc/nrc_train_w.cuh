@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     float loss_sum = 0.0f;
     uint32_t bad = 0;
     const uint32_t ntiles = (a.n + kTile - 1) / kTile;
-    if (tid == 0 && blockIdx.x < ntiles) fetch(0);  // W0 (streamed) or the whole image
+    pdl_trigger();  // the optimiser kernel may launch (its griddepcontrol.wait covers this grid)
     bool first = true;
 #pragma unroll 1
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -261,6 +261,12 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
             uint32_t h[32];
             encode_record<false>(rec, a.ep, h);
             store_row_swz(slot(0), r, h);
+        }
+        if (first) {
+            // the weights and this CTA's partial belong to the previous kernel
+            // (launched with PDL) until it has completed
+            pdl_wait();
+            if (tid == 0) fetch(0);  // W0 (streamed) or the whole image
         }
         sync_rows();
         // ---------------- forward: h_{L+1} = relu(W_L h_L), y = W5 h5
@@ -385,33 +391,48 @@ struct AdamWArgs {
     float* loss_out;
 };
 
+// grid = kPadded / 32 blocks of 256 threads: block b owns parameters
+// 32 b + lane; warp w sums partials p = w, w + 8, ... (all its loads in
+// flight), warp 0 adds the 8 warp sums in warp order (deterministic) and
+// applies the update.
 template <int W>
 __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
     using D = NetDims<W>;
-    const int j = int(blockIdx.x * blockDim.x + threadIdx.x);
-    if (blockIdx.x == 0 && threadIdx.x < 32 && a.loss_out != nullptr) {
-        float s = 0.0f;
-        for (int p = int(threadIdx.x); p < a.nloss; p += 32) s += a.loss_part[p];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (threadIdx.x == 0) *a.loss_out = s * a.loss_scale;
-    }
-    if (j >= D::kPadded) return;
+    static_assert(D::kPadded % 32 == 0, "32 parameters per block");
+    __shared__ float sred[8][32];
+    pdl_wait();  // launched as a programmatic dependent of the partials kernel
+    pdl_trigger();
+    const int lane = int(threadIdx.x & 31), wp = int(threadIdx.x >> 5);
+    const int j = int(blockIdx.x) * 32 + lane;
     float g = 0.0f;
     if (a.partials != nullptr) {
         const float* src = a.partials + j;
-        int p = 0;
+        float s = 0.0f;
 #pragma unroll 1
-        for (; p + 8 <= a.np; p += 8) {
-            float x[8];
+        for (int p0 = wp; p0 < a.np; p0 += 8 * 16) {
+            float x[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + size_t(p + u) * D::kPadded);
+            for (int u = 0; u < 16; ++u)
+                x[u] = (p0 + 8 * u < a.np) ? __ldcg(src + size_t(p0 + 8 * u) * D::kPadded) : 0.0f;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) g += x[u];
+            for (int u = 0; u < 16; ++u) s += x[u];
         }
-        for (; p < a.np; ++p) g += __ldcg(src + size_t(p) * D::kPadded);
+        sred[wp][lane] = s;
+        __syncthreads();
+        if (wp == 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) g += sred[k][lane];
+        }
     } else {
         g = j < D::kLogical ? a.grad_logical[j] : 0.0f;
+    }
+    if (wp != 0) return;
+    if (blockIdx.x == 0 && a.loss_out != nullptr) {
+        float s = 0.0f;
+        for (int p = lane; p < a.nloss; p += 32) s += a.loss_part[p];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) *a.loss_out = s * a.loss_scale;
     }
     if (a.grad_out != nullptr && j < D::kLogical) a.grad_out[j] = g;
     if (!a.apply) return;

@@ -1,8 +1,10 @@
-"""Width ablation (BASELINE.json configs[3]): 1080p query time and
-tensor-roofline fraction at hidden width 32 / 64 / 128 (input 64, depth 5),
-CUDA events, L2 flushed between reps.  Training is built for W = 64 only, so
-the frame column adds the W = 64 training time to every width.
-Writes one JSON line per width."""
+"""Width ablation (BASELINE.json configs[3]): the 1080p frame --
+query of 2,073,600 records + a 4 x 16,384-record training frame -- at hidden
+width 32 / 64 / 128 (input 64, depth 5): CUDA events, L2 flushed between reps,
+tensor-roofline fractions of the query and of the training.  Training runs
+through the per-step partials + Adam kernels at every width; W = 64 is also
+timed through the fused cooperative kernel (NRC_TRAIN_FUSED=1).
+Writes one JSON line per configuration."""
 import json
 import os
 import sys
@@ -26,7 +28,7 @@ out = torch.empty((n, 3), device="cuda")
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
 tr, tg = nrc_inputs.train_frame(0, noise=0.3)
 tr, tg = torch.from_numpy(tr).cuda(), torch.from_numpy(tg).cuda()
-c64 = nrc.RadianceCache()
+n_train = tr.shape[0]
 
 
 def timeit(fn, reps=50):
@@ -41,12 +43,23 @@ def timeit(fn, reps=50):
     return float(np.median(ts))
 
 
-t_train = timeit(lambda: c64.train_frame(tr, tg, 4, 16384, 1))
-for hw in (32, 64, 128):
+for hw, fused in ((32, False), (64, False), (64, True), (128, False)):
+    if fused:
+        os.environ["NRC_TRAIN_FUSED"] = "1"
     c = nrc.RadianceCache(nrc.Config(hidden_width=hw))
-    ms = timeit(lambda: c.query(recs, out))
-    flop = 2 * (64 * hw + 4 * hw * hw + 3 * hw)
-    tf = flop * n / (ms * 1e-3) / 1e12
-    print(json.dumps({"config": "C4 width ablation, 1080p query", "hidden_width": hw, "query_ms": ms,
-                      "queries_per_s": n / (ms * 1e-3), "flop_per_query": flop, "achieved_tflops": tf,
-                      "tensor_frac": tf / PEAK, "train_frame_ms_w64": t_train, "frame_ms": ms + t_train}))
+    os.environ.pop("NRC_TRAIN_FUSED", None)
+    q_ms = timeit(lambda: c.query(recs, out))
+    t_ms = timeit(lambda: c.train_frame(tr, tg, 4, 16384, 1), reps=30)
+    fq = 2 * (64 * hw + 4 * hw * hw + 3 * hw)          # query FLOP per record
+    ft = 2 * fq + 2 * (4 * hw * hw + 3 * hw)            # + dgrad (no layer 0) + wgrad per record
+    q_tf = fq * n / (q_ms * 1e-3) / 1e12
+    t_tf = ft * n_train / (t_ms * 1e-3) / 1e12
+    print(json.dumps({"config": "C4 width ablation, 1080p frame (query + 4x16384 train)", "hidden_width": hw,
+                      "train_kernel": "fused cooperative" if fused else "partials + adam (PDL)",
+                      "query_ms": q_ms, "train_ms": t_ms, "frame_ms": q_ms + t_ms,
+                      "queries_per_s": n / (q_ms * 1e-3), "records_per_s": n_train / (t_ms * 1e-3),
+                      "flop_per_query": fq, "flop_per_train_record": ft,
+                      "query_tflops": q_tf, "query_tensor_frac": q_tf / PEAK,
+                      "train_tflops": t_tf, "train_tensor_frac": t_tf / PEAK,
+                      "frame_tensor_frac": (fq * n + ft * n_train) / ((q_ms + t_ms) * 1e-3) / 1e12 / PEAK,
+                      "peak_tflops": PEAK}), flush=True)

@@ -45,8 +45,10 @@ def main(tag, d):
         lines.append(f"(not ours) {k[:49]:49s} {len(v):8d} {sum(v) / len(v):10.2f}")
     open(os.path.join(prof, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
-    traffic = {}
-    for name, rep in [("nrc_query_ts_kernel", "prof_query.ncu-rep"), ("nrc_train_kernel", "prof_train.ncu-rep")]:
+    tp = os.path.join(prof, f"{tag}_traffic.json")
+    traffic = json.load(open(tp)) if os.path.exists(tp) else {}  # keep kernels not re-captured this time
+    for name, rep in [("nrc_query_ts_kernel", "prof_query.ncu-rep"), ("nrc_train_kernel", "prof_train.ncu-rep"),
+                      ("nrc_train_w_kernel<64>", "prof_train_w.ncu-rep"), ("nrc_adam_w_kernel<64>", "prof_adam_w.ncu-rep")]:
         p = os.path.join(d, rep)
         if os.path.exists(p):
             m = raw(p, ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"])

@@ -23,6 +23,15 @@ def nrc():
     return p
 
 
+@pytest.fixture(params=["default", "fused"])
+def train_kernel(request, monkeypatch):
+    """Training through the default per-step kernels and through the fused
+    cooperative kernel (NRC_TRAIN_FUSED=1, read when a cache is created)."""
+    if request.param == "fused":
+        monkeypatch.setenv("NRC_TRAIN_FUSED", "1")
+    return request.param
+
+
 def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
@@ -182,7 +191,7 @@ def test_gradient_parity_16384(nrc, orc):
     assert l_gpu == pytest.approx(l_ref, rel=1e-2)
 
 
-def test_train_step_parity_c1(nrc, orc):
+def test_train_step_parity_c1(nrc, orc, train_kernel):
     """C1: 256 records, one step: loss, gradient, post-Adam W and W-bar."""
     recs, tg = nrc_inputs.train_frame(0, n=256, noise=0.3)
     cache = nrc.RadianceCache()
@@ -225,7 +234,7 @@ def test_adam_kernel_alone_matches_oracle(nrc, orc):
     assert np.max(np.abs(cache.get_params("ema") - wbar)) <= 1e-6 * np.max(np.abs(wbar)) + 1e-7
 
 
-def test_train_frame_equals_gathered_steps(nrc, orc):
+def test_train_frame_equals_gathered_steps(nrc, orc, train_kernel):
     """nrc_train_frame == s train steps on the LCG-gathered batches (bitwise)."""
     n, s, l, seed = 8192, 4, 2048, 11
     recs, tg = nrc_inputs.train_frame(5, n=n)
@@ -250,7 +259,7 @@ def test_train_frame_shrinks_batches(nrc):
     assert c.stats()["step"] == 4
 
 
-def test_determinism_bitwise(nrc):
+def test_determinism_bitwise(nrc, train_kernel):
     recs, tg = nrc_inputs.train_frame(7, n=16384, noise=0.3)
     q = nrc_inputs.records(5000, seed=17)
     outs = []
@@ -321,7 +330,7 @@ def test_frame_host_equals_device_calls(nrc):
     np.testing.assert_array_equal(a.get_params("ema"), b.get_params("ema"))
 
 
-def test_multi_tile_ctas_gradient_and_fused_step(nrc, orc):
+def test_multi_tile_ctas_gradient_and_fused_step(nrc, orc, train_kernel):
     """Batches larger than one tile per SM (40,000 rows = 313 tiles on <= 148
     CTAs): the partials-only path (train_backward) and the fused step
     (train_step: several tiles per CTA, phase A / phase B optimiser) against
@@ -343,7 +352,7 @@ def test_multi_tile_ctas_gradient_and_fused_step(nrc, orc):
     assert flip_frac <= 0.01 and worst <= 3e-2, (flip_frac, worst)
 
 
-def test_train_frame_more_than_eight_steps(nrc):
+def test_train_frame_more_than_eight_steps(nrc, train_kernel):
     """s = 11 steps run as two fused launches (8 + 3): bitwise equal to 11
     single steps on the gathered batches, losses included."""
     n, s, l, seed = 11 * 1024, 11, 1024, 5

@@ -1,7 +1,7 @@
 """Width ablation, training (BASELINE.json configs[3] "32/64/128-neuron hidden
 layers at 1080p query+train"): the width-generic training kernels
-(nrc_train_w.cuh) at hidden width 32 and 128 -- and at 64 through the same
-kernels (NRC_TRAIN_GENERIC=1) -- against the width-general fp64 oracle
+(nrc_train_w.cuh) at hidden width 32, 128 and 64 (the default training path
+at every width) against the width-general fp64 oracle
 (oracle.grad_batch_w / OracleCache(hidden_width=hw)), with the parity
 definitions of SURVEY 8(c) (tests/parity.py)."""
 import numpy as np
@@ -27,11 +27,8 @@ def dev(x):
 
 
 def make(nrc, hw, monkeypatch=None, **kw):
-    if hw == "64g":
-        monkeypatch.setenv("NRC_TRAIN_GENERIC", "1")
-        c = nrc.RadianceCache(nrc.Config(hidden_width=64, **kw))
-        monkeypatch.delenv("NRC_TRAIN_GENERIC")
-        return c, 64
+    if hw == "64g":  # the default training path at width 64
+        return nrc.RadianceCache(nrc.Config(hidden_width=64, **kw)), 64
     return nrc.RadianceCache(nrc.Config(hidden_width=hw, **kw)), hw
 
 
@@ -193,11 +190,13 @@ def test_width_backward_apply_equals_step_and_determinism(nrc, hw):
 
 
 def test_generic64_matches_fused64(nrc, orc, monkeypatch):
-    """Width 64 through the generic kernels vs the fused product kernel: both
-    within the gradient tolerance of each other after a 4-step frame."""
+    """Width 64 through the generic kernels vs the fused cooperative kernel
+    (NRC_TRAIN_FUSED=1): losses and queries agree after a 4-step frame."""
     recs, tg = nrc_inputs.train_frame(3, n=65536, noise=0.3)
     g, _ = make(nrc, "64g", monkeypatch)
+    monkeypatch.setenv("NRC_TRAIN_FUSED", "1")
     f = nrc.RadianceCache()
+    monkeypatch.delenv("NRC_TRAIN_FUSED")
     lg = g.train_frame(dev(recs), dev(tg), 4, 16384, 9).cpu().numpy()
     lf = f.train_frame(dev(recs), dev(tg), 4, 16384, 9).cpu().numpy()
     np.testing.assert_allclose(lg, lf, rtol=1e-2)
