@@ -616,7 +616,8 @@ static int train_grid(const nrc_handle* h, uint32_t n) {
 // Width-generic partials kernel (nrc_train_w.cuh): one step over n rows.
 static nrc_status launch_train_w(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
                                  const Gather& gth, cudaStream_t st, int* nparts) {
-    const TrainArgs ta = train_args(h, d_rec, d_tgt, n, gth);
+    TrainArgs ta = train_args(h, d_rec, d_tgt, n, gth);
+    if (h->dbg) ta.dbg = h->dbg + 4096 * (h->step % 4);  // diagnostics: one 4096-slot block per step
     const int grid = train_grid(h, n);
     *nparts = grid;
     if (h->wi.W == 32)
@@ -648,6 +649,7 @@ static AdamWArgs adam_w_args(nrc_handle* h) {
     aa.ema_c2 = k.ema_c2;
     aa.bad_grads = h->d_counters() + 0;
     aa.loss_part = h->d_loss_part();
+    if (h->dbg) aa.dbg = h->dbg + 4096 * ((h->step + 3) % 4);  // the step's block (step already incremented)
     return aa;
 }
 static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t st) {

@@ -80,10 +80,16 @@ __device__ __forceinline__ void train_gather_row(const TrainArgs& a, uint32_t ro
 // One training step's partials at width W: CTA c processes tiles c, c + grid,
 // ... and writes its un-normalised fp32 gradient sum (padded layout of
 // NetDims<W>) to partials[c] and its loss sum to loss_part[c].
+// diagnostics (nrc_debug_set_trace): global-timer marks of each CTA at dbg[32 cta + k]
+#define NRC_WTRC(k)                                                                     \
+    do {                                                                                \
+        if (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 127) a.dbg[32 * blockIdx.x + (k)] = global_ns(); \
+    } while (0)
 template <int W>
 __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     using D = NetDims<W>;
     using T = TrainW<W>;
+    NRC_WTRC(0);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     const uint32_t tid = threadIdx.x, r = tid, warp = tid >> 5, lane = tid & 31;
@@ -265,7 +271,9 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         if (first) {
             // the weights and this CTA's partial belong to the previous kernel
             // (launched with PDL) until it has completed
+            NRC_WTRC(1);
             pdl_wait();
+            NRC_WTRC(2);
             if (tid == 0) fetch(0);  // W0 (streamed) or the whole image
         }
         sync_rows();
@@ -277,6 +285,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
                 issue_fwd(L);
             }
             mma_wait();
+            NRC_WTRC(8 + L);
             if (T::kStream && L < 5 && tid == 0) fetch(L + 1);  // the buffer is free
             if (L == 5) break;
 #pragma unroll
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
             st_shared_v4(sG6_a + swz(r, 0), pack_h2(gy[0], gy[1]), pack_h2(gy[2], 0.0f), 0u, 0u);
         }
         sync_rows();
+        NRC_WTRC(3);
         // ---------------- backward: round j = dgrad_j + wgrad_j, then
         // G_{j+1} drains while they run; g_j overwrites h_j after both complete
 #pragma unroll 1
@@ -328,7 +338,9 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
                 issue_bwd(j);
             }
             if (j < 5) flush_g(j + 1, first);
+            NRC_WTRC(14 + 2 * (5 - j));
             mma_wait();
+            NRC_WTRC(15 + 2 * (5 - j));
             if (T::kStream && tid == 0) {
                 if (j > 1)
                     fetch(j - 1);
@@ -336,8 +348,11 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
                     fetch(0);  // the next tile's W0
             }
             mask_epilogue(j);
+            if (j >= 2) NRC_WTRC(24 + (5 - j));
             sync_rows();
+            if (j >= 2) NRC_WTRC(28 + (5 - j));
         }
+        NRC_WTRC(4);
         if (warp == 0) issue_bwd(0);  // G_0 += g_1^T h_0 (no gradient w.r.t. the encoding)
         flush_g(1, first);
         mma_wait();
@@ -345,6 +360,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         tc_fence_before();
         __syncthreads();
         tc_fence_after();
+        NRC_WTRC(5);
         first = false;
     }
     // ---------------- this CTA's loss sum (fixed order over the 4 row warps)
@@ -365,8 +381,10 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         const uint32_t nb = b[0] + b[1] + b[2] + b[3];
         if (nb) atomicAdd(a.bad_targets, (unsigned long long)nb);
     }
+    NRC_WTRC(6);
     if (warp == 0) tmem_dealloc(tmem_base, T::kTmemCols);
 }
+#undef NRC_WTRC
 
 // Reduce + Adam + EMA at width W: thread j owns padded parameter j.
 //   partials != nullptr: g = sum over p < np of partials[p][j] (ascending p);
@@ -389,6 +407,7 @@ struct AdamWArgs {
     int nloss;
     float loss_scale;
     float* loss_out;
+    long long* dbg;          // diagnostics: global-timer marks of blocks 0 and last at dbg[4088..4091]
 };
 
 // grid = kPadded / 32 blocks of 256 threads: block b owns parameters
@@ -402,9 +421,17 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
     __shared__ float sred[8][32];
     pdl_wait();  // launched as a programmatic dependent of the partials kernel
     pdl_trigger();
+    const bool trc = a.dbg != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x + 1 == gridDim.x);
+    if (trc) a.dbg[4088 + 2 * (blockIdx.x != 0)] = global_ns();
     const int lane = int(threadIdx.x & 31), wp = int(threadIdx.x >> 5);
     const int j = int(blockIdx.x) * 32 + lane;
     float g = 0.0f;
+    // warp 0's optimiser state, loaded under the partial loads (one L2 round trip)
+    float m = 0.0f, v = 0.0f, w = 0.0f, e = 0.0f;
+    if (wp == 0 && a.apply) {
+        m = ld_global_f32(a.m + j), v = ld_global_f32(a.v + j);
+        w = ld_global_f32(a.w + j), e = ld_global_f32(a.ema + j);
+    }
     if (a.partials != nullptr) {
         const float* src = a.partials + j;
         float s = 0.0f;
@@ -441,7 +468,6 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
         g = 0.0f;
         atomicAdd(a.bad_grads, 1ull);
     }
-    float m = a.m[j], v = a.v[j], w = a.w[j], e = a.ema[j];
     m = a.b1 * m + (1.0f - a.b1) * g;
     v = a.b2 * v + (1.0f - a.b2) * g * g;
     w = w - a.lr * (m * a.inv_bc1) / (sqrtf(v * a.inv_bc2) + a.eps);
@@ -456,6 +482,7 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
     const uint32_t off = D::img_byte(i, row, col);
     *reinterpret_cast<__half*>(a.wimg + off) = __float2half_rn(w);
     *reinterpret_cast<__half*>(a.eimg + off) = __float2half_rn(e);
+    if (trc) a.dbg[4089 + 2 * (blockIdx.x != 0)] = global_ns();
 }
 
 }  // namespace nrc

@@ -1,0 +1,60 @@
+"""Global-timer phase trace of the default training path (nrc_train_w_kernel
++ nrc_adam_w_kernel, PDL-chained) over one 4-step frame, via
+nrc_debug_set_trace: per step, per-CTA marks 0 start, 1 encoded (before
+griddepcontrol.wait), 2 after the wait, 3 forward + loss done, 4 backward
+rounds 5..1 done, 5 tile done (G0 drained), 6 loss written, 8+L forward layer
+L's MMA done, 14+2(5-j) / 15+2(5-j) backward round j before / after its MMA
+wait; Adam blocks 0 and last: start (after wait) / end.  argv[1]: hidden
+width (64)."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import nrc_inputs
+import paper_2106_12372_b200 as nrc
+
+hw = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+tr, tg = nrc_inputs.train_frame(0, noise=0.3)
+tr, tg = torch.from_numpy(tr).cuda(), torch.from_numpy(tg).cuda()
+c = nrc.RadianceCache(nrc.Config(hidden_width=hw))
+for _ in range(5):
+    c.train_frame(tr, tg, 4, 16384, 1)
+buf = torch.zeros(4 * 4096, dtype=torch.int64, device="cuda")
+c.L.nrc_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+c.L.nrc_debug_set_trace(c.h, ctypes.c_void_p(buf.data_ptr()))
+torch.cuda.synchronize()
+c.train_frame(tr, tg, 4, 16384, 1)
+torch.cuda.synchronize()
+d = buf.cpu().numpy().reshape(4, 4096)
+step0 = c.stats()["step"] - 4
+t0 = None
+names = {0: "start", 1: "encoded", 2: "after wait", 8: "fwd L0 mma", 9: "fwd L1 mma", 10: "fwd L2 mma",
+         11: "fwd L3 mma", 12: "fwd L4 mma", 13: "fwd L5 mma", 3: "fwd+loss"}
+for j in range(5, 0, -1):
+    names[14 + 2 * (5 - j)] = f"bwd {j} issued"
+    names[15 + 2 * (5 - j)] = f"bwd {j} mma"
+for j in range(5, 1, -1):
+    names[24 + (5 - j)] = f"bwd {j} mask done"
+    names[28 + (5 - j)] = f"bwd {j} synced"
+names.update({4: "bwd 5..1", 5: "tile done", 6: "loss written"})
+order = [0, 1, 2, 8, 9, 10, 11, 12, 13, 3]
+for j in range(5, 0, -1):
+    order += [14 + 2 * (5 - j), 15 + 2 * (5 - j)] + ([24 + (5 - j), 28 + (5 - j)] if j >= 2 else [])
+order += [4, 5, 6]
+names = {k: names[k] for k in order}
+for k in range(4):
+    blk = d[(step0 + k) % 4]
+    g = blk[:32 * 127].reshape(127, 32)
+    g = g[g[:, 0] != 0]
+    if t0 is None:
+        t0 = g[:, 0].min()
+    print(f"--- step {k} ({len(g)} CTAs), ns from the frame's first CTA start")
+    for i, nm in names.items():
+        col = g[:, i] - t0
+        print(f"  {nm:14s} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}")
+    print(f"  adam blk0 {blk[4088] - t0:7d} -> {blk[4089] - t0:7d}   last blk {blk[4090] - t0:7d} -> {blk[4091] - t0:7d}")
+c.L.nrc_debug_set_trace(c.h, None)
