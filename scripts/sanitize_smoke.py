@@ -1,6 +1,8 @@
 """Small end-to-end workload for compute-sanitizer runs: query, train_step,
 train_frame, train_backward/apply, encode, assemble_targets, query_accumulate
-on small sizes (diagnostics)."""
+on small sizes at hidden width 64 (default training path), training at width
+32 and 128, and (NRC_SANITIZE_FUSED=1) the fused cooperative train kernel
+(diagnostics).  NRC_SANITIZE_MIN=1: query + one train step only (memcheck)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -10,9 +12,12 @@ c = nrc.RadianceCache()
 recs = nrc_inputs.records(1000, seed=1)
 q = c.query(dev(recs))
 tr, tg = nrc_inputs.train_frame(0, n=4096)
-if os.environ.get("NRC_SANITIZE_FUSED", "1") == "1":  # the grid-barrier kernel (skipped under memcheck)
-    c.train_step(dev(tr[:1000]), dev(tg[:1000]))
-    c.train_frame(dev(tr), dev(tg), 4, 1024, 3)
+c.train_step(dev(tr[:300]), dev(tg[:300]))
+if os.environ.get("NRC_SANITIZE_MIN", "0") == "1":
+    torch.cuda.synchronize()
+    print("sanitize workload (min) ok", float(q.sum()))
+    sys.exit(0)
+c.train_frame(dev(tr), dev(tg), 4, 1024, 3)
 g, l = c.train_backward(dev(tr[:300]), dev(tg[:300]))
 c.train_apply(g, 300)
 e = c.encode(dev(recs))
@@ -21,5 +26,14 @@ i32 = lambda x: torch.from_numpy(x.astype(np.int32)).cuda()
 t = c.self_training_targets(i32(first), i32(length), i32(flags), dev(vert), dev(trec))
 img = torch.zeros((1000, 3), device="cuda")
 c.query_accumulate(dev(recs), i32(np.arange(1000)), dev(np.ones((1000, 3), np.float32)), img)
+for hw in (32, 128):  # width-ablation training (streamed weights at 128)
+    cw = nrc.RadianceCache(nrc.Config(hidden_width=hw))
+    cw.train_frame(dev(tr), dev(tg), 2, 300, 5)
+    cw.query(dev(recs))
+if os.environ.get("NRC_SANITIZE_FUSED", "1") == "1":  # the grid-barrier kernel (not under racecheck)
+    os.environ["NRC_TRAIN_FUSED"] = "1"
+    cf = nrc.RadianceCache()
+    cf.train_step(dev(tr[:1000]), dev(tg[:1000]))
+    cf.train_frame(dev(tr), dev(tg), 4, 1024, 3)
 torch.cuda.synchronize()
 print("sanitize workload ok", float(q.sum()), float(t.sum()), float(img.sum()))
