@@ -14,8 +14,10 @@ frame is split across ranks -- query rows sharded with no communication;
 training either replicated after one all-gather of the frame's records
 (--train-mode replicated, the default) or data-parallel (--train-mode dp:
 each rank takes l/N rows of every batch, one NCCL all-reduce of the gradient
-per step, identical Adam on every rank) -- strong scaling, max-over-ranks
-device time.
+per step, identical Adam on every rank; --train-mode allreduce-peer: the same
+split with the all-reduce fused into the optimiser kernel over peer memory;
+--train-mode peer: the record all-gather fused into the training kernel) --
+strong scaling, max-over-ranks device time.
 
 --impl reference: the fp64 CPU oracle (oracle/, as it stands) on the host
 cores, timed on a bounded sample of the same frame and scaled to the frame.
@@ -264,6 +266,11 @@ def run_nrc(args):
             lo, hi = nrc.shard(N_TRAIN, rank, world)
             dpf.train_frame_peer(d_r[lo:hi], d_t[lo:hi], TRAIN_S, TRAIN_L, 1000 + fi % 2, parts_ready=True)
             launches += dpf.last_launch_count
+        elif args.train_mode == "allreduce-peer":
+            # SURVEY 8(e) mitigation 2 / N3 (ii): each rank's tiles of every batch, the
+            # gradient all-reduce fused into the optimiser over peer memory (no NCCL)
+            dpf.train_frame_allreduce_peer(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
+            launches += dpf.last_launch_count
         elif args.train_mode == "replicated":
             # N3 (i): this rank's screen-region records, one all-gather, replicated training
             lo, hi = nrc.shard(N_TRAIN, rank, world)
@@ -376,12 +383,14 @@ def main():
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
-    ap.add_argument("--train-mode", choices=["dp", "replicated", "peer"], default="replicated",
+    ap.add_argument("--train-mode", choices=["dp", "replicated", "peer", "allreduce-peer"], default="replicated",
                     help="N > 1 training: one all-gather of the frame's records per frame and replicated "
                          "training (replicated, SURVEY N3 (i); default: the training step is latency-bound, so "
                          "fewer rows per GPU do not shorten it while per-step collectives add up), or "
                          "data-parallel with one all-reduce per step (dp, north_star's description), or the "
-                         "all-gather fused into the training kernel over peer memory (peer)")
+                         "all-gather fused into the training kernel over peer memory (peer), or data-parallel "
+                         "with the gradient all-reduce fused into the optimiser over peer memory "
+                         "(allreduce-peer)")
     args = ap.parse_args()
     if args.workload == "4k":
         global N_QUERY, METRIC, CONFIG_NAME

@@ -209,7 +209,32 @@ nrc_status nrc_train_frame_parts(nrc_handle* h, const nrc_record* const* rec_par
                                  uint32_t n_parts, uint32_t n_per_part, uint32_t s, uint32_t l,
                                  uint64_t shuffle_seed, float* d_losses, void* stream);
 
-/* CUDA IPC for nrc_train_frame_parts.  nrc_ipc_export: the 64-byte handle of
+/* Data-parallel frame training with the gradient all-reduce fused into the
+ * optimiser over peer memory (SURVEY 8(e) mitigation 2, 8(f) N3 (ii); no NCCL
+ * call).  `world` <= 8 ranks hold identically initialised caches and the
+ * same (replicated) frame records d_rec / d_tgt (n_total records, shuffled
+ * and split as in nrc_train_frame).  A step's l rows form T = ceil(l / 128)
+ * tiles (T <= 128, i.e. l <= 16,384); rank r computes the fp32 gradient
+ * partials of tiles [r T / world, (r+1) T / world) into its own state arena
+ * (two slot halves by step parity), a one-thread hand-off kernel adds 1 to
+ * every rank's counter (system-scope release; peer memory over NVLink) and
+ * waits until all ranks have published the step, then the optimiser kernel
+ * reduces the T tile partials in tile order straight from their owners'
+ * arenas (peer loads) and applies Adam + EMA.  Every rank ends bitwise equal
+ * to single-GPU nrc_train_frame on the same records (same tiles, same
+ * partials, same summation order).  peer_state: host array of `world` device
+ * pointers to every rank's state arena in rank order (this rank's own
+ * d_state at index rank; peers' mapped with nrc_ipc_import).  All ranks must
+ * make the same sequence of calls; the hand-off gives up after ~20 s
+ * (counted by nrc_dp_timeouts) instead of hanging.  d_losses: s fp32
+ * (optional).  NRC_ERR_UNSUPPORTED with NRC_TRAIN_FUSED=1 or T > 128. */
+nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
+                                   uint32_t s, uint32_t l, uint64_t shuffle_seed, uint32_t rank, uint32_t world,
+                                   void* const* peer_state, float* d_losses, void* stream);
+/* Number of nrc_train_frame_dp_peer hand-offs that timed out (synchronous). */
+nrc_status nrc_dp_timeouts(nrc_handle* h, uint64_t* count);
+
+/* CUDA IPC for nrc_train_frame_parts and nrc_train_frame_dp_peer.  nrc_ipc_export: the 64-byte handle of
  * the device allocation that contains d_ptr and d_ptr's offset in it;
  * nrc_ipc_import (another process): maps it, *d_ptr = mapped base + offset;
  * nrc_ipc_close: unmaps (pass the imported pointer and its offset).  A

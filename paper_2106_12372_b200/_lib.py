@@ -35,8 +35,8 @@ SYMBOLS = [
     "nrc_train_backward", "nrc_train_apply", "nrc_train_frame", "nrc_train_frame_backward", "nrc_lcg_params", "nrc_encode", "nrc_get_params",
     "nrc_set_params", "nrc_get_stats", "nrc_param_count", "nrc_status_string", "nrc_last_error",
     "nrc_frame_scratch_bytes", "nrc_frame_host", "nrc_selftest_umma", "nrc_last_launch_count",
-    "nrc_assemble_targets", "nrc_query_accumulate", "nrc_train_frame_parts", "nrc_ipc_export",
-    "nrc_ipc_import", "nrc_ipc_close",
+    "nrc_assemble_targets", "nrc_query_accumulate", "nrc_train_frame_parts", "nrc_train_frame_dp_peer",
+    "nrc_dp_timeouts", "nrc_ipc_export", "nrc_ipc_import", "nrc_ipc_close",
 ]
 
 
@@ -72,6 +72,9 @@ def load(build_if_missing: bool = True):
     L.nrc_encode.restype = st; L.nrc_encode.argtypes = [vp, vp, u64, vp, vp]
     L.nrc_train_frame_parts.restype = st
     L.nrc_train_frame_parts.argtypes = [vp, vp, vp, u32, u32, u32, u32, u64, vp, vp]
+    L.nrc_train_frame_dp_peer.restype = st
+    L.nrc_train_frame_dp_peer.argtypes = [vp, vp, vp, u32, u32, u32, u64, u32, u32, vp, vp, vp]
+    L.nrc_dp_timeouts.restype = st; L.nrc_dp_timeouts.argtypes = [vp, P(u64)]
     L.nrc_ipc_export.restype = st; L.nrc_ipc_export.argtypes = [vp, vp, P(u64)]
     L.nrc_ipc_import.restype = st; L.nrc_ipc_import.argtypes = [vp, u64, P(vp)]
     L.nrc_ipc_close.restype = st; L.nrc_ipc_close.argtypes = [vp, u64]

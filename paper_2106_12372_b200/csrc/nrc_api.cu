@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -136,7 +137,9 @@ StateLayout layout(int W) {
     // training scratch: per-CTA fp32 gradient partials (padded layout of the width)
     L.partials = take(sizeof(float) * size_t(wi.padded) * kMaxPartials);
     L.loss_part = take(sizeof(float) * kMaxPartials);
-    L.counters = take(sizeof(unsigned long long) * 4);
+    // [0] non-finite gradients, [1] non-finite targets, [2]/[3] fused-kernel
+    // grid barriers, [4] fused peer all-reduce hand-off, [5] its timeouts
+    L.counters = take(sizeof(unsigned long long) * 8);
     L.total = o;
     return L;
 }
@@ -165,6 +168,8 @@ struct nrc_handle {
     unsigned long long gbarA = 0; // arrivals so far on its phase-A (W3..W5 partials written) counter
     bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
     bool train_fused = false;     // width 64 through the fused cooperative kernel (NRC_TRAIN_FUSED=1, comparison)
+    unsigned long long dp_expect = 0;  // hand-off counter value after the last nrc_train_frame_dp_peer step
+    uint64_t dp_seq = 0;               // steps done by nrc_train_frame_dp_peer (partial-slot parity)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
     int train_ctas = 0;           // cap on the train grid (0: one CTA per tile up to all SMs)
@@ -934,6 +939,100 @@ nrc_status nrc_train_frame_parts(nrc_handle* h, const nrc_record* const* rec_par
     // d_rec / d_tgt are unused in peer mode (every row resolves to a part)
     return train_frame_impl(h, rec_parts[0], tgt_parts[0], uint32_t(n_total), s_, l, shuffle_seed, d_losses, g,
                             static_cast<cudaStream_t>(stream));
+}
+
+nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
+                                   uint32_t s_, uint32_t l, uint64_t shuffle_seed, uint32_t rank, uint32_t world,
+                                   void* const* peer_state, float* d_losses, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
+    h->launches = 0;
+    if (world == 0 || world > uint32_t(kMaxParts) || rank >= world || !peer_state)
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_dp_peer: 1..8 ranks, rank < world, peer_state");
+    if (peer_state[rank] != h->state)
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_dp_peer: peer_state[rank] must be this cache's arena");
+    for (uint32_t p = 0; p < world; ++p)
+        if (!peer_state[p] || !aligned(peer_state[p], 256))
+            return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_dp_peer: NULL or misaligned peer arena");
+    if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
+    if (!d_rec || !d_tgt || !aligned(d_rec, 16) || !aligned(d_tgt, 4))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_dp_peer: NULL or misaligned pointer");
+    if (uint64_t(s_) * l > n_total) l = n_total / s_;
+    if (l == 0) return NRC_OK;
+    const uint32_t T = (l + kTile - 1) / kTile;  // tiles per step
+    if (T > uint32_t(kMaxDpTiles) || int(T) > h->num_sms)
+        return fail(h, NRC_ERR_UNSUPPORTED, "nrc_train_frame_dp_peer: at most 128 tiles (16,384 rows) per step");
+    if (train_generic(h) == false)
+        return fail(h, NRC_ERR_UNSUPPORTED, "nrc_train_frame_dp_peer: not with NRC_TRAIN_FUSED=1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto t_lo = [&](uint32_t k) { return k * T / world; };  // rank k owns tiles [t_lo(k), t_lo(k + 1))
+    Gather g{true, 0, 0, 0, n_total, 0};
+    nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
+    DpPeers peers{};
+    for (uint32_t p = 0; p < world; ++p)
+        peers.ctr[p] = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(peer_state[p]) + h->L.counters) + 4;
+    const size_t pad = size_t(h->wi.padded);
+    uint32_t launches = 0;
+    for (uint32_t j = 0; j < s_; ++j) {
+        const uint32_t parity = uint32_t(h->dp_seq & 1u);
+        // 1. this rank's tiles of batch j -> per-tile partials in slot half `parity`
+        const uint32_t r0 = t_lo(rank) * kTile, r1 = std::min(t_lo(rank + 1) * kTile, l);
+        if (r1 > r0) {
+            g.offset = uint64_t(j) * l + r0;
+            TrainArgs ta = train_args(h, d_rec, d_tgt, r1 - r0, g);
+            ta.partials = h->d_partials() + size_t(parity) * kMaxDpTiles * pad;
+            ta.loss_part = h->d_loss_part() + size_t(parity) * kMaxDpTiles;
+            const int grid = int(t_lo(rank + 1) - t_lo(rank));  // one tile per CTA: CTA c -> tile t_lo(rank) + c
+            if (h->wi.W == 32)
+                NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::kSmemBytes, st, ta));
+            else if (h->wi.W == 128)
+                NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<128>, dim3(grid), dim3(128), TrainW<128>::kSmemBytes, st, ta));
+            else
+                NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta));
+            NRC_LAUNCHED(h, "nrc_train_w_kernel");
+            ++launches;
+        }
+        // 2. publish to every rank, wait for every rank (system-scope counters)
+        h->dp_expect += world;
+        nrc_dp_exchange_kernel<<<1, 32, 0, st>>>(peers, int(world), h->d_counters() + 4, h->dp_expect,
+                                                  h->d_counters() + 5);
+        NRC_LAUNCHED(h, "nrc_dp_exchange_kernel");
+        // 3. reduce all T tile partials in tile order from their owners' arenas + Adam + EMA
+        h->step += 1;
+        AdamWArgs aa = adam_w_args(h);
+        for (uint32_t k = 0; k < world; ++k) {
+            const float* part = reinterpret_cast<const float*>(static_cast<uint8_t*>(peer_state[k]) + h->L.partials);
+            const float* loss = reinterpret_cast<const float*>(static_cast<uint8_t*>(peer_state[k]) + h->L.loss_part);
+            for (uint32_t t = t_lo(k); t < t_lo(k + 1); ++t) {
+                const size_t slot = size_t(parity) * kMaxDpTiles + (t - t_lo(k));
+                aa.tile_part[t] = part + slot * pad;
+                aa.tile_loss[t] = loss + slot;
+            }
+        }
+        aa.np = int(T);
+        aa.nloss = int(T);
+        aa.apply = 1;
+        aa.inv_n = float(1.0 / double(l));
+        aa.loss_scale = aa.inv_n;
+        aa.loss_out = d_losses ? d_losses + j : nullptr;
+        if ((s = launch_adam_w(h, aa, st)) != NRC_OK) return s;
+        launches += 2;
+        h->dp_seq += 1;
+    }
+    h->launches = launches;
+    return NRC_OK;
+}
+
+nrc_status nrc_dp_timeouts(nrc_handle* h, uint64_t* count) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if (!count) return NRC_ERR_INVALID_ARGUMENT;
+    unsigned long long c = 0;
+    NRC_CUDA(h, cudaDeviceSynchronize());
+    NRC_CUDA(h, cudaMemcpy(&c, h->d_counters() + 5, sizeof(c), cudaMemcpyDeviceToHost));
+    *count = c;
+    return NRC_OK;
 }
 
 nrc_status nrc_ipc_export(const void* d_ptr, uint8_t* handle, uint64_t* offset) {

@@ -392,6 +392,13 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
 //   grad_out: the reduced sum in the logical layout (nrc_train_backward).
 //   apply: Adam (R11) + EMA (Eq. 2, R12) on g * inv_n, writing
 //   the fp32 state and both fp16 operand images.
+constexpr int kMaxDpTiles = 128;  // tiles per step in the fused peer all-reduce path
+// a peer's (or our own) partial, read at system scope, not cached on this SM
+__device__ __forceinline__ float ld_sys_f32(const float* p) {
+    float v;
+    asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
 struct AdamWArgs {
     const float* partials;
     int np;
@@ -408,6 +415,11 @@ struct AdamWArgs {
     float loss_scale;
     float* loss_out;
     long long* dbg;          // diagnostics: global-timer marks of blocks 0 and last at dbg[4088..4091]
+    // peer mode (nrc_train_frame_dp_peer): partial p of the reduction is the
+    // tile-p partial at tile_part[p] (in its owner's arena, possibly a peer's),
+    // loss partial p at tile_loss[p]; used when tile_part[0] != nullptr
+    const float* tile_part[kMaxDpTiles];
+    const float* tile_loss[kMaxDpTiles];
 };
 
 // grid = kPadded / 32 blocks of 256 threads: block b owns parameters
@@ -432,7 +444,26 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
         m = ld_global_f32(a.m + j), v = ld_global_f32(a.v + j);
         w = ld_global_f32(a.w + j), e = ld_global_f32(a.ema + j);
     }
-    if (a.partials != nullptr) {
+    if (a.tile_part[0] != nullptr) {
+        // fused all-reduce: partial p read from its owner's arena (NVLink loads
+        // for peers), the same order as the local sum below
+        const int pidx = j;
+        float s = 0.0f;
+#pragma unroll 1
+        for (int p0 = wp; p0 < a.np; p0 += 8 * 16) {
+            float x[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) x[u] = (p0 + 8 * u < a.np) ? ld_sys_f32(a.tile_part[p0 + 8 * u] + pidx) : 0.0f;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) s += x[u];
+        }
+        sred[wp][lane] = s;
+        __syncthreads();
+        if (wp == 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) g += sred[k][lane];
+        }
+    } else if (a.partials != nullptr) {
         const float* src = a.partials + j;
         float s = 0.0f;
 #pragma unroll 1
@@ -456,7 +487,7 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
     if (wp != 0) return;
     if (blockIdx.x == 0 && a.loss_out != nullptr) {
         float s = 0.0f;
-        for (int p = lane; p < a.nloss; p += 32) s += a.loss_part[p];
+        for (int p = lane; p < a.nloss; p += 32) s += a.tile_part[0] != nullptr ? ld_sys_f32(a.tile_loss[p]) : a.loss_part[p];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane == 0) *a.loss_out = s * a.loss_scale;
@@ -483,6 +514,34 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
     *reinterpret_cast<__half*>(a.wimg + off) = __float2half_rn(w);
     *reinterpret_cast<__half*>(a.eimg + off) = __float2half_rn(e);
     if (trc) a.dbg[4089 + 2 * (blockIdx.x != 0)] = global_ns();
+}
+
+// Fused peer all-reduce hand-off (nrc_train_frame_dp_peer), one thread: after
+// this rank's partials kernel (stream order), publish them to every rank with
+// a system-scope release add on its counter, then wait until all `world` ranks
+// have published step `target / world` (acquire).  Bounded: after ~20 s it
+// gives up and counts a timeout instead of hanging the GPU.
+struct DpPeers {
+    unsigned long long* ctr[kMaxParts];  // every rank's hand-off counter (own included)
+};
+__global__ void nrc_dp_exchange_kernel(DpPeers peers, int world, unsigned long long* own, unsigned long long target,
+                                       unsigned long long* timeouts) {
+    pdl_trigger();  // the optimiser kernel may become resident (it waits for this grid)
+    if (threadIdx.x != 0) return;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    for (int p = 0; p < world; ++p)
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(peers.ctr[p]) : "memory");
+    const long long t0 = global_ns();
+    unsigned long long v = 0;
+    while (true) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(own) : "memory");
+        if (v >= target) break;
+        if (global_ns() - t0 > 20000000000ll) {
+            atomicAdd(timeouts, 1ull);
+            break;
+        }
+        __nanosleep(128);
+    }
 }
 
 }  // namespace nrc

@@ -130,6 +130,31 @@ class DataParallelFrame:
         self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
         return out
 
+    def train_frame_allreduce_peer(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int,
+                                   shuffle_seed: int, losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+        """SURVEY 8(e) mitigation 2 / 8(f) N3 (ii): data-parallel training with
+        the per-step gradient all-reduce fused into the optimiser kernel over
+        peer memory (nrc_train_frame_dp_peer): every rank computes the partials
+        of its share of each batch's 128-row tiles, then every rank's optimiser
+        reads all ranks' partials in tile order (NVLink loads) -- no NCCL call,
+        bitwise equal to single-GPU nrc_train_frame.  Records replicated on
+        every rank (as in train_frame).  The state arenas are exchanged once
+        (CUDA IPC over the process group)."""
+        from .nrc import ipc_export_ptr, ipc_import
+        if getattr(self, "_arena_ptrs", None) is None:
+            mine = ipc_export_ptr(self.cache.state_ptr)
+            everyone = [None] * self.world
+            dist.all_gather_object(everyone, mine, group=self.group)
+            self._arena_ptrs = [self.cache.state_ptr if r == self.rank else ipc_import(*everyone[r])
+                                for r in range(self.world)]
+            if torch.cuda.is_available():
+                torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)  # every arena is initialised before any peer writes to it
+        out = self.cache.train_frame_dp_peer(records, targets, s, l, shuffle_seed, self.rank, self.world,
+                                             self._arena_ptrs, losses)
+        self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
+        return out
+
     def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
                     losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
         """All s steps of the frame's training on the full (replicated) record

@@ -123,6 +123,17 @@ def ipc_export(t: torch.Tensor):
     return bytes(h), off.value
 
 
+def ipc_export_ptr(ptr: int):
+    """(64-byte handle, offset) of the device allocation containing address ptr."""
+    L = _lib.load()
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_uint64()
+    st = L.nrc_ipc_export(ctypes.c_void_p(int(ptr)), h, ctypes.byref(off))
+    if st != 0:
+        raise NRCError(f"nrc_ipc_export: {L.nrc_status_string(st).decode()}")
+    return bytes(h), off.value
+
+
 def ipc_import(handle: bytes, offset: int) -> int:
     """Device pointer (int) to another process's allocation + offset."""
     L = _lib.load()
@@ -264,6 +275,35 @@ class RadianceCache:
                                                  int(shuffle_seed) & (2 ** 64 - 1), _ptr(losses), _stream(stream)),
                     "nrc_train_frame_parts")
         return losses
+
+    @property
+    def state_ptr(self) -> int:
+        """Device address of this cache's state arena (256-byte aligned)."""
+        return self._state_ptr
+
+    def train_frame_dp_peer(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
+                            rank: int, world: int, peer_states, losses: Optional[torch.Tensor] = None,
+                            stream=None) -> torch.Tensor:
+        """nrc_train_frame_dp_peer: data-parallel frame training with the
+        gradient all-reduce fused into the optimiser over peer memory
+        (peer_states: every rank's state-arena address, own included)."""
+        records = self._rec(records)
+        n = records.shape[0]
+        self._f32(targets, (n, 3), "targets")
+        if len(peer_states) != world:
+            raise NRCError("one state arena per rank required")
+        ps = (ctypes.c_void_p * world)(*[int(p) for p in peer_states])
+        if losses is None:
+            losses = torch.zeros(max(int(s), 1), dtype=torch.float32, device=self.device)
+        self._check(self.L.nrc_train_frame_dp_peer(self.h, _ptr(records), _ptr(targets), n, int(s), int(l),
+                                                   int(shuffle_seed) & (2 ** 64 - 1), int(rank), int(world), ps,
+                                                   _ptr(losses), _stream(stream)), "nrc_train_frame_dp_peer")
+        return losses
+
+    def dp_timeouts(self) -> int:
+        c = ctypes.c_uint64()
+        self._check(self.L.nrc_dp_timeouts(self.h, ctypes.byref(c)), "nrc_dp_timeouts")
+        return int(c.value)
 
     def train_frame_backward(self, records: torch.Tensor, targets: torch.Tensor, l: int, shuffle_seed: int, j: int,
                              row_begin: int, row_end: int, grad: Optional[torch.Tensor] = None,

@@ -162,3 +162,48 @@ def test_replicated_frame_after_allgather(tmp_path):
     ref.train_frame(torch.from_numpy(recs), torch.from_numpy(tgts), S, L, SEED, ref_losses)
     np.testing.assert_array_equal(res[0]["w"], ref.oc.w)
     np.testing.assert_array_equal(res[0]["losses"], ref_losses.numpy())
+
+
+class ArenaRecorder:
+    """Stand-in cache for the fused peer all-reduce orchestration: records
+    the arena list nrc_train_frame_dp_peer would receive."""
+
+    def __init__(self, rank):
+        self.state_ptr = 0x10000 * (rank + 1)
+        self.calls = []
+
+    def train_frame_dp_peer(self, records, targets, s, l, seed, rank, world, peer_states, losses=None):
+        self.calls.append((s, l, seed, rank, world, list(peer_states)))
+        return losses
+
+
+def _worker_arena(rank, world, port, out_dir):
+    import paper_2106_12372_b200.nrc as nrcmod
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        # CUDA IPC stand-ins: a "handle" names the exporting address; an
+        # imported mapping is that address + 1 (a different virtual address)
+        nrcmod.ipc_export_ptr = lambda ptr: (b"%d" % ptr, 0)
+        nrcmod.ipc_import = lambda handle, off: int(handle) + 1 + off
+        cache = ArenaRecorder(rank)
+        frame = dp.DataParallelFrame(cache)
+        recs = torch.zeros((8, 16))
+        for seed in (1, 2):  # the exchange happens once
+            frame.train_frame_allreduce_peer(recs, torch.zeros((8, 3)), 2, 4, seed)
+        np.save(os.path.join(out_dir, f"arena{rank}.npy"), np.array(cache.calls, dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduce_peer_arena_exchange(tmp_path):
+    """train_frame_allreduce_peer: every rank passes one arena per rank in
+    rank order -- its own address at its index, the peers' mapped addresses
+    elsewhere -- with its rank and the world size, exchanged once."""
+    world = 2
+    mp.spawn(_worker_arena, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        calls = np.load(tmp_path / f"arena{r}.npy", allow_pickle=True)
+        assert len(calls) == 2
+        for (s, l, seed, rank, w, peers), want_seed in zip(calls, (1, 2)):
+            assert (s, l, seed, rank, w) == (2, 4, want_seed, r, world)
+            assert peers == [0x10000 * (k + 1) + (0 if k == r else 1) for k in range(world)]
