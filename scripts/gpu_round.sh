@@ -20,4 +20,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:nrc_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:nrc_adam_w_kernel -s 8 -c 1 \
   -o gpurun_out/prof_adam_w -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_adam_w.log 2>&1
 bash scripts/ncu_width.sh
+timeout 900 python scripts/c3_convergence.py --out gpurun_out/c3.json > gpurun_out/c3.log 2>&1
 ls -la gpurun_out
