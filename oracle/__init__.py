@@ -70,6 +70,8 @@ def lib():
         L.orc_backward.restype = None; L.orc_backward.argtypes = [vp, vp, vp, vp]
         L.orc_grad_batch.restype = None
         L.orc_grad_batch.argtypes = [vp, vp, vp, i64, vp, vp, d, ctypes.c_uint, vp, vp, vp]
+        L.orc_grad_batch_exact.restype = None
+        L.orc_grad_batch_exact.argtypes = [vp, vp, vp, i64, vp, vp, d, ctypes.c_uint, vp, vp, vp]
         L.orc_adam.restype = i64; L.orc_adam.argtypes = [vp, vp, vp, vp, i64, i64, d, d, d, d]
         L.orc_ema.restype = None; L.orc_ema.argtypes = [vp, vp, i64, i64, d, ctypes.c_int]
         L.orc_lcg_params.restype = None; L.orc_lcg_params.argtypes = [u64, u64, vp, vp, vp]
@@ -308,8 +310,9 @@ def backward(W, H, dy):
     return G
 
 
-def grad_batch(W, recs, tgts, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), eps=0.01, flags=FACTORIZE):
-    """Un-normalised sum over records of dl/dW, the loss sum, #bad targets."""
+def grad_batch(W, recs, tgts, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), eps=0.01, flags=FACTORIZE, exact=False):
+    """Un-normalised sum over records of dl/dW, the loss sum, #bad targets
+    (exact=True: with the exact encoding, N4)."""
     W = _c(W, np.float64)
     recs = _c(recs, np.float32).reshape(-1, 16)
     tgts = _c(tgts, np.float32).reshape(-1, 3)
@@ -317,7 +320,8 @@ def grad_batch(W, recs, tgts, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), eps=0.01, fl
     G = np.zeros(NPARAM, np.float64)
     ls = np.zeros(1, np.float64)
     nb = np.zeros(1, np.int64)
-    lib().orc_grad_batch(W.ctypes.data, recs.ctypes.data, tgts.ctypes.data, recs.shape[0], lo.ctypes.data,
+    fn = lib().orc_grad_batch_exact if exact else lib().orc_grad_batch
+    fn(W.ctypes.data, recs.ctypes.data, tgts.ctypes.data, recs.shape[0], lo.ctypes.data,
                          hi.ctypes.data, float(eps), int(flags), G.ctypes.data, ls.ctypes.data, nb.ctypes.data)
     return G, float(ls[0]), int(nb[0])
 

@@ -23,6 +23,8 @@
  *       forms, SPEC worked examples, periodicity, integral of quartic = 1)
  *   orc_encode ............................................. pinned (golden
  *       vector tests/golden/encode_c0.txt, structural invariants)
+ *   orc_grad_batch_exact (N4 training) ..................... pinned (central
+ *       finite differences through the exact encodings)
  *   orc_freq_sin / orc_gauss / orc_encode_exact (N4) ....... pinned (sin at
  *       dyadic points, Gaussian closed forms, layout shared with orc_encode)
  *   orc_query_accumulate ................................... pinned (unit
@@ -450,9 +452,9 @@ void orc_backward(const double* W, const double* H, const double* dy, double* G)
  * fixed number of contiguous chunks, each summed in index order, and the
  * chunk sums are added in chunk order. */
 #define ORC_CHUNKS 64
-void orc_grad_batch(const double* W, const float* recs, const float* tgts, int64_t n, const float* lo,
-                    const float* hi, double eps, unsigned flags, double* G, double* loss_sum,
-                    int64_t* n_bad_targets)
+static void orc_grad_batch_enc(const double* W, const float* recs, const float* tgts, int64_t n, const float* lo,
+                               const float* hi, double eps, unsigned flags, double* G, double* loss_sum,
+                               int64_t* n_bad_targets, int exact)
 {
     double* Gc = (double*)calloc((size_t)ORC_CHUNKS * ORC_NPARAM, sizeof(double));
     double lc[ORC_CHUNKS];
@@ -471,7 +473,7 @@ void orc_grad_batch(const double* W, const float* recs, const float* tgts, int64
                 continue;
             }
             double e[64], H[6 * 64], y[3], yhat[3], t[3], dyhat[3], dy[3];
-            orc_encode(rec, lo, hi, e);
+            if (exact) orc_encode_exact(rec, lo, hi, e); else orc_encode(rec, lo, hi, e);
             orc_forward(W, e, H, y);
             for (int c = 0; c < 3; ++c) {
                 double f = (flags & ORC_FACTORIZE) ? (double)rec[10 + c] + (double)rec[13 + c] : 1.0;
@@ -500,6 +502,23 @@ void orc_grad_batch(const double* W, const float* recs, const float* tgts, int64
     free(Gc);
     if (loss_sum) *loss_sum = lsum;
     if (n_bad_targets) *n_bad_targets = nbad;
+}
+
+void orc_grad_batch(const double* W, const float* recs, const float* tgts, int64_t n, const float* lo,
+                    const float* hi, double eps, unsigned flags, double* G, double* loss_sum,
+                    int64_t* n_bad_targets)
+{
+    orc_grad_batch_enc(W, recs, tgts, n, lo, hi, eps, flags, G, loss_sum, n_bad_targets, 0);
+}
+
+/* orc_grad_batch with the exact encoding (N4: sin frequency + Gaussian
+ * one-blob, orc_encode_exact) -- the training counterpart of
+ * orc_query_batch_exact. */
+void orc_grad_batch_exact(const double* W, const float* recs, const float* tgts, int64_t n, const float* lo,
+                          const float* hi, double eps, unsigned flags, double* G, double* loss_sum,
+                          int64_t* n_bad_targets)
+{
+    orc_grad_batch_enc(W, recs, tgts, n, lo, hi, eps, flags, G, loss_sum, n_bad_targets, 1);
 }
 
 /* ---- Adam (reading R11: lr, beta1, beta2, eps outside sqrt,

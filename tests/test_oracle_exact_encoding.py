@@ -4,6 +4,7 @@ one-blob's closed forms, and the shared layout with orc_encode."""
 import math
 
 import numpy as np
+import pytest
 
 import nrc_inputs
 
@@ -42,3 +43,43 @@ def test_encode_exact_layout(orc):
             np.testing.assert_allclose(e[:, 12 * a + d], np.sin(np.pi * v * 2.0 ** d), rtol=0, atol=1e-12)
     # one-blob entries lie in (0, 1/sqrt(2 pi)]
     assert np.all(e[:, 36:56] > 0) and np.all(e[:, 36:56] <= 1 / math.sqrt(2 * math.pi))
+
+
+def test_grad_batch_exact_finite_differences(orc):
+    """orc_grad_batch_exact (N4 training): the un-normalised batch gradient
+    through the exact encodings matches central finite differences of the
+    batch loss (lambda frozen) built from the pinned encode_exact,
+    forward and loss_frozen, within 1e-4 relative."""
+    import nrc_inputs
+    rng = np.random.default_rng(91)
+    NP, OFF = 20672, [0, 4096, 8192, 12288, 16384, 20480, 20672]
+    checked = 0
+    for trial in range(8):
+        W = rng.normal(0, 1.5 / 8, NP)
+        recs = nrc_inputs.records(2, seed=600 + trial)
+        tg = nrc_inputs.targets(recs, noise=0.3, seed=trial)
+        G, _, _ = orc.grad_batch(W, recs, tg, exact=True)
+        E = orc.encode_exact(recs)
+        F = (recs[:, 10:13] + recs[:, 13:16]).astype(np.float64)
+        lams, minabs = [], np.inf
+        for e, f in zip(E, F):
+            _, y = orc.forward(W, e)
+            lams.append(0.2126 * y[0] * f[0] + 0.7152 * y[1] * f[1] + 0.0722 * y[2] * f[2])
+            h = e
+            for i in range(5):
+                z = W[OFF[i]:OFF[i + 1]].reshape(64, 64) @ h
+                minabs = min(minabs, np.abs(z).min())
+                h = np.maximum(z, 0)
+        if minabs < 1e-4:
+            continue
+
+        def L(Wx):
+            return sum(orc.loss_frozen(orc.forward(Wx, e)[1] * f, t, 0.01, lam)
+                       for e, f, t, lam in zip(E, F, tg.astype(np.float64), lams))
+        for j in rng.choice(NP, 16, replace=False):
+            Wp = W.copy(); Wp[j] += 1e-6
+            Wm = W.copy(); Wm[j] -= 1e-6
+            fd = (L(Wp) - L(Wm)) / 2e-6
+            assert G[j] == pytest.approx(fd, rel=1e-4, abs=1e-8 * max(1, np.abs(G).max()))
+            checked += 1
+    assert checked >= 64
