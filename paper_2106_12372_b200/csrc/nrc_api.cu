@@ -444,7 +444,10 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
                         "cudaFuncSetAttribute(train w64)")) != NRC_OK ||
         (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 TrainW<128>::kSmemBytes),
-                        "cudaFuncSetAttribute(train w128)")) != NRC_OK)
+                        "cudaFuncSetAttribute(train w128)")) != NRC_OK ||
+        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<64, true>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, TrainW<64>::kSmemBytes),
+                        "cudaFuncSetAttribute(train w64 exact)")) != NRC_OK)
         return bail(s);
 
     // Glorot-uniform init from the counter-based splitmix64 stream (R16):
@@ -618,6 +621,16 @@ static int train_grid(const nrc_handle* h, uint32_t n) {
     if (h->train_ctas > 0 && h->train_ctas < cap) cap = h->train_ctas;
     return grid > cap ? cap : grid;
 }
+// The partials kernel for this handle's width / encoding, one tile per CTA up to `grid`.
+static cudaError_t launch_train_w_grid(nrc_handle* h, const TrainArgs& ta, int grid, cudaStream_t st) {
+    if (h->wi.W == 32)
+        return launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::kSmemBytes, st, ta);
+    if (h->wi.W == 128)
+        return launch_pdl(nrc_train_w_kernel<128>, dim3(grid), dim3(128), TrainW<128>::kSmemBytes, st, ta);
+    if (h->ep.exact)  // NRC_EXACT_ENCODING (width 64 only, validate_config)
+        return launch_pdl(nrc_train_w_kernel<64, true>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta);
+    return launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta);
+}
 // Width-generic partials kernel (nrc_train_w.cuh): one step over n rows.
 static nrc_status launch_train_w(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
                                  const Gather& gth, cudaStream_t st, int* nparts) {
@@ -625,12 +638,7 @@ static nrc_status launch_train_w(nrc_handle* h, const nrc_record* d_rec, const f
     if (h->dbg) ta.dbg = h->dbg + 4096 * (h->step % 4);  // diagnostics: one 4096-slot block per step
     const int grid = train_grid(h, n);
     *nparts = grid;
-    if (h->wi.W == 32)
-        NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::kSmemBytes, st, ta));
-    else if (h->wi.W == 128)
-        NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<128>, dim3(grid), dim3(128), TrainW<128>::kSmemBytes, st, ta));
-    else
-        NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta));
+    NRC_CUDA(h, launch_train_w_grid(h, ta, grid, st));
     NRC_LAUNCHED(h, "nrc_train_w_kernel");
     return NRC_OK;
 }
@@ -984,12 +992,7 @@ nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const
             ta.partials = h->d_partials() + size_t(parity) * kMaxDpTiles * pad;
             ta.loss_part = h->d_loss_part() + size_t(parity) * kMaxDpTiles;
             const int grid = int(t_lo(rank + 1) - t_lo(rank));  // one tile per CTA: CTA c -> tile t_lo(rank) + c
-            if (h->wi.W == 32)
-                NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::kSmemBytes, st, ta));
-            else if (h->wi.W == 128)
-                NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<128>, dim3(grid), dim3(128), TrainW<128>::kSmemBytes, st, ta));
-            else
-                NRC_CUDA(h, launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta));
+            NRC_CUDA(h, launch_train_w_grid(h, ta, grid, st));
             NRC_LAUNCHED(h, "nrc_train_w_kernel");
             ++launches;
         }

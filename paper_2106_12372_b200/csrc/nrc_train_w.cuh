@@ -85,7 +85,8 @@ __device__ __forceinline__ void train_gather_row(const TrainArgs& a, uint32_t ro
     do {                                                                                \
         if (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 127) a.dbg[32 * blockIdx.x + (k)] = global_ns(); \
     } while (0)
-template <int W>
+// EXACT: sin / Gaussian encoding primitives (NRC_EXACT_ENCODING, N4; width 64)
+template <int W, bool EXACT = false>
 __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     using D = NetDims<W>;
     using T = TrainW<W>;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         train_gather_row(a, row, rec, tg);
         {
             uint32_t h[32];
-            encode_record<false>(rec, a.ep, h);
+            encode_record<EXACT>(rec, a.ep, h);
             store_row_swz(slot(0), r, h);
         }
         if (first) {

@@ -1,12 +1,12 @@
 """Exact encodings (NRC_EXACT_ENCODING; readings R21, R22) on
-the GPU against the fp64 oracle: encoding within one fp16 ulp and query
-parity."""
+the GPU against the fp64 oracle: encoding within one fp16 ulp, query parity
+and the training gradient through the exact encodings (both training paths)."""
 import numpy as np
 import pytest
 import torch
 
 import nrc_inputs
-from parity import TOL_RADIANCE, fp16_ulp, radiance_err
+from parity import TOL_GRAD, TOL_RADIANCE, fp16_ulp, per_matrix_err, radiance_err
 
 pytestmark = pytest.mark.gpu
 
@@ -52,6 +52,28 @@ def test_exact_training_runs(nrc):
     losses = [c.train_frame(dev(tr), dev(tg), 4, 4096, j).cpu().numpy() for j in range(20)]
     assert np.all(np.isfinite(losses))
     assert np.mean(losses[-1]) < np.mean(losses[0])
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_exact_gradient_parity(nrc, orc, monkeypatch, fused):
+    """Training with NRC_EXACT_ENCODING encodes the training records with the
+    same exact primitives as the query: train_backward's gradient against
+    orc_grad_batch_exact (per matrix within 3e-2, loss within 1e-2) and away
+    from the cheap-encoding gradient -- for the default per-step kernels and
+    the fused cooperative kernel (NRC_TRAIN_FUSED=1)."""
+    if fused:
+        monkeypatch.setenv("NRC_TRAIN_FUSED", "1")
+    c = nrc.RadianceCache(nrc.Config(flags=nrc.FACTORIZE | nrc.CLAMP_QUERY | nrc.EXACT_ENCODING))
+    recs = nrc_inputs.records(3000, seed=502)
+    tg = nrc_inputs.targets(recs, noise=0.3, seed=3)
+    W = c.get_params("train").astype(np.float64)
+    g, ls = c.train_backward(dev(recs), dev(tg))
+    g = g.cpu().numpy()
+    ref, l_ref, _ = orc.grad_batch(W, recs, tg, exact=True)
+    assert max(per_matrix_err(g, ref)) <= TOL_GRAD
+    assert float(ls.item()) == pytest.approx(l_ref, rel=1e-2)
+    cheap, _, _ = orc.grad_batch(W, recs, tg)
+    assert max(per_matrix_err(cheap, ref)) > 3 * TOL_GRAD
 
 
 def test_exact_requires_width_64(nrc):
