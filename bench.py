@@ -163,6 +163,30 @@ def omp_threads():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_single_thread_ms():
+    """The oracle on one host thread (SURVEY 8(d) oracle timing): a 4096-query
+    + 512-record sample in a subprocess with OMP_NUM_THREADS=1, scaled to the
+    frame; None if it fails."""
+    code = ("import sys; sys.path.insert(0, %r); import bench; "
+            "print(bench.oracle_frame_estimate(4096, 512)[0])" % ROOT)
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, OMP_NUM_THREADS="1"),
+                             capture_output=True, text=True, timeout=300)
+        return float(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -190,7 +214,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (nrc_inputs seeded records)",
         "config": frame_config(args.gpus, args.train_mode),
         "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
-        "cpu_baseline": {"value": ms, "unit": "ms", "cores": omp_threads(), "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": omp_threads(), "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -306,6 +331,7 @@ def run_nrc(args):
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in ev]
     ms = float(np.mean(step_ms))
+    pct = [float(x) for x in np.percentile(step_ms, [10, 50, 90])]  # this rank's step distribution
     q_ms = float(np.mean(qt))
     if world > 1:
         t = torch.tensor([ms, q_ms], dtype=torch.float64, device=dev)
@@ -350,6 +376,7 @@ def run_nrc(args):
         "config": frame_config(world, args.train_mode),
         "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
         "query_ms": q_ms, "train_ms": ms - q_ms,
+        "ms_p10_p50_p90": pct,
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "nrc_query_ts_kernel", "achieved": achieved, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic, "traffic_unit": "bytes/launch",
@@ -364,7 +391,8 @@ def run_nrc(args):
     if rank == 0 and not args.no_cpu_baseline:
         cms, sample, _, _ = oracle_frame_estimate(16384, 2048)
         line["cpu_baseline"] = {"value": cms, "unit": "ms", "cores": omp_threads(), "kind": "oracle",
-                                "sample": sample}
+                                "sample": sample, "cpu_model": cpu_model(),
+                                "single_thread_value": oracle_single_thread_ms()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
