@@ -91,6 +91,17 @@ def lib():
         L.orc_train_step_w.restype = d
         L.orc_train_step_w.argtypes = [ctypes.c_int, vp, vp, vp, vp, i64, vp, vp, i64, vp, vp, d, ctypes.c_uint,
                                        d, d, d, d, d, ctypes.c_int, vp, vp, vp]
+        ci = ctypes.c_int
+        L.orc_param_count_d.restype = i64; L.orc_param_count_d.argtypes = [ci, ci]
+        L.orc_forward_stash_d.restype = None; L.orc_forward_stash_d.argtypes = [ci, ci, vp, vp, vp, vp]
+        L.orc_backward_d.restype = None; L.orc_backward_d.argtypes = [ci, ci, vp, vp, vp, vp]
+        L.orc_query_batch_d.restype = None; L.orc_query_batch_d.argtypes = [ci, ci, vp, vp, i64, vp, vp, ctypes.c_uint, vp]
+        L.orc_grad_batch_d.restype = None
+        L.orc_grad_batch_d.argtypes = [ci, ci, vp, vp, vp, i64, vp, vp, d, ctypes.c_uint, vp, vp, vp]
+        L.orc_init_weights_d.restype = None; L.orc_init_weights_d.argtypes = [ci, ci, u64, vp]
+        L.orc_train_step_d.restype = d
+        L.orc_train_step_d.argtypes = [ci, ci, vp, vp, vp, vp, i64, vp, vp, i64, vp, vp, d, ctypes.c_uint,
+                                       d, d, d, d, d, ctypes.c_int, vp, vp, vp]
         L.orc_gauss.restype = d; L.orc_gauss.argtypes = [d]
         L.orc_freq_sin.restype = None; L.orc_freq_sin.argtypes = [d, vp]
         L.orc_one_blob_gauss.restype = None; L.orc_one_blob_gauss.argtypes = [d, ctypes.c_int, vp]
@@ -231,6 +242,57 @@ def grad_batch_w(hw, W, recs, tgts, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), eps=0.
     return G, float(ls[0]), int(nb[0])
 
 
+# ---------------------------------------------------------------- depth variants (N4)
+def param_count_d(hw: int, nh: int) -> int:
+    return int(lib().orc_param_count_d(int(hw), int(nh)))
+
+
+def forward_stash_d(hw, nh, W, e):
+    W = _c(W, np.float64); e = _c(e, np.float64)
+    H = np.zeros(64 + nh * hw, np.float64); y = np.zeros(3, np.float64)
+    lib().orc_forward_stash_d(int(hw), int(nh), W.ctypes.data, e.ctypes.data, H.ctypes.data, y.ctypes.data)
+    return H, y
+
+
+def backward_d(hw, nh, W, H, dy):
+    W = _c(W, np.float64); H = _c(H, np.float64); dy = _c(dy, np.float64)
+    G = np.zeros(param_count_d(hw, nh), np.float64)
+    lib().orc_backward_d(int(hw), int(nh), W.ctypes.data, H.ctypes.data, dy.ctypes.data, G.ctypes.data)
+    return G
+
+
+def query_d(hw, nh, W, recs, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), flags=FACTORIZE | CLAMP_QUERY) -> np.ndarray:
+    W = _c(W, np.float64)
+    assert W.size == param_count_d(hw, nh)
+    recs = _c(recs, np.float32).reshape(-1, 16)
+    lo, hi = _c(aabb_lo, np.float32), _c(aabb_hi, np.float32)
+    q = np.zeros((recs.shape[0], 3), np.float64)
+    lib().orc_query_batch_d(int(hw), int(nh), W.ctypes.data, recs.ctypes.data, recs.shape[0], lo.ctypes.data,
+                            hi.ctypes.data, int(flags), q.ctypes.data)
+    return q
+
+
+def grad_batch_d(hw, nh, W, recs, tgts, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), eps=0.01, flags=FACTORIZE):
+    W = _c(W, np.float64)
+    assert W.size == param_count_d(hw, nh)
+    recs = _c(recs, np.float32).reshape(-1, 16)
+    tgts = _c(tgts, np.float32).reshape(-1, 3)
+    lo, hi = _c(aabb_lo, np.float32), _c(aabb_hi, np.float32)
+    G = np.zeros(param_count_d(hw, nh), np.float64)
+    ls = np.zeros(1, np.float64)
+    nb = np.zeros(1, np.int64)
+    lib().orc_grad_batch_d(int(hw), int(nh), W.ctypes.data, recs.ctypes.data, tgts.ctypes.data, recs.shape[0],
+                           lo.ctypes.data, hi.ctypes.data, float(eps), int(flags), G.ctypes.data, ls.ctypes.data,
+                           nb.ctypes.data)
+    return G, float(ls[0]), int(nb[0])
+
+
+def init_weights_d(hw: int, nh: int, seed: int) -> np.ndarray:
+    W = np.zeros(param_count_d(hw, nh), np.float32)
+    lib().orc_init_weights_d(int(hw), int(nh), int(seed) & (2**64 - 1), W.ctypes.data)
+    return W
+
+
 # ---------------------------------------------------------------- exact encodings (N4)
 def gauss(x: float) -> float:
     return lib().orc_gauss(float(x))
@@ -365,12 +427,14 @@ class OracleCache:
 
     def __init__(self, W32=None, seed=1, aabb_lo=(0, 0, 0), aabb_hi=(1, 1, 1), lr=1e-2, b1=0.9, b2=0.99,
                  adam_eps=1e-8, loss_eps=0.01, ema_alpha=0.99, flags=FACTORIZE | CLAMP_QUERY,
-                 ema_printed=False, hidden_width=64):
+                 ema_printed=False, hidden_width=64, hidden_layers=5):
         self.hw = int(hidden_width)
+        self.nh = int(hidden_layers)
         if W32 is None:
-            W32 = init_weights(seed) if self.hw == 64 else init_weights_w(self.hw, seed)
+            W32 = (init_weights_d(self.hw, self.nh, seed) if self.nh != 5 else
+                   init_weights(seed) if self.hw == 64 else init_weights_w(self.hw, seed))
         W32 = np.asarray(W32, np.float32)
-        self.P = NPARAM if self.hw == 64 else param_count_w(self.hw)
+        self.P = param_count_d(self.hw, self.nh) if self.nh != 5 else NPARAM if self.hw == 64 else param_count_w(self.hw)
         assert W32.size == self.P
         self.w = W32.astype(np.float64)
         self.m = np.zeros(self.P); self.v = np.zeros(self.P)
@@ -391,6 +455,15 @@ class OracleCache:
         self.t += 1
         G = np.zeros(self.P, np.float64)
         bg = np.zeros(1, np.int64); bt = np.zeros(1, np.int64)
+        if self.nh != 5:
+            l = lib().orc_train_step_d(self.hw, self.nh, self.w.ctypes.data, self.m.ctypes.data, self.v.ctypes.data,
+                                       self.wbar.ctypes.data, self.t, recs.ctypes.data, tgts.ctypes.data, n,
+                                       self.lo.ctypes.data, self.hi.ctypes.data, self.loss_eps,
+                                       int(self.flags & FACTORIZE), self.lr, self.b1, self.b2, self.adam_eps,
+                                       self.ema_alpha, int(self.ema_printed), G.ctypes.data, bg.ctypes.data,
+                                       bt.ctypes.data)
+            self.bad_grads += int(bg[0]); self.bad_targets += int(bt[0])
+            return (l, G) if return_grad else l
         if self.hw != 64:
             l = lib().orc_train_step_w(self.hw, self.w.ctypes.data, self.m.ctypes.data, self.v.ctypes.data,
                                        self.wbar.ctypes.data, self.t, recs.ctypes.data, tgts.ctypes.data, n,
@@ -410,6 +483,8 @@ class OracleCache:
 
     def query(self, recs, use_ema=True):
         W = self.wbar if (use_ema and self.ema_alpha > 0) else self.w
+        if self.nh != 5:
+            return query_d(self.hw, self.nh, W, recs, self.lo, self.hi, self.flags)
         if self.hw != 64:
             return query_w(self.hw, W, recs, self.lo, self.hi, self.flags)
         return query(W, recs, self.lo, self.hi, self.flags)

@@ -23,6 +23,9 @@
  *       forms, SPEC worked examples, periodicity, integral of quartic = 1)
  *   orc_encode ............................................. pinned (golden
  *       vector tests/golden/encode_c0.txt, structural invariants)
+ *   orc_*_d (depth nh, N4) ................................... pinned (nh = 5
+ *       equals the pinned width functions; identity-layer extensions of a
+ *       net compute the same function and gradients; finite differences)
  *   orc_grad_batch_exact (N4 training) ..................... pinned (central
  *       finite differences through the exact encodings)
  *   orc_freq_sin / orc_gauss / orc_encode_exact (N4) ....... pinned (sin at
@@ -811,6 +814,188 @@ double orc_train_step_w(int hw, double* w, double* m, double* v, double* wbar, i
     if (n <= 0) return 0.0;
     double* G = (double*)malloc(sizeof(double) * (size_t)P);
     orc_grad_batch_w(hw, w, recs, tgts, n, lo, hi, loss_eps, flags, G, &lsum, bad_targets);
+    for (int64_t j = 0; j < P; ++j) G[j] /= (double)n;
+    if (G_out) memcpy(G_out, G, sizeof(double) * (size_t)P);
+    int64_t bad = orc_adam(w, m, v, G, P, t, lr, b1, b2, adam_eps);
+    if (bad_grads) *bad_grads = bad;
+    orc_ema(wbar, w, P, t, ema_a, ema_printed);
+    free(G);
+    return lsum / (double)n;
+}
+
+/* ---- depth variants ("depth other than 5"): the network of
+ * orc_forward_w with nh hidden layers instead of five (P:L694 fixes five; the
+ * variant keeps the 64-dim input, hidden width hw, ReLU, linear 3-output
+ * layer).  Logical layout: W0 [hw][64], W1..W_{nh-1} [hw][hw], W_nh [3][hw]
+ * (the output layer), row-major [out][in]; P = 64 hw + (nh-1) hw^2 + 3 hw.
+ * H holds h_0 (64 values) then h_1..h_nh (hw each). */
+int64_t orc_param_count_d(int hw, int nh) { return 64 * (int64_t)hw + (int64_t)(nh - 1) * hw * hw + 3 * (int64_t)hw; }
+
+static int64_t orc_mat_off_d(int hw, int nh, int i)
+{
+    (void)nh;
+    if (i == 0) return 0;
+    return 64 * (int64_t)hw + (int64_t)(i - 1) * hw * hw; /* i = nh: the output layer */
+}
+
+void orc_forward_stash_d(int hw, int nh, const double* W, const double* e, double* H, double* y)
+{
+    for (int k = 0; k < ORC_IN; ++k) H[k] = e[k];
+    for (int i = 0; i < nh; ++i) {
+        const int in = i == 0 ? ORC_IN : hw;
+        const double* Wi = W + orc_mat_off_d(hw, nh, i);
+        const double* hin = i == 0 ? H : H + ORC_IN + (int64_t)(i - 1) * hw;
+        double* hout = H + ORC_IN + (int64_t)i * hw;
+        for (int o = 0; o < hw; ++o) {
+            double acc = 0.0;
+            for (int k = 0; k < in; ++k) acc += Wi[(int64_t)in * o + k] * hin[k];
+            hout[o] = acc > 0.0 ? acc : 0.0;
+        }
+    }
+    const double* Wo = W + orc_mat_off_d(hw, nh, nh);
+    const double* hl = H + ORC_IN + (int64_t)(nh - 1) * hw;
+    for (int o = 0; o < 3; ++o) {
+        double acc = 0.0;
+        for (int k = 0; k < hw; ++k) acc += Wo[(int64_t)hw * o + k] * hl[k];
+        y[o] = acc;
+    }
+}
+
+/* Reverse mode (cf. orc_backward_w): G_nh += dy h_nh^T; delta = W_nh^T dy;
+ * for i = nh-1..0: g = delta * 1[h_{i+1} > 0] (R17); G_i += g h_i^T;
+ * delta = W_i^T g (i > 0). */
+void orc_backward_d(int hw, int nh, const double* W, const double* H, const double* dy, double* G)
+{
+    double delta[128], g[128];
+    const double* Wo = W + orc_mat_off_d(hw, nh, nh);
+    double* Go = G + orc_mat_off_d(hw, nh, nh);
+    const double* hl = H + ORC_IN + (int64_t)(nh - 1) * hw;
+    for (int o = 0; o < 3; ++o)
+        for (int k = 0; k < hw; ++k) Go[(int64_t)hw * o + k] += dy[o] * hl[k];
+    for (int k = 0; k < hw; ++k) {
+        double acc = 0.0;
+        for (int o = 0; o < 3; ++o) acc += Wo[(int64_t)hw * o + k] * dy[o];
+        delta[k] = acc;
+    }
+    for (int i = nh - 1; i >= 0; --i) {
+        const int in = i == 0 ? ORC_IN : hw;
+        const double* Wi = W + orc_mat_off_d(hw, nh, i);
+        double* Gi = G + orc_mat_off_d(hw, nh, i);
+        const double* hout = H + ORC_IN + (int64_t)i * hw;
+        const double* hin = i == 0 ? H : H + ORC_IN + (int64_t)(i - 1) * hw;
+        for (int o = 0; o < hw; ++o) g[o] = hout[o] > 0.0 ? delta[o] : 0.0;
+        for (int o = 0; o < hw; ++o)
+            for (int k = 0; k < in; ++k) Gi[(int64_t)in * o + k] += g[o] * hin[k];
+        if (i > 0) {
+            for (int k = 0; k < in; ++k) {
+                double acc = 0.0;
+                for (int o = 0; o < hw; ++o) acc += Wi[(int64_t)in * o + k] * g[o];
+                delta[k] = acc;
+            }
+        }
+    }
+}
+
+void orc_query_batch_d(int hw, int nh, const double* W, const float* recs, int64_t n, const float* lo,
+                       const float* hi, unsigned flags, double* q)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double e[64], H[64 + 16 * 128], y[3];
+        const float* rec = recs + 16 * i;
+        orc_encode(rec, lo, hi, e);
+        orc_forward_stash_d(hw, nh, W, e, H, y);
+        for (int c = 0; c < 3; ++c) {
+            double v = y[c];
+            if (flags & ORC_FACTORIZE) v *= (double)rec[10 + c] + (double)rec[13 + c];
+            if ((flags & ORC_CLAMP_QUERY) && v < 0.0) v = 0.0;
+            q[3 * i + c] = v;
+        }
+    }
+}
+
+/* orc_grad_batch at width hw and depth nh (same fixed chunking). */
+void orc_grad_batch_d(int hw, int nh, const double* W, const float* recs, const float* tgts, int64_t n,
+                      const float* lo, const float* hi, double eps, unsigned flags, double* G, double* loss_sum,
+                      int64_t* n_bad_targets)
+{
+    const int64_t P = orc_param_count_d(hw, nh);
+    double* Gc = (double*)calloc((size_t)ORC_CHUNKS * (size_t)P, sizeof(double));
+    double lc[ORC_CHUNKS];
+    int64_t bc[ORC_CHUNKS];
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int ch = 0; ch < ORC_CHUNKS; ++ch) {
+        int64_t i0 = n * ch / ORC_CHUNKS, i1 = n * (ch + 1) / ORC_CHUNKS;
+        double* Gk = Gc + (size_t)ch * (size_t)P;
+        double lsum = 0.0;
+        int64_t nbad = 0;
+        for (int64_t i = i0; i < i1; ++i) {
+            const float* rec = recs + 16 * i;
+            const float* tg = tgts + 3 * i;
+            if (!(isfinite(tg[0]) && isfinite(tg[1]) && isfinite(tg[2]))) {
+                ++nbad;
+                continue;
+            }
+            double e[64], H[64 + 16 * 128], y[3], yhat[3], t[3], dyhat[3], dy[3];
+            orc_encode(rec, lo, hi, e);
+            orc_forward_stash_d(hw, nh, W, e, H, y);
+            for (int c = 0; c < 3; ++c) {
+                double f = (flags & ORC_FACTORIZE) ? (double)rec[10 + c] + (double)rec[13 + c] : 1.0;
+                yhat[c] = y[c] * f;
+                t[c] = tg[c];
+            }
+            lsum += orc_loss(yhat, t, eps, dyhat);
+            for (int c = 0; c < 3; ++c) {
+                double f = (flags & ORC_FACTORIZE) ? (double)rec[10 + c] + (double)rec[13 + c] : 1.0;
+                dy[c] = dyhat[c] * f;
+            }
+            orc_backward_d(hw, nh, W, H, dy, Gk);
+        }
+        lc[ch] = lsum;
+        bc[ch] = nbad;
+    }
+    memset(G, 0, sizeof(double) * (size_t)P);
+    double lsum = 0.0;
+    int64_t nbad = 0;
+    for (int ch = 0; ch < ORC_CHUNKS; ++ch) {
+        const double* Gk = Gc + (size_t)ch * (size_t)P;
+        for (int64_t j = 0; j < P; ++j) G[j] += Gk[j];
+        lsum += lc[ch];
+        nbad += bc[ch];
+    }
+    free(Gc);
+    if (loss_sum) *loss_sum = lsum;
+    if (n_bad_targets) *n_bad_targets = nbad;
+}
+
+/* Reading R16 at width hw and depth nh: counter (i << 32 | r fan_in + c),
+ * layer index i = 0..nh (the output layer is i = nh; at nh = 5 this is
+ * orc_init_weights_w). */
+void orc_init_weights_d(int hw, int nh, uint64_t seed, float* W32)
+{
+    for (int i = 0; i <= nh; ++i) {
+        int rows = i < nh ? hw : 3, cols = i == 0 ? ORC_IN : hw;
+        double bound = sqrt(6.0 / ((double)cols + (double)rows));
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) {
+                uint64_t ctr = ((uint64_t)i << 32) | (uint64_t)(r * cols + c);
+                double u = (double)(orc_splitmix64(seed ^ ctr) >> 11) * (1.0 / 9007199254740992.0);
+                W32[orc_mat_off_d(hw, nh, i) + (int64_t)cols * r + c] = (float)((2.0 * u - 1.0) * bound);
+            }
+    }
+}
+
+/* orc_train_step at width hw and depth nh. */
+double orc_train_step_d(int hw, int nh, double* w, double* m, double* v, double* wbar, int64_t t, const float* recs,
+                        const float* tgts, int64_t n, const float* lo, const float* hi, double loss_eps,
+                        unsigned flags, double lr, double b1, double b2, double adam_eps, double ema_a,
+                        int ema_printed, double* G_out, int64_t* bad_grads, int64_t* bad_targets)
+{
+    const int64_t P = orc_param_count_d(hw, nh);
+    double lsum = 0.0;
+    if (n <= 0) return 0.0;
+    double* G = (double*)malloc(sizeof(double) * (size_t)P);
+    orc_grad_batch_d(hw, nh, w, recs, tgts, n, lo, hi, loss_eps, flags, G, &lsum, bad_targets);
     for (int64_t j = 0; j < P; ++j) G[j] /= (double)n;
     if (G_out) memcpy(G_out, G, sizeof(double) * (size_t)P);
     int64_t bad = orc_adam(w, m, v, G, P, t, lr, b1, b2, adam_eps);
