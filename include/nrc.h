@@ -97,7 +97,10 @@ typedef struct nrc_config {
                                 * query and training alike.  nrc_param_count() gives
                                 * 64 W + 4 W^2 + 3 W (logical layout: W0 W x 64,
                                 * W1..W4 W x W, W5 3 x W, row-major [out][in]).        */
-    uint32_t n_hidden_layers;  /* 5; fixed in ABI v1                         */
+    uint32_t n_hidden_layers;  /* 5; depth variants: 1..8 / 1..7 / 1..5
+                                * at hidden_width 32 / 64 / 128 (training-kernel shared
+                                * memory), query and training alike; parameters
+                                * 64 W + (n-1) W^2 + 3 W                              */
     uint32_t max_batch;        /* largest n accepted by query/train calls             */
     float aabb_min[3];         /* position normalisation domain (R3)           */
     float aabb_max[3];

@@ -41,10 +41,10 @@ template <int G, int S>
 struct QueryLauncherTS {
     static cudaError_t set_smem() {
         return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    query_ts_smem_bytes<G, S>());
+                                    query_ts_smem_bytes_nh<G, S, 64>(TrainW<64>::kMaxNh));
     }
     static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
-        nrc_query_ts_kernel<G, S><<<grid, 128 * G, query_ts_smem_bytes<G, S>(), st>>>(qa);
+        nrc_query_ts_kernel<G, S><<<grid, 128 * G, query_ts_smem_bytes_nh<G, S, 64>(int(qa.nh)), st>>>(qa);
     }
 };
 #define NRC_QCFG(G, S) {&QueryLauncher<G, S>::set_smem, &QueryLauncher<G, S>::launch, G}
@@ -62,20 +62,20 @@ template <int G, int S, int W>
 struct QueryLauncherW {
     static cudaError_t set_smem() {
         return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    query_ts_smem_bytes<G, S, W>());
+                                    query_ts_smem_bytes_nh<G, S, W>(TrainW<W>::kMaxNh));
     }
     static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
-        nrc_query_ts_kernel<G, S, W><<<grid, 128 * G, query_ts_smem_bytes<G, S, W>(), st>>>(qa);
+        nrc_query_ts_kernel<G, S, W><<<grid, 128 * G, query_ts_smem_bytes_nh<G, S, W>(int(qa.nh)), st>>>(qa);
     }
 };
 template <int G, int S, int W>
 struct QueryLauncherExact {
     static cudaError_t set_smem() {
         return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    query_ts_smem_bytes<G, S, W>());
+                                    query_ts_smem_bytes_nh<G, S, W>(TrainW<W>::kMaxNh));
     }
     static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
-        nrc_query_ts_kernel<G, S, W, true><<<grid, 128 * G, query_ts_smem_bytes<G, S, W>(), st>>>(qa);
+        nrc_query_ts_kernel<G, S, W, true><<<grid, 128 * G, query_ts_smem_bytes_nh<G, S, W>(int(qa.nh)), st>>>(qa);
     }
 };
 const QueryEntry kQueryExact = {&QueryLauncherExact<5, 1, 64>::set_smem, &QueryLauncherExact<5, 1, 64>::launch, 5};
@@ -87,29 +87,36 @@ const QueryEntry kQueryW32 = {&QueryLauncherW<NRC_W32_G, 1, 32>::set_smem, &Quer
 const QueryEntry kQueryW128 = {&QueryLauncherW<2, 1, 128>::set_smem, &QueryLauncherW<2, 1, 128>::launch, 2};
 constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
 
-// Runtime view of NetDims<W> (nrc_device.cuh) for the host code.
+// Runtime view of NetRt<W> (nrc_device.cuh) for the host code: width W,
+// nh hidden layers (layers 0..nh, nh = the output layer).
+constexpr int kMaxLayers = 9;  // nh <= 8
 struct WidthInfo {
-    int W = 64, padded = 0, logical = 0, img = 0;
-    int pad_off[7] = {}, rows[6] = {}, cols[6] = {};
+    int W = 64, nh = 5, padded = 0, logical = 0, img = 0;
+    int pad_off[kMaxLayers + 1] = {}, rows[kMaxLayers] = {}, cols[kMaxLayers] = {};
 };
 template <int W>
-WidthInfo width_info_t() {
-    using D = NetDims<W>;
+WidthInfo width_info_t(int nh) {
+    const NetRt<W> D(nh);
     WidthInfo w;
     w.W = W;
-    w.padded = D::kPadded;
-    w.logical = D::kLogical;
-    w.img = D::kImg;
-    for (int i = 0; i < 7; ++i) w.pad_off[i] = D::pad_off(i);
-    for (int i = 0; i < 6; ++i) {
-        w.rows[i] = i < 5 ? W : 3;  // logical rows (W5 has 3)
-        w.cols[i] = D::cols(i);
+    w.nh = nh;
+    w.padded = D.padded();
+    w.logical = D.logical();
+    w.img = D.img();
+    for (int i = 0; i <= nh + 1; ++i) w.pad_off[i] = D.pad_off(i);
+    for (int i = 0; i <= nh; ++i) {
+        w.rows[i] = i < nh ? W : 3;  // logical rows (the output layer has 3)
+        w.cols[i] = D.cols(i);
     }
     return w;
 }
 bool width_supported(uint32_t W) { return W == 32 || W == 64 || W == 128; }
-WidthInfo width_info(int W) {
-    return W == 32 ? width_info_t<32>() : W == 128 ? width_info_t<128>() : width_info_t<64>();
+// depth variants: 1..TrainW<W>::kMaxNh hidden layers (shared memory of the training kernel)
+int max_hidden_layers(uint32_t W) {
+    return W == 32 ? TrainW<32>::kMaxNh : W == 128 ? TrainW<128>::kMaxNh : TrainW<64>::kMaxNh;
+}
+WidthInfo width_info(int W, int nh) {
+    return W == 32 ? width_info_t<32>(nh) : W == 128 ? width_info_t<128>(nh) : width_info_t<64>(nh);
 }
 
 struct StateLayout {
@@ -118,8 +125,8 @@ struct StateLayout {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-StateLayout layout(int W) {
-    const WidthInfo wi = width_info(W);
+StateLayout layout(int W, int nh) {
+    const WidthInfo wi = width_info(W, nh);
     StateLayout L{};
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -259,9 +266,9 @@ static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, si
 
 template <int W>
 static void launch_images(nrc_handle* h, cudaStream_t st) {
-    const int blocks = (NetDims<W>::kPadded + 255) / 256;
-    nrc_image_w_kernel<W><<<blocks, 256, 0, st>>>(h->d_w(), h->d_wimg());
-    nrc_image_w_kernel<W><<<blocks, 256, 0, st>>>(h->d_ema(), h->d_eimg());
+    const int blocks = (h->wi.padded + 255) / 256;
+    nrc_image_w_kernel<W><<<blocks, 256, 0, st>>>(h->d_w(), h->d_wimg(), h->wi.nh);
+    nrc_image_w_kernel<W><<<blocks, 256, 0, st>>>(h->d_ema(), h->d_eimg(), h->wi.nh);
 }
 
 extern "C" {
@@ -301,8 +308,12 @@ static nrc_status validate_config(const nrc_config* c, std::string* why) {
         *why = "NRC_EXACT_ENCODING is built for hidden_width 64";
         return NRC_ERR_UNSUPPORTED;
     }
-    if (!width_supported(c->hidden_width) || c->n_hidden_layers != 5) {
-        *why = "hidden_width must be 32, 64 (P:L694) or 128 (width ablation) with 5 hidden layers";
+    if (!width_supported(c->hidden_width)) {
+        *why = "hidden_width must be 32, 64 (P:L694) or 128 (width ablation)";
+        return NRC_ERR_UNSUPPORTED;
+    }
+    if (c->n_hidden_layers < 1 || int(c->n_hidden_layers) > max_hidden_layers(c->hidden_width)) {
+        *why = "n_hidden_layers must be 5 (P:L694) or, for the depth variants, 1..8 / 1..7 / 1..5 at width 32 / 64 / 128";
         return NRC_ERR_UNSUPPORTED;
     }
     if (c->max_batch == 0) {
@@ -328,7 +339,7 @@ static nrc_status validate_config(const nrc_config* c, std::string* why) {
 size_t nrc_state_bytes(const nrc_config* cfg) {
     std::string why;
     if (validate_config(cfg, &why) != NRC_OK) return 0;
-    return layout(int(cfg->hidden_width)).total;
+    return layout(int(cfg->hidden_width), int(cfg->n_hidden_layers)).total;
 }
 
 const char* nrc_status_string(nrc_status s) {
@@ -382,7 +393,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
         std::fprintf(stderr, "nrc_init: %s\n", why.c_str());
         return s;
     }
-    const StateLayout L = layout(int(cfg->hidden_width));
+    const StateLayout L = layout(int(cfg->hidden_width), int(cfg->n_hidden_layers));
     if (!d_state || !aligned(d_state, 256)) return NRC_ERR_INVALID_ARGUMENT;
     if (state_bytes < L.total) return NRC_ERR_OUT_OF_MEMORY;
 
@@ -390,7 +401,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     h->cfg = *cfg;
     h->state = static_cast<uint8_t*>(d_state);
     h->L = L;
-    h->wi = width_info(int(cfg->hidden_width));
+    h->wi = width_info(int(cfg->hidden_width), int(cfg->n_hidden_layers));
     h->step = 0;
     h->launches = 0;
     for (int i = 0; i < 3; ++i) {
@@ -437,16 +448,16 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
                         "cudaFuncSetAttribute(train exact)")) != NRC_OK)
         return bail(s);
     if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                TrainW<32>::kSmemBytes),
+                                                TrainW<32>::smem_bytes(TrainW<32>::kMaxNh)),
                         "cudaFuncSetAttribute(train w32)")) != NRC_OK ||
         (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                TrainW<64>::kSmemBytes),
+                                                TrainW<64>::smem_bytes(TrainW<64>::kMaxNh)),
                         "cudaFuncSetAttribute(train w64)")) != NRC_OK ||
         (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                TrainW<128>::kSmemBytes),
+                                                TrainW<128>::smem_bytes(TrainW<128>::kMaxNh)),
                         "cudaFuncSetAttribute(train w128)")) != NRC_OK ||
-        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<64, true>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, TrainW<64>::kSmemBytes),
+        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TrainW<64>::smem_bytes(TrainW<64>::kMaxNh)),
                         "cudaFuncSetAttribute(train w64 exact)")) != NRC_OK)
         return bail(s);
 
@@ -454,7 +465,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     // counter (layer << 32 | r * fan_in + c), bound sqrt(6 / (fan_in + fan_out)).
     const WidthInfo& wi = h->wi;
     std::vector<float> w(size_t(wi.padded), 0.0f);
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i <= wi.nh; ++i) {  // layer wi.nh is the output layer
         const int rows = wi.rows[i], cols = wi.cols[i];
         const double bound = std::sqrt(6.0 / (double(cols) + double(rows)));
         for (int r = 0; r < rows; ++r)
@@ -489,7 +500,7 @@ static nrc_status check_train_width(nrc_handle* h) {
     if (width_supported(uint32_t(h->wi.W))) return NRC_OK;
     return fail(h, NRC_ERR_UNSUPPORTED, "unsupported hidden width for training");
 }
-static bool train_generic(const nrc_handle* h) { return h->wi.W != 64 || !h->train_fused; }
+static bool train_generic(const nrc_handle* h) { return h->wi.W != 64 || h->wi.nh != 5 || !h->train_fused; }
 static nrc_status check_handle(nrc_handle* h) {
     if (!h || !h->state) return NRC_ERR_STATE;
     int dev = -1;
@@ -512,8 +523,10 @@ static nrc_status query_impl(nrc_handle* h, const nrc_record* d_rec, uint64_t n,
     qa.pix = d_pix;
     qa.thr = d_thr;
     qa.image = d_image;
-    // the fused accumulate epilogue exists in the TMEM kernels only (entry 0 and the width kernels)
-    const int cfg = d_image ? 0 : h->query_cfg;
+    qa.nh = uint32_t(h->wi.nh);
+    // the fused accumulate epilogue and the depth variants exist in the TMEM
+    // kernels only (entry 0 and the width kernels)
+    const int cfg = (d_image || h->wi.nh != 5) ? 0 : h->query_cfg;
     const QueryEntry& qe = h->ep.exact        ? kQueryExact
                            : h->wi.W == 32   ? kQueryW32
                            : h->wi.W == 128  ? kQueryW128
@@ -612,6 +625,7 @@ static TrainArgs train_args(nrc_handle* h, const nrc_record* d_rec, const float*
     ta.loss_part = h->d_loss_part();
     ta.bad_targets = h->d_counters() + 1;
     ta.dbg = h->dbg;
+    ta.nh = uint32_t(h->wi.nh);
     return ta;
 }
 static int train_grid(const nrc_handle* h, uint32_t n) {
@@ -623,13 +637,14 @@ static int train_grid(const nrc_handle* h, uint32_t n) {
 }
 // The partials kernel for this handle's width / encoding, one tile per CTA up to `grid`.
 static cudaError_t launch_train_w_grid(nrc_handle* h, const TrainArgs& ta, int grid, cudaStream_t st) {
+    const int nh = h->wi.nh;
     if (h->wi.W == 32)
-        return launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::kSmemBytes, st, ta);
+        return launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::smem_bytes(nh), st, ta);
     if (h->wi.W == 128)
-        return launch_pdl(nrc_train_w_kernel<128>, dim3(grid), dim3(128), TrainW<128>::kSmemBytes, st, ta);
+        return launch_pdl(nrc_train_w_kernel<128>, dim3(grid), dim3(128), TrainW<128>::smem_bytes(nh), st, ta);
     if (h->ep.exact)  // NRC_EXACT_ENCODING (width 64 only, validate_config)
-        return launch_pdl(nrc_train_w_kernel<64, true>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta);
-    return launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::kSmemBytes, st, ta);
+        return launch_pdl(nrc_train_w_kernel<64, true>, dim3(grid), dim3(128), TrainW<64>::smem_bytes(nh), st, ta);
+    return launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::smem_bytes(nh), st, ta);
 }
 // Width-generic partials kernel (nrc_train_w.cuh): one step over n rows.
 static nrc_status launch_train_w(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
@@ -663,6 +678,7 @@ static AdamWArgs adam_w_args(nrc_handle* h) {
     aa.bad_grads = h->d_counters() + 0;
     aa.loss_part = h->d_loss_part();
     if (h->dbg) aa.dbg = h->dbg + 4096 * ((h->step + 3) % 4);  // the step's block (step already incremented)
+    aa.nh = h->wi.nh;
     return aa;
 }
 static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t st) {

@@ -56,6 +56,39 @@ struct NetDims {
     }
 };
 static_assert(NetDims<64>::kPadded == kParamPadded && NetDims<64>::kImg == kImgBytes, "W=64 layout");
+
+// NetDims<W> with a run-time number of hidden layers nh (SURVEY N4 depth
+// variants; nh = 5 gives NetDims<W>): layers 0..nh, layer nh is the output
+// layer (rows padded to 16); the same padded fp32 and fp16 image layouts.
+template <int W>
+struct NetRt {
+    int nh;
+    __host__ __device__ explicit NetRt(int nh_) : nh(nh_) {}
+    __host__ __device__ int rows(int i) const { return i < nh ? W : kOutPad; }
+    __host__ __device__ static constexpr int cols(int i) { return i == 0 ? 64 : W; }
+    __host__ __device__ static constexpr int kblocks(int i) { return (cols(i) + 63) / 64; }
+    __host__ __device__ int pad_off(int i) const {
+        return i == 0 ? 0 : i <= nh ? 64 * W + (i - 1) * W * W : 64 * W + (nh - 1) * W * W + kOutPad * W;
+    }
+    __host__ __device__ int img_off(int i) const {
+        return i == 0 ? 0
+                      : i <= nh ? W * 128 + (i - 1) * ((W + 63) / 64) * W * 128
+                                : W * 128 + (nh - 1) * ((W + 63) / 64) * W * 128 + ((W + 63) / 64) * kOutPad * 128;
+    }
+    __host__ __device__ int padded() const { return pad_off(nh + 1); }
+    __host__ __device__ int logical() const { return 64 * W + (nh - 1) * W * W + 3 * W; }
+    __host__ __device__ int img() const { return img_off(nh + 1); }
+    __host__ __device__ uint32_t img_byte(int i, int r, int c) const {
+        return uint32_t(img_off(i) + (c >> 6) * rows(i) * 128 + r * 128) +
+               ((uint32_t((c & 63) >> 3) ^ uint32_t(r & 7)) << 4) + uint32_t(c & 7) * 2u;
+    }
+    // layer of padded parameter j
+    __host__ __device__ int layer_of(int j) const {
+        int i = 0;
+        while (i < nh && j >= pad_off(i + 1)) ++i;
+        return i;
+    }
+};
 constexpr int kTileBytes = kTile * 128;               // 16 KB per 128x64 fp16 tile
 constexpr int kRecFloats = 16;                        // 64-B record
 

@@ -32,6 +32,7 @@ struct QueryArgs {
     const uint32_t* pix;
     const float* thr;
     float* image;
+    uint32_t nh;         // hidden layers (5; depth variants in the TMEM kernel only)
 };
 
 constexpr int kRecTileBytes = kTile * kRecFloats * 4;  // 8 KB of records per tile

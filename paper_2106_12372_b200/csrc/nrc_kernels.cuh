@@ -92,16 +92,15 @@ __global__ void __launch_bounds__(kRedThreads) nrc_adam_kernel(AdamArgs a) {
     adam_ema_update(j, g * a.inv_n, op, a.w, a.m, a.v, a.ema, a.wimg, a.eimg, a.bad_grads);
 }
 
-// fp32 padded array -> fp16 operand image at hidden width W (NetDims<W>).
+// fp32 padded array -> fp16 operand image at hidden width W and depth nh.
 template <int W>
-__global__ void nrc_image_w_kernel(const float* __restrict__ w, uint8_t* __restrict__ img) {
-    using D = NetDims<W>;
+__global__ void nrc_image_w_kernel(const float* __restrict__ w, uint8_t* __restrict__ img, int nh) {
+    const NetRt<W> D(nh);
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= D::kPadded) return;
-    int i = 0;
-    while (i < 5 && j >= D::pad_off(i + 1)) ++i;
-    const int rel = j - D::pad_off(i), r = rel / D::cols(i), c = rel % D::cols(i);
-    *reinterpret_cast<__half*>(img + D::img_byte(i, r, c)) = __float2half_rn(w[j]);
+    if (j >= D.padded()) return;
+    const int i = D.layer_of(j);
+    const int rel = j - D.pad_off(i), r = rel / D.cols(i), c = rel % D.cols(i);
+    *reinterpret_cast<__half*>(img + D.img_byte(i, r, c)) = __float2half_rn(w[j]);
 }
 
 // Sum the per-CTA partials in fixed order into a logical-layout gradient

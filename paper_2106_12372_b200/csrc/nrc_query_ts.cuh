@@ -33,6 +33,11 @@ template <int G, int S, int W = 64>
 __host__ __device__ constexpr int query_ts_smem_bytes() {
     return 1024 + NetDims<W>::kImg + G * kRecTileBytes + 8 * (1 + (S + 1) * G) + 16;
 }
+// with nh hidden layers (depth variants)
+template <int G, int S, int W = 64>
+__host__ __device__ int query_ts_smem_bytes_nh(int nh) {
+    return 1024 + NetRt<W>(nh).img() + G * kRecTileBytes + 8 * (1 + (S + 1) * G) + 16;
+}
 
 // One layer's K chain (K/16 MMAs, A in TMEM at a + 8 k, B K-major blocks of
 // 64: b0 for k < 4, b1 for k >= 4), then a commit.  Elected lane only.
@@ -62,7 +67,8 @@ __device__ __forceinline__ void umma_ta_chain_commit(uint32_t d, uint32_t a, uin
 template <int G, int S, int W = 64, bool EXACT = false>
 __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args) {
     static_assert(G * S <= ts_max_slots<W>(), "TMEM holds 512 columns");
-    using D = NetDims<W>;
+    const NetRt<W> D(int(args.nh));  // layer shapes / offsets at this depth
+    const int nh = D.nh, img = D.img();
     constexpr uint32_t kACols = (W > 64 ? W : 64) / 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
@@ -73,8 +79,8 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     const bool issuer_warp = wq == (g & 3u);
     const bool issuer = r == 32u * (g & 3u);
     uint8_t* sW = smem;
-    const float* sRec = reinterpret_cast<const float*>(smem + D::kImg + g * kRecTileBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + D::kImg + G * kRecTileBytes);
+    const float* sRec = reinterpret_cast<const float*>(smem + img + g * kRecTileBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + img + G * kRecTileBytes);
     uint64_t* wbar = &bars[0];
     uint64_t* mma_bar = &bars[1 + (S + 1) * g];  // [S]
     uint64_t* rec_bar = &bars[1 + (S + 1) * g + S];
@@ -93,8 +99,8 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (tid == 0) {
-        mbar_arrive_expect_tx(wbar, D::kImg);
-        bulk_g2s(sW, args.wimg, D::kImg, wbar);
+        mbar_arrive_expect_tx(wbar, uint32_t(img));
+        bulk_g2s(sW, args.wimg, uint32_t(img), wbar);
     }
 
     const uint64_t n = args.n;
@@ -123,16 +129,16 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     };
     // called by the whole issuer warp (converged)
     auto issue_layer = [&](int s, int L) {
-        const uint32_t wl = sW_a + uint32_t(D::img_off(L));
-        const uint32_t idesc = make_idesc(128, D::rows(L), 0, 0);
+        const uint32_t wl = sW_a + uint32_t(D.img_off(L));
+        const uint32_t idesc = make_idesc(128, D.rows(L), 0, 0);
         const uint32_t d = warp_uniform(d_col(s)), a = warp_uniform(a_col(s));
         const uint64_t b0 = warp_uniform(desc_kmajor(wl, 0));
-        const uint64_t b1 = warp_uniform(desc_kmajor(wl + uint32_t(D::rows(L)) * 128u, 0));
+        const uint64_t b1 = warp_uniform(desc_kmajor(wl + uint32_t(D.rows(L)) * 128u, 0));
         tc_fence_after();
         if (elect_one()) {
-            if (D::cols(L) == 32)
+            if (D.cols(L) == 32)
                 umma_ta_chain_commit<2>(d, a, b0, b1, idesc, &mma_bar[s]);
-            else if (D::cols(L) == 64)
+            else if (D.cols(L) == 64)
                 umma_ta_chain_commit<4>(d, a, b0, b1, idesc, &mma_bar[s]);
             else
                 umma_ta_chain_commit<8>(d, a, b0, b1, idesc, &mma_bar[s]);
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
             phase[s] ^= 1;
             tc_fence_after();
             const uint32_t t_d = d_col(s) + lane_off;
-            if (layer[s] < 5) {
+            if (layer[s] < nh) {
                 // h_{L+1} = relu(acc) -> fp16, written over h_L in the slot's TMEM A
 #pragma unroll
                 for (int part = 0; part < W / 32; ++part) {

@@ -51,6 +51,7 @@ struct TrainArgs {
     unsigned long long gbar_base;
     unsigned long long* gbarA;  // arrivals of CTAs whose W3..W5 partials are written (phase A)
     unsigned long long gbarA_base;
+    uint32_t nh;              // hidden layers (nrc_train_w_kernel; the fused kernel is built for 5)
 };
 
 // SMEM: weight image | h0..h5 stash (6 tiles) | 3 rotating gradient tiles |

@@ -38,6 +38,13 @@ struct TrainW {
     static constexpr int kKB = (W + 63) / 64;      // 64-wide blocks of a hidden activation
     static constexpr int kNW = W > 64 ? W : 64;    // dgrad N, wgrad N (j >= 1), accumulator columns
     static constexpr int kWBytes = kStream ? kKB * W * 128 : (D::kImg + 1023) / 1024 * 1024;
+    // depth variants: the same layout with nh hidden layers
+    static constexpr int kMaxNh = W == 32 ? 8 : W == 64 ? 7 : 5;  // SMEM: image + (nh+1) stash slots
+    __host__ __device__ static int w_bytes(int nh) {
+        return kStream ? kKB * W * 128 : (NetRt<W>(nh).img() + 1023) / 1024 * 1024;
+    }
+    __host__ __device__ static constexpr int stash_bytes(int nh) { return kTileBytes + nh * kKB * kTileBytes; }
+    __host__ __device__ static int smem_bytes(int nh) { return 1024 + w_bytes(nh) + stash_bytes(nh) + kTileBytes + 64; }
     static constexpr int kStashBytes = kTileBytes + 5 * kKB * kTileBytes;
     static constexpr int kSmemBytes = 1024 + kWBytes + kStashBytes + kTileBytes + 64;
     static constexpr uint32_t kTmemCols = 3 * kNW <= 256 ? 256u : 512u;
@@ -47,6 +54,7 @@ struct TrainW {
     __host__ __device__ static constexpr int wg_n(int j) { return j == 0 ? 64 : kNW; }
 };
 static_assert(TrainW<128>::kSmemBytes <= 232448 && TrainW<64>::kSmemBytes <= 232448, "227 KB of SMEM per CTA");
+// (smem_bytes(kMaxNh) <= 232448 for W = 32 / 64 / 128: 199,744 / 207,936 / 230,464 B)
 
 // SWIZZLE_128B descriptor with an explicit leading byte offset (the stride
 // between 64-wide MN blocks of an MN-major operand, SBO = 8 lines = 1024 B).
@@ -88,16 +96,18 @@ __device__ __forceinline__ void train_gather_row(const TrainArgs& a, uint32_t ro
 // EXACT: sin / Gaussian encoding primitives (NRC_EXACT_ENCODING, N4; width 64)
 template <int W, bool EXACT = false>
 __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
-    using D = NetDims<W>;
+    const NetRt<W> D(int(a.nh));  // layer shapes / offsets at this depth (nh hidden layers)
+    const int nh = D.nh;
     using T = TrainW<W>;
+    const int wbytes = T::w_bytes(nh), stash_bytes = T::stash_bytes(nh);
     NRC_WTRC(0);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     const uint32_t tid = threadIdx.x, r = tid, warp = tid >> 5, lane = tid & 31;
     const uint32_t sW_a = smem_u32(smem);
-    const uint32_t sH_a = sW_a + T::kWBytes;
-    const uint32_t sG6_a = sH_a + T::kStashBytes;  // dL/dy tile (columns 0..2 used)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::kWBytes + T::kStashBytes + kTileBytes);
+    const uint32_t sH_a = sW_a + uint32_t(wbytes);
+    const uint32_t sG6_a = sH_a + uint32_t(stash_bytes);  // dL/dy tile (columns 0..2 used)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + wbytes + stash_bytes + kTileBytes);
     uint64_t* wbar = &bars[0];
     uint64_t* mma_bar = &bars[1];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
@@ -127,13 +137,15 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     const uint32_t t_acc = tmem_base;
     auto t_g = [&](int j) -> uint32_t { return tmem_base + uint32_t(T::kNW) * (1u + uint32_t(j & 1)); };
     auto slot = [&](int i) -> uint32_t { return sH_a + uint32_t(T::slot_off(i)); };
-    auto wl = [&](int L) -> uint32_t { return T::kStream ? sW_a : sW_a + uint32_t(D::img_off(L)); };
+    auto wl = [&](int L) -> uint32_t { return T::kStream ? sW_a : sW_a + uint32_t(D.img_off(L)); };
+    // wgrad_j's M: the out-neuron rows (M = 64 holds rows 16 w + lane of warp w, lane < 16)
+    auto wg_m = [&](int j) { return (j < nh && W > 64) ? 128 : 64; };
 
     uint32_t phase = 0, w_phase = 0;
     // weight bytes of layer L (streamed) or the whole image (resident), issued by thread 0
     auto fetch = [&](int L) {
-        const uint32_t off = T::kStream ? uint32_t(D::img_off(L)) : 0u;
-        const uint32_t bytes = T::kStream ? uint32_t(D::img_off(L + 1) - D::img_off(L)) : uint32_t(D::kImg);
+        const uint32_t off = T::kStream ? uint32_t(D.img_off(L)) : 0u;
+        const uint32_t bytes = T::kStream ? uint32_t(D.img_off(L + 1) - D.img_off(L)) : uint32_t(D.img());
         mbar_arrive_expect_tx(wbar, bytes);
         for (uint32_t o = 0; o < bytes; o += 8192u) {
             const uint32_t b = bytes - o < 8192u ? bytes - o : 8192u;
@@ -157,20 +169,20 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     };
     // forward layer L (whole warp 0, converged; one elected lane issues + commits)
     auto issue_fwd = [&](int L) {
-        const uint32_t idesc = warp_uniform(make_idesc(128, D::rows(L), 0, 0));
+        const uint32_t idesc = warp_uniform(make_idesc(128, D.rows(L), 0, 0));
         const uint64_t a0 = warp_uniform(desc_kmajor(slot(L), 0));
         const uint64_t a1 = warp_uniform(desc_kmajor(slot(L) + kTileBytes, 0));
         const uint64_t b0 = warp_uniform(desc_kmajor(wl(L), 0));
-        const uint64_t b1 = warp_uniform(desc_kmajor(wl(L) + uint32_t(D::rows(L)) * 128u, 0));
+        const uint64_t b1 = warp_uniform(desc_kmajor(wl(L) + uint32_t(D.rows(L)) * 128u, 0));
         const uint32_t d = warp_uniform(t_acc);
         tc_fence_after();
         if (elect_one()) {
-            if (D::cols(L) == 32) {
+            if (D.cols(L) == 32) {
                 umma_f16(d, a0, b0, idesc, 0u);
                 umma_f16(d, a0 + 2, b0 + 2, idesc, 1u);
             } else {
                 umma_ss4<kKmajStep, kKmajStep>(d, a0, b0, idesc, 0u);
-                if (D::cols(L) == 128) umma_ss4<kKmajStep, kKmajStep>(d, a1, b1, idesc, 1u);
+                if (D.cols(L) == 128) umma_ss4<kKmajStep, kKmajStep>(d, a1, b1, idesc, 1u);
             }
             umma_commit(mma_bar);
         }
@@ -178,22 +190,22 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     };
     // round j of the backward pass: dgrad_j (j >= 1) and wgrad_j, one commit
     auto issue_bwd = [&](int j) {
-        const uint32_t gsrc = j == 5 ? sG6_a : slot(j + 1);  // g_{j+1}
+        const uint32_t gsrc = j == nh ? sG6_a : slot(j + 1);  // g_{j+1}
         const uint32_t d_acc = warp_uniform(t_acc), d_g = warp_uniform(t_g(j));
         // dgrad: delta_j = g_{j+1} W_j (K = rows(j) out-neurons)
         const uint32_t id_d = warp_uniform(make_idesc(128, T::kNW, 0, 1));
         const uint64_t da0 = warp_uniform(desc_kmajor(gsrc, 0));
         const uint64_t da1 = warp_uniform(desc_kmajor(gsrc + kTileBytes, 0));
-        const uint64_t db = warp_uniform(desc_mn_lbo(wl(j), uint32_t(D::rows(j)) * 128u));
+        const uint64_t db = warp_uniform(desc_mn_lbo(wl(j), uint32_t(D.rows(j)) * 128u));
         // wgrad: G_j += g_{j+1}^T h_j (K = 128 rows)
-        const uint32_t id_w = warp_uniform(make_idesc(T::wg_m(j), T::wg_n(j), 1, 1));
+        const uint32_t id_w = warp_uniform(make_idesc(wg_m(j), T::wg_n(j), 1, 1));
         const uint64_t wa = warp_uniform(desc_mn_lbo(gsrc, kTileBytes));
         const uint64_t wb = warp_uniform(desc_mn_lbo(slot(j), kTileBytes));
         tc_fence_after();
         if (elect_one()) {
             if (j >= 1) {
-                if (j == 5) {
-                    umma_f16(d_acc, da0, db, id_d, 0u);  // K = 16 (W5 padded rows)
+                if (j == nh) {
+                    umma_f16(d_acc, da0, db, id_d, 0u);  // K = 16 (output layer, padded rows)
                 } else if (W == 32) {
                     umma_f16(d_acc, da0, db, id_d, 0u);
                     umma_f16(d_acc, da0 + kKmajStep, db + kMNmajStep, id_d, 1u);
@@ -207,21 +219,21 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         }
         __syncwarp();
     };
-    float* part = a.partials + size_t(blockIdx.x) * D::kPadded;
+    float* part = a.partials + size_t(blockIdx.x) * D.padded();
     // drain G_j (TMEM) into this CTA's partial (plain store on the first tile, else add)
     auto flush_g = [&](int j, bool first) {
-        const int M = T::wg_m(j);
+        const int M = wg_m(j);
         const int o = M == 128 ? int(r) : int(warp) * 16 + int(lane);
-        const int rows_pad = j < 5 ? W : kOutPad;
+        const int rows_pad = j < nh ? W : kOutPad;
         const bool valid = (M == 128 || lane < 16) && o < rows_pad;
         constexpr int kMaxParts32 = (W > 64 ? W : 64) / 32;
 #pragma unroll
         for (int p = 0; p < kMaxParts32; ++p) {
-            if (32 * p >= D::cols(j)) break;
+            if (32 * p >= D.cols(j)) break;
             uint32_t v[32];
             tmem_ld32(t_g(j) + lane_off + 32u * p, v);
             if (valid) {
-                float4* dst = reinterpret_cast<float4*>(part + D::pad_off(j) + o * D::cols(j) + 32 * p);
+                float4* dst = reinterpret_cast<float4*>(part + D.pad_off(j) + o * D.cols(j) + 32 * p);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     float4 x = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
@@ -280,15 +292,15 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         sync_rows();
         // ---------------- forward: h_{L+1} = relu(W_L h_L), y = W5 h5
 #pragma unroll 1
-        for (int L = 0; L < 6; ++L) {
+        for (int L = 0; L <= nh; ++L) {
             if (warp == 0) {
                 if (T::kStream || (L == 0 && first)) wwait();
                 issue_fwd(L);
             }
             mma_wait();
-            NRC_WTRC(8 + L);
-            if (T::kStream && L < 5 && tid == 0) fetch(L + 1);  // the buffer is free
-            if (L == 5) break;
+            if (nh == 5) NRC_WTRC(8 + L);
+            if (T::kStream && L < nh && tid == 0) fetch(L + 1);  // the buffer is free
+            if (L == nh) break;
 #pragma unroll
             for (int p = 0; p < W / 32; ++p) {
                 uint32_t v[32];
@@ -333,15 +345,15 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         // ---------------- backward: round j = dgrad_j + wgrad_j, then
         // G_{j+1} drains while they run; g_j overwrites h_j after both complete
 #pragma unroll 1
-        for (int j = 5; j >= 1; --j) {
+        for (int j = nh; j >= 1; --j) {
             if (warp == 0) {
-                if (T::kStream && j < 5) wwait();  // W_j (W5 is still resident from the forward)
+                if (T::kStream && j < nh) wwait();  // W_j (the output layer is still resident from the forward)
                 issue_bwd(j);
             }
-            if (j < 5) flush_g(j + 1, first);
-            NRC_WTRC(14 + 2 * (5 - j));
+            if (j < nh) flush_g(j + 1, first);
+            if (nh == 5) NRC_WTRC(14 + 2 * (5 - j));
             mma_wait();
-            NRC_WTRC(15 + 2 * (5 - j));
+            if (nh == 5) NRC_WTRC(15 + 2 * (5 - j));
             if (T::kStream && tid == 0) {
                 if (j > 1)
                     fetch(j - 1);
@@ -349,9 +361,9 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
                     fetch(0);  // the next tile's W0
             }
             mask_epilogue(j);
-            if (j >= 2) NRC_WTRC(24 + (5 - j));
+            if (nh == 5 && j >= 2) NRC_WTRC(24 + (5 - j));
             sync_rows();
-            if (j >= 2) NRC_WTRC(28 + (5 - j));
+            if (nh == 5 && j >= 2) NRC_WTRC(28 + (5 - j));
         }
         NRC_WTRC(4);
         if (warp == 0) issue_bwd(0);  // G_0 += g_1^T h_0 (no gradient w.r.t. the encoding)
@@ -416,6 +428,7 @@ struct AdamWArgs {
     float loss_scale;
     float* loss_out;
     long long* dbg;          // diagnostics: global-timer marks of blocks 0 and last at dbg[4088..4091]
+    int nh;                  // hidden layers (depth variants)
     // peer mode (nrc_train_frame_dp_peer): partial p of the reduction is the
     // tile-p partial at tile_part[p] (in its owner's arena, possibly a peer's),
     // loss partial p at tile_loss[p]; used when tile_part[0] != nullptr
@@ -429,8 +442,7 @@ struct AdamWArgs {
 // applies the update.
 template <int W>
 __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
-    using D = NetDims<W>;
-    static_assert(D::kPadded % 32 == 0, "32 parameters per block");
+    const NetRt<W> D(a.nh);  // kPadded(nh) is a multiple of 32 for every width
     __shared__ float sred[8][32];
     pdl_wait();  // launched as a programmatic dependent of the partials kernel
     pdl_trigger();
@@ -472,7 +484,7 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
             float x[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u)
-                x[u] = (p0 + 8 * u < a.np) ? __ldcg(src + size_t(p0 + 8 * u) * D::kPadded) : 0.0f;
+                x[u] = (p0 + 8 * u < a.np) ? __ldcg(src + size_t(p0 + 8 * u) * D.padded()) : 0.0f;
 #pragma unroll
             for (int u = 0; u < 16; ++u) s += x[u];
         }
@@ -483,7 +495,7 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
             for (int k = 0; k < 8; ++k) g += sred[k][lane];
         }
     } else {
-        g = j < D::kLogical ? a.grad_logical[j] : 0.0f;
+        g = j < D.logical() ? a.grad_logical[j] : 0.0f;
     }
     if (wp != 0) return;
     if (blockIdx.x == 0 && a.loss_out != nullptr) {
@@ -493,7 +505,7 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane == 0) *a.loss_out = s * a.loss_scale;
     }
-    if (a.grad_out != nullptr && j < D::kLogical) a.grad_out[j] = g;
+    if (a.grad_out != nullptr && j < D.logical()) a.grad_out[j] = g;
     if (!a.apply) return;
     g *= a.inv_n;
     if (!isfinite(g)) {  // non-finite gradient entries are zeroed and counted
@@ -508,10 +520,9 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
     a.v[j] = v;
     a.w[j] = w;
     a.ema[j] = e;
-    int i = 0;
-    while (i < 5 && j >= D::pad_off(i + 1)) ++i;
-    const int rel = j - D::pad_off(i), row = rel / D::cols(i), col = rel % D::cols(i);
-    const uint32_t off = D::img_byte(i, row, col);
+    const int i = D.layer_of(j);
+    const int rel = j - D.pad_off(i), row = rel / D.cols(i), col = rel % D.cols(i);
+    const uint32_t off = D.img_byte(i, row, col);
     *reinterpret_cast<__half*>(a.wimg + off) = __float2half_rn(w);
     *reinterpret_cast<__half*>(a.eimg + off) = __float2half_rn(e);
     if (trc) a.dbg[4089 + 2 * (blockIdx.x != 0)] = global_ns();

@@ -21,6 +21,20 @@ def offsets_w(hw):
     return [int(x) for x in np.concatenate([[0], np.cumsum(sizes)])]
 
 
+def offsets_d(hw, nh):
+    """Matrix offsets at hidden width hw with nh hidden layers (depth variants):
+    W0 hw x 64, W1..W_{nh-1} hw x hw, W_nh 3 x hw."""
+    sizes = [hw * 64] + [hw * hw] * (nh - 1) + [3 * hw]
+    return [int(x) for x in np.concatenate([[0], np.cumsum(sizes)])]
+
+
+def per_matrix_err_d(a, b, off):
+    """per_matrix_err over an arbitrary number of matrices (offsets `off`)."""
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return [float(np.max(np.abs(a[off[i]:off[i + 1]] - b[off[i]:off[i + 1]])) /
+                  max(np.max(np.abs(b[off[i]:off[i + 1]])), 1e-30)) for i in range(len(off) - 1)]
+
+
 def radiance_err(q_gpu, q_ref):
     q_gpu = np.asarray(q_gpu, np.float64); q_ref = np.asarray(q_ref, np.float64)
     return [float(np.max(np.abs(q_gpu[:, c] - q_ref[:, c])) / max(np.max(np.abs(q_ref[:, c])), 1e-30))
