@@ -120,7 +120,7 @@ WidthInfo width_info(int W, int nh) {
 }
 
 struct StateLayout {
-    size_t w, m, v, ema, wimg, eimg, partials, loss_part, counters, total;
+    size_t w, m, v, ema, wimg, eimg, partials, loss_part, counters, dp_tables, total;
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -147,6 +147,8 @@ StateLayout layout(int W, int nh) {
     // [0] non-finite gradients, [1] non-finite targets, [2]/[3] fused-kernel
     // grid barriers, [4] fused peer all-reduce hand-off, [5] its timeouts
     L.counters = take(sizeof(unsigned long long) * 8);
+    // nrc_train_frame_dp_peer: per step parity, kMaxDpTiles partial + loss pointers
+    L.dp_tables = take(sizeof(const float*) * 2 * 2 * kMaxDpTiles);
     L.total = o;
     return L;
 }
@@ -682,7 +684,7 @@ static AdamWArgs adam_w_args(nrc_handle* h) {
     return aa;
 }
 static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t st) {
-    const dim3 grid(unsigned(h->wi.padded / 32)), block(256);
+    const dim3 grid(unsigned((h->wi.padded / 32 + kAdamGroups - 1) / kAdamGroups)), block(256 * kAdamGroups);
     if (h->wi.W == 32)
         NRC_CUDA(h, launch_pdl(nrc_adam_w_kernel<32>, grid, block, 0, st, aa));
     else if (h->wi.W == 128)
@@ -997,6 +999,23 @@ nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const
     for (uint32_t p = 0; p < world; ++p)
         peers.ctr[p] = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(peer_state[p]) + h->L.counters) + 4;
     const size_t pad = size_t(h->wi.padded);
+    // reduction tables of both slot parities: [parity][partials | losses][tile]
+    const float** d_tab = reinterpret_cast<const float**>(h->state + h->L.dp_tables);
+    {
+        std::vector<const float*> tab(size_t(2) * 2 * kMaxDpTiles, nullptr);
+        for (uint32_t par = 0; par < 2; ++par)
+            for (uint32_t k = 0; k < world; ++k) {
+                const float* part = reinterpret_cast<const float*>(static_cast<uint8_t*>(peer_state[k]) + h->L.partials);
+                const float* loss = reinterpret_cast<const float*>(static_cast<uint8_t*>(peer_state[k]) + h->L.loss_part);
+                for (uint32_t t = t_lo(k); t < t_lo(k + 1); ++t) {
+                    const size_t slot = size_t(par) * kMaxDpTiles + (t - t_lo(k));
+                    tab[(par * 2 + 0) * kMaxDpTiles + t] = part + slot * pad;
+                    tab[(par * 2 + 1) * kMaxDpTiles + t] = loss + slot;
+                }
+            }
+        // pageable source: staged before the call returns, so `tab` may go
+        NRC_CUDA(h, cudaMemcpyAsync(d_tab, tab.data(), sizeof(const float*) * tab.size(), cudaMemcpyHostToDevice, st));
+    }
     uint32_t launches = 0;
     for (uint32_t j = 0; j < s_; ++j) {
         const uint32_t parity = uint32_t(h->dp_seq & 1u);
@@ -1020,15 +1039,8 @@ nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const
         // 3. reduce all T tile partials in tile order from their owners' arenas + Adam + EMA
         h->step += 1;
         AdamWArgs aa = adam_w_args(h);
-        for (uint32_t k = 0; k < world; ++k) {
-            const float* part = reinterpret_cast<const float*>(static_cast<uint8_t*>(peer_state[k]) + h->L.partials);
-            const float* loss = reinterpret_cast<const float*>(static_cast<uint8_t*>(peer_state[k]) + h->L.loss_part);
-            for (uint32_t t = t_lo(k); t < t_lo(k + 1); ++t) {
-                const size_t slot = size_t(parity) * kMaxDpTiles + (t - t_lo(k));
-                aa.tile_part[t] = part + slot * pad;
-                aa.tile_loss[t] = loss + slot;
-            }
-        }
+        aa.tile_part = d_tab + (parity * 2 + 0) * kMaxDpTiles;
+        aa.tile_loss = d_tab + (parity * 2 + 1) * kMaxDpTiles;
         aa.np = int(T);
         aa.nloss = int(T);
         aa.apply = 1;

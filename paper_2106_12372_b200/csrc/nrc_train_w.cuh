@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
 //   apply: Adam (R11) + EMA (Eq. 2, R12) on g * inv_n, writing
 //   the fp32 state and both fp16 operand images.
 constexpr int kMaxDpTiles = 128;  // tiles per step in the fused peer all-reduce path
+constexpr int kAdamGroups = 4;    // 32-parameter groups (256 threads each) per optimiser block
 // a peer's (or our own) partial, read at system scope, not cached on this SM
 __device__ __forceinline__ float ld_sys_f32(const float* p) {
     float v;
@@ -429,11 +430,13 @@ struct AdamWArgs {
     float* loss_out;
     long long* dbg;          // diagnostics: global-timer marks of blocks 0 and last at dbg[4088..4091]
     int nh;                  // hidden layers (depth variants)
-    // peer mode (nrc_train_frame_dp_peer): partial p of the reduction is the
-    // tile-p partial at tile_part[p] (in its owner's arena, possibly a peer's),
-    // loss partial p at tile_loss[p]; used when tile_part[0] != nullptr
-    const float* tile_part[kMaxDpTiles];
-    const float* tile_loss[kMaxDpTiles];
+    // peer mode (nrc_train_frame_dp_peer), if tile_part != nullptr: device
+    // tables of np pointers -- partial p of the reduction is the tile-p partial
+    // at tile_part[p] (in its owner's arena, possibly a peer's), loss partial p
+    // at tile_loss[p].  (Tables in device memory keep the kernel parameters
+    // small: a 2 KB parameter block measurably slowed every launch.)
+    const float* const* tile_part;
+    const float* const* tile_loss;
 };
 
 // grid = kPadded / 32 blocks of 256 threads: block b owns parameters
@@ -441,15 +444,23 @@ struct AdamWArgs {
 // flight), warp 0 adds the 8 warp sums in warp order (deterministic) and
 // applies the update.
 template <int W>
-__global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
+__global__ void __launch_bounds__(kAdamGroups * 256, 2) nrc_adam_w_kernel(AdamWArgs a) {
     const NetRt<W> D(a.nh);  // kPadded(nh) is a multiple of 32 for every width
-    __shared__ float sred[8][32];
+    __shared__ float sred_all[kAdamGroups][8][32];
     pdl_wait();  // launched as a programmatic dependent of the partials kernel
     pdl_trigger();
     const bool trc = a.dbg != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x + 1 == gridDim.x);
+    // (trace: group 0 of the first / last block)
     if (trc) a.dbg[4088 + 2 * (blockIdx.x != 0)] = global_ns();
-    const int lane = int(threadIdx.x & 31), wp = int(threadIdx.x >> 5);
-    const int j = int(blockIdx.x) * 32 + lane;
+    // kAdamGroups independent 256-thread groups per block (fewer, larger
+    // blocks: block dispatch, not the work, bounded the 672-block launch on
+    // some boxes); group q owns parameters 32 (kAdamGroups block + q) + lane
+    const int q = int(threadIdx.x >> 8), lt = int(threadIdx.x & 255);
+    const int lane = lt & 31, wp = lt >> 5;
+    const int grp = int(blockIdx.x) * kAdamGroups + q;
+    const bool live = grp * 32 < D.padded();
+    const int j = live ? grp * 32 + lane : lane;  // dead groups read valid addresses, write nothing
+    float (&sred)[8][32] = sred_all[q];
     float g = 0.0f;
     // warp 0's optimiser state, loaded under the partial loads (one L2 round trip)
     float m = 0.0f, v = 0.0f, w = 0.0f, e = 0.0f;
@@ -457,7 +468,7 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
         m = ld_global_f32(a.m + j), v = ld_global_f32(a.v + j);
         w = ld_global_f32(a.w + j), e = ld_global_f32(a.ema + j);
     }
-    if (a.tile_part[0] != nullptr) {
+    if (a.tile_part != nullptr) {
         // fused all-reduce: partial p read from its owner's arena (NVLink loads
         // for peers), the same order as the local sum below
         const int pidx = j;
@@ -497,10 +508,10 @@ __global__ void __launch_bounds__(256) nrc_adam_w_kernel(AdamWArgs a) {
     } else {
         g = j < D.logical() ? a.grad_logical[j] : 0.0f;
     }
-    if (wp != 0) return;
-    if (blockIdx.x == 0 && a.loss_out != nullptr) {
+    if (wp != 0 || !live) return;
+    if (blockIdx.x == 0 && q == 0 && a.loss_out != nullptr) {
         float s = 0.0f;
-        for (int p = lane; p < a.nloss; p += 32) s += a.tile_part[0] != nullptr ? ld_sys_f32(a.tile_loss[p]) : a.loss_part[p];
+        for (int p = lane; p < a.nloss; p += 32) s += a.tile_part != nullptr ? ld_sys_f32(a.tile_loss[p]) : a.loss_part[p];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane == 0) *a.loss_out = s * a.loss_scale;
