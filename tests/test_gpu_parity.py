@@ -305,14 +305,17 @@ def test_init_matches_oracle_init(nrc, orc):
         np.testing.assert_array_equal(c.get_params("ema"), orc.init_weights(seed))
 
 
-def test_frame_host_equals_device_calls(nrc):
+@pytest.mark.parametrize("hw,nh", [(64, 5), (128, 3), (32, 8)])
+def test_frame_host_equals_device_calls(nrc, hw, nh):
     """nrc_frame_host (pinned host buffers, chunked copies overlapped with the
     query) gives the same bits as nrc_query + nrc_train_frame on device data,
-    over two consecutive frames (scratch and event reuse)."""
+    over two consecutive frames (scratch and event reuse) -- at the paper's
+    network and at a width / depth variant."""
     nq, s, l = 600_001, 4, 2048
     q = nrc_inputs.records(nq, seed=61)
     tr, tg = nrc_inputs.train_frame(4, n=s * l)
-    a, b = nrc.RadianceCache(), nrc.RadianceCache()
+    cfg = nrc.Config(hidden_width=hw, n_hidden_layers=nh)
+    a, b = nrc.RadianceCache(cfg), nrc.RadianceCache(cfg)
     hq = torch.from_numpy(q).pin_memory()
     ht, htg = torch.from_numpy(tr).pin_memory(), torch.from_numpy(tg).pin_memory()
     hrgb = torch.empty((nq, 3), dtype=torch.float32).pin_memory()
