@@ -63,27 +63,27 @@ static_assert(NetDims<64>::kPadded == kParamPadded && NetDims<64>::kImg == kImgB
 template <int W>
 struct NetRt {
     int nh;
-    __host__ __device__ explicit NetRt(int nh_) : nh(nh_) {}
-    __host__ __device__ int rows(int i) const { return i < nh ? W : kOutPad; }
+    __host__ __device__ constexpr explicit NetRt(int nh_) : nh(nh_) {}
+    __host__ __device__ constexpr int rows(int i) const { return i < nh ? W : kOutPad; }
     __host__ __device__ static constexpr int cols(int i) { return i == 0 ? 64 : W; }
     __host__ __device__ static constexpr int kblocks(int i) { return (cols(i) + 63) / 64; }
-    __host__ __device__ int pad_off(int i) const {
+    __host__ __device__ constexpr int pad_off(int i) const {
         return i == 0 ? 0 : i <= nh ? 64 * W + (i - 1) * W * W : 64 * W + (nh - 1) * W * W + kOutPad * W;
     }
-    __host__ __device__ int img_off(int i) const {
+    __host__ __device__ constexpr int img_off(int i) const {
         return i == 0 ? 0
                       : i <= nh ? W * 128 + (i - 1) * ((W + 63) / 64) * W * 128
                                 : W * 128 + (nh - 1) * ((W + 63) / 64) * W * 128 + ((W + 63) / 64) * kOutPad * 128;
     }
-    __host__ __device__ int padded() const { return pad_off(nh + 1); }
-    __host__ __device__ int logical() const { return 64 * W + (nh - 1) * W * W + 3 * W; }
-    __host__ __device__ int img() const { return img_off(nh + 1); }
-    __host__ __device__ uint32_t img_byte(int i, int r, int c) const {
+    __host__ __device__ constexpr int padded() const { return pad_off(nh + 1); }
+    __host__ __device__ constexpr int logical() const { return 64 * W + (nh - 1) * W * W + 3 * W; }
+    __host__ __device__ constexpr int img() const { return img_off(nh + 1); }
+    __host__ __device__ constexpr uint32_t img_byte(int i, int r, int c) const {
         return uint32_t(img_off(i) + (c >> 6) * rows(i) * 128 + r * 128) +
                ((uint32_t((c & 63) >> 3) ^ uint32_t(r & 7)) << 4) + uint32_t(c & 7) * 2u;
     }
     // layer of padded parameter j
-    __host__ __device__ int layer_of(int j) const {
+    __host__ __device__ constexpr int layer_of(int j) const {
         int i = 0;
         while (i < nh && j >= pad_off(i + 1)) ++i;
         return i;

@@ -33,28 +33,27 @@ namespace nrc {
 
 template <int W>
 struct TrainW {
-    using D = NetDims<W>;
     static constexpr bool kStream = W > 64;        // per-layer weight streaming
     static constexpr int kKB = (W + 63) / 64;      // 64-wide blocks of a hidden activation
     static constexpr int kNW = W > 64 ? W : 64;    // dgrad N, wgrad N (j >= 1), accumulator columns
-    static constexpr int kWBytes = kStream ? kKB * W * 128 : (D::kImg + 1023) / 1024 * 1024;
-    // depth variants: the same layout with nh hidden layers
-    static constexpr int kMaxNh = W == 32 ? 8 : W == 64 ? 7 : 5;  // SMEM: image + (nh+1) stash slots
-    __host__ __device__ static int w_bytes(int nh) {
+    // depth variants: nh hidden layers, limited by the shared memory
+    // of image + (nh + 1) stash slots + the dL/dy tile
+    static constexpr int kMaxNh = W == 32 ? 8 : W == 64 ? 7 : 5;
+    __host__ __device__ static constexpr int w_bytes(int nh) {
         return kStream ? kKB * W * 128 : (NetRt<W>(nh).img() + 1023) / 1024 * 1024;
     }
     __host__ __device__ static constexpr int stash_bytes(int nh) { return kTileBytes + nh * kKB * kTileBytes; }
-    __host__ __device__ static int smem_bytes(int nh) { return 1024 + w_bytes(nh) + stash_bytes(nh) + kTileBytes + 64; }
-    static constexpr int kStashBytes = kTileBytes + 5 * kKB * kTileBytes;
-    static constexpr int kSmemBytes = 1024 + kWBytes + kStashBytes + kTileBytes + 64;
+    __host__ __device__ static constexpr int smem_bytes(int nh) {
+        return 1024 + w_bytes(nh) + stash_bytes(nh) + kTileBytes + 64;
+    }
     static constexpr uint32_t kTmemCols = 3 * kNW <= 256 ? 256u : 512u;
     __host__ __device__ static constexpr int slot_off(int i) { return i == 0 ? 0 : kTileBytes + (i - 1) * kKB * kTileBytes; }
-    // wgrad_j's M: the out-neuron rows (M = 64 holds rows 16 w + lane of warp w, lane < 16)
-    __host__ __device__ static constexpr int wg_m(int j) { return (j < 5 && W > 64) ? 128 : 64; }
     __host__ __device__ static constexpr int wg_n(int j) { return j == 0 ? 64 : kNW; }
 };
-static_assert(TrainW<128>::kSmemBytes <= 232448 && TrainW<64>::kSmemBytes <= 232448, "227 KB of SMEM per CTA");
-// (smem_bytes(kMaxNh) <= 232448 for W = 32 / 64 / 128: 199,744 / 207,936 / 230,464 B)
+static_assert(TrainW<32>::smem_bytes(TrainW<32>::kMaxNh) <= 232448 &&
+                  TrainW<64>::smem_bytes(TrainW<64>::kMaxNh) <= 232448 &&
+                  TrainW<128>::smem_bytes(TrainW<128>::kMaxNh) <= 232448,
+              "227 KB of SMEM per CTA at the deepest supported network");
 
 // SWIZZLE_128B descriptor with an explicit leading byte offset (the stride
 // between 64-wide MN blocks of an MN-major operand, SBO = 8 lines = 1024 B).
