@@ -383,7 +383,11 @@ def run_nrc(args):
                      "traffic_source": traffic_src,
                      "algorithmic_bytes": BYTES_QUERY * nq_local,
                      "peak_source": f"{peak_src} bf16 dense burst (fp16 same rate)",
-                     "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_local} queries"},
+                     "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_local} queries",
+                     # the same against the 2.25 PF dense fp16 spec, and the
+                     # kernel's HBM fraction (algorithmic bytes / time / HBM peak)
+                     "frac_vs_spec_2250": achieved / 2250.0,
+                     "hbm_frac": BYTES_QUERY * nq_local / (q_ms * 1e-3) / 1e9 / peak_bw},
         "clocks": clk.summary(),
     }
     if e2e:
