@@ -86,3 +86,25 @@ def test_frame_scratch_bytes(libnrc):
     assert libnrc.nrc_frame_scratch_bytes(0, 0) >= 0
     nb = libnrc.nrc_frame_scratch_bytes(2073600, 65536)
     assert nb >= 2073600 * (64 + 12) + 65536 * 76
+
+
+@pytest.mark.parametrize("hw,nh,ok", [(64, 5, True), (64, 1, True), (64, 7, True), (64, 8, False), (64, 0, False),
+                                      (32, 8, True), (32, 9, False), (128, 5, True), (128, 6, False)])
+def test_state_bytes_depth_and_width(libnrc, hw, nh, ok):
+    """Host-side sizing of the state arena for the width / depth variants
+    (SURVEY C4, N4): the arena holds the four fp32 parameter arrays of the
+    padded layout (64 W + (n-1) W^2 + 16 W floats), two fp16 operand images
+    and 256 per-CTA fp32 gradient partials; unsupported depths give 0."""
+    from paper_2106_12372_b200 import _lib
+    c = _lib.NrcConfig(); libnrc.nrc_default_config(ctypes.byref(c))
+    c.hidden_width, c.n_hidden_layers = hw, nh
+    nb = libnrc.nrc_state_bytes(ctypes.byref(c))
+    if not ok:
+        assert nb == 0
+        return
+    padded = 64 * hw + (nh - 1) * hw * hw + 16 * hw
+    assert nb >= 4 * 4 * padded + 256 * 4 * padded
+    # one more hidden layer adds W^2 floats to every per-parameter array
+    if nh > 1:
+        c.n_hidden_layers = nh - 1
+        assert libnrc.nrc_state_bytes(ctypes.byref(c)) < nb
