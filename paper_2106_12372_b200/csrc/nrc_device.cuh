@@ -358,14 +358,15 @@ struct EncodeParams {
 };
 
 // quartic(x) = 15/16 (1 - x^2)^2 on |x| <= 1, else 0: clamping
-// 1 - x^2 at 0 gives the compact support without a compare.
+// 1 - x^2 at 0 gives the compact support without a compare; 1 - x^2 <= 1, so
+// the clamp is a saturate folded into the FFMA (FFMA.SAT, same value).
 __device__ __forceinline__ float quartic_f(float x) {
-    const float t = fmaxf(fmaf(-x, x, 1.0f), 0.0f);
+    const float t = __saturatef(fmaf(-x, x, 1.0f));
     return (0.9375f * t) * t;
 }
 // One-blob, k = 4, centres (i + 1/2)/4, width 1/4, clamp to [0,1] (R6).
 __device__ __forceinline__ void one_blob4(float s, float* o) {
-    s = fminf(fmaxf(s, 0.0f), 1.0f);
+    s = __saturatef(s);
     float x = 4.0f * s;
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[i] = quartic_f(x - (float(i) + 0.5f));
