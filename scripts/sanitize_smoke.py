@@ -26,10 +26,12 @@ i32 = lambda x: torch.from_numpy(x.astype(np.int32)).cuda()
 t = c.self_training_targets(i32(first), i32(length), i32(flags), dev(vert), dev(trec))
 img = torch.zeros((1000, 3), device="cuda")
 c.query_accumulate(dev(recs), i32(np.arange(1000)), dev(np.ones((1000, 3), np.float32)), img)
-for hw in (32, 128):  # width-ablation training (streamed weights at 128)
-    cw = nrc.RadianceCache(nrc.Config(hidden_width=hw))
+for hw, nh in ((32, 5), (128, 5), (64, 2), (32, 8)):  # width / depth variants (streamed weights at 128)
+    cw = nrc.RadianceCache(nrc.Config(hidden_width=hw, n_hidden_layers=nh))
     cw.train_frame(dev(tr), dev(tg), 2, 300, 5)
     cw.query(dev(recs))
+cd = nrc.RadianceCache()  # fused peer all-reduce path at world 1 (hand-off kernel, table-driven optimiser)
+cd.train_frame_dp_peer(dev(tr), dev(tg), 2, 1024, 7, 0, 1, [cd.state_ptr])
 if os.environ.get("NRC_SANITIZE_FUSED", "1") == "1":  # the grid-barrier kernel (not under racecheck)
     os.environ["NRC_TRAIN_FUSED"] = "1"
     cf = nrc.RadianceCache()
