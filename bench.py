@@ -309,6 +309,8 @@ def run_nrc(args):
 
     torch.cuda.synchronize()
     barrier()  # every rank's frame buffers are on the device (peer mode reads them remotely)
+    if world > 1:
+        dpf.verify_replicas()  # the same seeded init on every rank
     for i in range(args.warmup):
         frame(i)
     torch.cuda.synchronize()
@@ -330,6 +332,9 @@ def run_nrc(args):
         torch.cuda.synchronize()
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in ev]
+    replicas = None
+    if world > 1:  # bitwise-identical replicas after the timed frames (outside the timing)
+        replicas = "identical crc32 %08x" % dpf.verify_replicas()
     ms = float(np.mean(step_ms))
     pct = [float(x) for x in np.percentile(step_ms, [10, 50, 90])]  # this rank's step distribution
     q_ms = float(np.mean(qt))
@@ -390,6 +395,8 @@ def run_nrc(args):
                      "hbm_frac": BYTES_QUERY * nq_local / (q_ms * 1e-3) / 1e9 / peak_bw},
         "clocks": clk.summary(),
     }
+    if replicas:
+        line["replicas"] = replicas
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and not args.no_cpu_baseline:

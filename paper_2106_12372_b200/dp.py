@@ -59,6 +59,25 @@ class DataParallelFrame:
         self.loss_sum = self.buf[NPARAM:]
         self.last_launch_count = 0
 
+    def replica_checksum(self) -> int:
+        """CRC32 of this rank's fp32 training and EMA parameters (host copy)."""
+        import zlib
+        w = self.cache.get_params("train")
+        e = self.cache.get_params("ema")
+        return zlib.crc32(w.tobytes() + e.tobytes())
+
+    def verify_replicas(self) -> int:
+        """every rank holds a bitwise-identical replica (same seeded
+        init, identical reduced gradients or identical gathered data, the same
+        deterministic kernels).  Gathers every rank's checksum and raises if
+        any differs; returns the common checksum."""
+        mine = self.replica_checksum()
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=self.group)
+        if any(c != mine for c in everyone):
+            raise RuntimeError(f"replicas diverged: checksums {everyone}")
+        return mine
+
     def query_rows(self, n: int) -> Tuple[int, int]:
         return shard(n, self.rank, self.world)
 

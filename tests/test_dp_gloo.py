@@ -76,6 +76,9 @@ class OracleShard:
         out.copy_(torch.from_numpy(self.oc.query(records.numpy())))
         return out
 
+    def get_params(self, which="train"):
+        return (self.oc.w if which == "train" else self.oc.wbar).astype(np.float32)
+
 
 N_TOTAL, S, L, SEED = 3 * 1001 + 5, 3, 1001, 77
 
@@ -106,8 +109,10 @@ def _worker_replicated(rank, world, port, out_dir, n_total):
         shard_cache = OracleShard(seed=5)
         frame = dp.DataParallelFrame(shard_cache, dtype=torch.float64)
         losses = torch.zeros(S, dtype=torch.float64)
+        frame.verify_replicas()  # identical seeded init on every rank
         frame.train_frame_replicated(torch.from_numpy(recs[lo:hi].copy()), torch.from_numpy(tgts[lo:hi].copy()),
                                      S, L, SEED, losses)
+        frame.verify_replicas()  # and bitwise identical after the replicated frame
         np.savez(os.path.join(out_dir, f"rep{rank}.npz"), w=shard_cache.oc.w, losses=losses.numpy())
     finally:
         dist.destroy_process_group()
@@ -207,3 +212,25 @@ def test_allreduce_peer_arena_exchange(tmp_path):
         for (s, l, seed, rank, w, peers), want_seed in zip(calls, (1, 2)):
             assert (s, l, seed, rank, w) == (2, 4, want_seed, r, world)
             assert peers == [0x10000 * (k + 1) + (0 if k == r else 1) for k in range(world)]
+
+
+def _worker_diverged(rank, world, port, out_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        frame = dp.DataParallelFrame(OracleShard(seed=5 + rank))  # different init on each rank
+        try:
+            frame.verify_replicas()
+            raised = False
+        except RuntimeError:
+            raised = True
+        np.save(os.path.join(out_dir, f"div{rank}.npy"), np.array([raised]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_verify_replicas_detects_divergence(tmp_path):
+    """Negative control: replicas with different initial weights are reported."""
+    world = 2
+    mp.spawn(_worker_diverged, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert bool(np.load(tmp_path / f"div{r}.npy")[0])
