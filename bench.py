@@ -10,9 +10,11 @@ forward / relative-L2 / backward step followed by Adam + EMA.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nrc|reference]
 
 N > 1 (launched with torch.distributed.run, one rank per GPU, NCCL): the same
-frame is split across ranks -- query rows sharded with no communication;
-training either replicated after one all-gather of the frame's records
-(--train-mode replicated, the default) or data-parallel (--train-mode dp:
+frame is split across ranks -- by function by default (--train-mode
+dedicated: rank 0 trains, ranks 1..N-1 shard the query rows, then the new
+query image is broadcast), or query rows sharded over all ranks with the
+training replicated after one all-gather of the frame's records
+(--train-mode replicated) or data-parallel (--train-mode dp:
 each rank takes l/N rows of every batch, one NCCL all-reduce of the gradient
 per step, identical Adam on every rank; --train-mode allreduce-peer: the same
 split with the all-reduce fused into the optimiser kernel over peer memory;
@@ -253,7 +255,11 @@ def run_nrc(args):
             dist.barrier()
 
     # ---- inputs (synthetic, resident in HBM before timing)
-    q0, q1 = nrc.shard(N_QUERY, rank, world)
+    dedicated = world > 1 and args.train_mode == "dedicated"
+    if dedicated:  # rank 0 trains, ranks 1..N-1 split the query rows
+        q0, q1 = (0, 0) if rank == 0 else nrc.shard(N_QUERY, rank - 1, world - 1)
+    else:
+        q0, q1 = nrc.shard(N_QUERY, rank, world)
     recs_q_all = nrc_inputs.records(N_QUERY, seed=nrc_inputs.SEED_QUERY)
     recs_q = torch.from_numpy(recs_q_all[q0:q1].copy()).to(dev)
     nq_local = q1 - q0
@@ -276,6 +282,21 @@ def run_nrc(args):
         """One 1080p frame: query (EMA weights of the previous frame) + training."""
         d_r, d_t, _, _ = frames[fi % 2]
         launches = 0
+        if dedicated:
+            # rank 0: the frame's training; ranks >= 1: their query rows; then the
+            # new query image from rank 0 to all (SURVEY 8(e), N3)
+            if timed_query:
+                q_start.record(stream)
+            if rank > 0:
+                cache.query(recs_q, rgb)
+                launches += cache.last_launch_count
+            if timed_query:
+                q_end.record(stream)
+            if rank == 0:  # DataParallelFrame.frame_dedicated, with the query timed separately
+                cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
+                launches += cache.last_launch_count
+            dist.broadcast(cache.query_image(), src=0)
+            return launches
         if timed_query:
             q_start.record(stream)
         cache.query(recs_q, rgb)
@@ -310,7 +331,7 @@ def run_nrc(args):
     torch.cuda.synchronize()
     barrier()  # every rank's frame buffers are on the device (peer mode reads them remotely)
     if world > 1:
-        dpf.verify_replicas()  # the same seeded init on every rank
+        dpf.verify_replicas(image_only=dedicated)  # the same seeded init on every rank
     for i in range(args.warmup):
         frame(i)
     torch.cuda.synchronize()
@@ -334,7 +355,7 @@ def run_nrc(args):
     step_ms = [s.elapsed_time(e) for s, e in ev]
     replicas = None
     if world > 1:  # bitwise-identical replicas after the timed frames (outside the timing)
-        replicas = "identical crc32 %08x" % dpf.verify_replicas()
+        replicas = "identical crc32 %08x" % dpf.verify_replicas(image_only=dedicated)
     ms = float(np.mean(step_ms))
     pct = [float(x) for x in np.percentile(step_ms, [10, 50, 90])]  # this rank's step distribution
     q_ms = float(np.mean(qt))
@@ -372,7 +393,8 @@ def run_nrc(args):
 
     peak_tf, peak_bw, peak_src = peaks()
     traffic, traffic_src = ncu_traffic("nrc_query_ts_kernel")
-    q_flops = FLOP_QUERY * nq_local
+    nq_roof = (N_QUERY + world - 2) // (world - 1) if dedicated else nq_local  # the busiest query rank
+    q_flops = FLOP_QUERY * nq_roof
     achieved = q_flops / (q_ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -386,13 +408,13 @@ def run_nrc(args):
         "roofline": {"bound": "tensor", "kernel": "nrc_query_ts_kernel", "achieved": achieved, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic, "traffic_unit": "bytes/launch",
                      "traffic_source": traffic_src,
-                     "algorithmic_bytes": BYTES_QUERY * nq_local,
+                     "algorithmic_bytes": BYTES_QUERY * nq_roof,
                      "peak_source": f"{peak_src} bf16 dense burst (fp16 same rate)",
-                     "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_local} queries",
+                     "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_roof} queries",
                      # the same against the 2.25 PF dense fp16 spec, and the
                      # kernel's HBM fraction (algorithmic bytes / time / HBM peak)
                      "frac_vs_spec_2250": achieved / 2250.0,
-                     "hbm_frac": BYTES_QUERY * nq_local / (q_ms * 1e-3) / 1e9 / peak_bw},
+                     "hbm_frac": BYTES_QUERY * nq_roof / (q_ms * 1e-3) / 1e9 / peak_bw},
         "clocks": clk.summary(),
     }
     if replicas:
@@ -422,14 +444,17 @@ def main():
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
-    ap.add_argument("--train-mode", choices=["dp", "replicated", "peer", "allreduce-peer"], default="replicated",
-                    help="N > 1 training: one all-gather of the frame's records per frame and replicated "
-                         "training (replicated, SURVEY N3 (i); default: the training step is latency-bound, so "
-                         "fewer rows per GPU do not shorten it while per-step collectives add up), or "
+    ap.add_argument("--train-mode", choices=["dp", "replicated", "peer", "allreduce-peer", "dedicated"],
+                    default="dedicated",
+                    help="N > 1 training: split by function (dedicated, the default: rank 0 trains -- the "
+                         "latency-bound step fewer rows per GPU would not shorten -- while the other ranks "
+                         "query, then the new query image is broadcast), one all-gather of the frame's records "
+                         "per frame and replicated training (replicated, SURVEY N3 (i)), or "
                          "data-parallel with one all-reduce per step (dp, north_star's description), or the "
                          "all-gather fused into the training kernel over peer memory (peer), or data-parallel "
                          "with the gradient all-reduce fused into the optimiser over peer memory "
-                         "(allreduce-peer)")
+                         "(allreduce-peer), or split by function: rank 0 trains while the other ranks "
+                         "query, then the new query image is broadcast (dedicated)")
     args = ap.parse_args()
     if args.workload == "4k":
         global N_QUERY, METRIC, CONFIG_NAME

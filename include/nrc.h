@@ -280,6 +280,15 @@ nrc_status nrc_set_params(nrc_handle* h, nrc_param_set which, const float* h_in,
 /* Adam step count t and the non-finite counters.  Synchronous. */
 nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets);
 
+/* The fp16 operand image nrc_query reads (the EMA weights W-bar, or W with
+ * NRC_QUERY_RAW_WEIGHTS / ema_alpha = 0): its device address inside the
+ * state arena and its size in bytes.  Multi-GPU use: a rank that only
+ * queries receives it from the training rank (a broadcast of these bytes
+ * between identically configured caches), SURVEY 8(e) / N3.  The bytes are
+ * rewritten by every training call on this handle; a transfer must be
+ * ordered after them and before the next query that should see it. */
+nrc_status nrc_query_image(nrc_handle* h, void** d_image, size_t* bytes);
+
 /* 20,672 at width 64 (5*64*64 + 3*64; reading R1). */
 size_t nrc_param_count(const nrc_handle* h);
 

@@ -1185,6 +1185,16 @@ nrc_status nrc_set_params(nrc_handle* h, nrc_param_set which, const float* h_in,
     return NRC_OK;
 }
 
+nrc_status nrc_query_image(nrc_handle* h, void** d_image, size_t* bytes) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if (!d_image || !bytes) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query_image: NULL output");
+    const bool raw = (h->cfg.flags & NRC_QUERY_RAW_WEIGHTS) || h->cfg.ema_alpha == 0.0f;
+    *d_image = raw ? h->d_wimg() : h->d_eimg();
+    *bytes = size_t(h->wi.img);
+    return NRC_OK;
+}
+
 nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;

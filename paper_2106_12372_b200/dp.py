@@ -59,19 +59,51 @@ class DataParallelFrame:
         self.loss_sum = self.buf[NPARAM:]
         self.last_launch_count = 0
 
-    def replica_checksum(self) -> int:
-        """CRC32 of this rank's fp32 training and EMA parameters (host copy)."""
+    def replica_checksum(self, image_only: bool = False) -> int:
+        """CRC32 of this rank's fp32 training and EMA parameters (host copy), or
+        of the fp16 image the query reads (image_only: the state a query-only
+        rank of the dedicated mode keeps in sync)."""
         import zlib
+        if image_only:
+            return zlib.crc32(self.cache.query_image().cpu().numpy().tobytes())
         w = self.cache.get_params("train")
         e = self.cache.get_params("ema")
         return zlib.crc32(w.tobytes() + e.tobytes())
 
-    def verify_replicas(self) -> int:
+    def dedicated_query_rows(self, n: int) -> Tuple[int, int]:
+        """Dedicated mode: rank 0 trains and queries nothing; ranks 1..P-1 split
+        the n query rows."""
+        if self.rank == 0:
+            return 0, 0
+        return shard(n, self.rank - 1, self.world - 1)
+
+    def frame_dedicated(self, records_query_local: torch.Tensor, out: torch.Tensor, records: torch.Tensor,
+                        targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
+                        losses: Optional[torch.Tensor] = None, stream=None):
+        """One frame with the work split by function: rank 0
+        runs the whole frame's training (the latency-bound part, which more
+        GPUs cannot shorten), ranks 1..P-1 run the frame's query on their row
+        shards with the previous frame's W-bar -- the order of the paper's frame
+        (the query reads W-bar from before this frame's training) --
+        and then rank 0's new query image is broadcast to every rank.  Results
+        equal the single-GPU frame sequence bitwise (same kernels, same data)."""
+        if self.world < 2:
+            raise ValueError("the dedicated mode needs at least two ranks")
+        if self.rank == 0:
+            self.cache.train_frame(records, targets, s, l, shuffle_seed, losses)
+        elif records_query_local.shape[0] > 0:
+            self.cache.query(records_query_local, out, stream=stream)
+        launches = getattr(self.cache, "last_launch_count", 0)
+        dist.broadcast(self.cache.query_image(), src=0, group=self.group)
+        self.last_launch_count = launches
+        return out
+
+    def verify_replicas(self, image_only: bool = False) -> int:
         """every rank holds a bitwise-identical replica (same seeded
         init, identical reduced gradients or identical gathered data, the same
         deterministic kernels).  Gathers every rank's checksum and raises if
         any differs; returns the common checksum."""
-        mine = self.replica_checksum()
+        mine = self.replica_checksum(image_only)
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine, group=self.group)
         if any(c != mine for c in everyone):

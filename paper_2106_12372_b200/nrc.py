@@ -300,6 +300,14 @@ class RadianceCache:
                                                    _ptr(losses), _stream(stream)), "nrc_train_frame_dp_peer")
         return losses
 
+    def query_image(self) -> torch.Tensor:
+        """The fp16 operand image nrc_query reads, as a uint8 view of the state
+        arena (for broadcasting it from a training rank)."""
+        ptr, nb = ctypes.c_void_p(), ctypes.c_size_t()
+        self._check(self.L.nrc_query_image(self.h, ctypes.byref(ptr), ctypes.byref(nb)), "nrc_query_image")
+        off = int(ptr.value) - self.state.data_ptr()
+        return self.state[off:off + int(nb.value)]
+
     def dp_timeouts(self) -> int:
         c = ctypes.c_uint64()
         self._check(self.L.nrc_dp_timeouts(self.h, ctypes.byref(c)), "nrc_dp_timeouts")

@@ -79,6 +79,11 @@ class OracleShard:
     def get_params(self, which="train"):
         return (self.oc.w if which == "train" else self.oc.wbar).astype(np.float32)
 
+    def query_image(self):
+        """Stand-in for the query's fp16 image: a view of the fp64 W-bar the
+        stand-in query reads (so a broadcast into it changes later queries)."""
+        return torch.from_numpy(self.oc.wbar)
+
 
 N_TOTAL, S, L, SEED = 3 * 1001 + 5, 3, 1001, 77
 
@@ -234,3 +239,48 @@ def test_verify_replicas_detects_divergence(tmp_path):
     mp.spawn(_worker_diverged, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     for r in range(world):
         assert bool(np.load(tmp_path / f"div{r}.npy")[0])
+
+
+F_DED = 3
+
+
+def _worker_dedicated(rank, world, port, out_dir):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        shard_cache = OracleShard(seed=5)
+        frame = dp.DataParallelFrame(shard_cache, dtype=torch.float64)
+        q = nrc_inputs.records(500, seed=nrc_inputs.SEED_QUERY)
+        q0, q1 = frame.dedicated_query_rows(q.shape[0])
+        outs = []
+        for f in range(F_DED):
+            recs, tgts = nrc_inputs.train_frame(f, n=N_TOTAL, noise=0.3)
+            rgb = torch.zeros((q1 - q0, 3), dtype=torch.float64)
+            frame.frame_dedicated(torch.from_numpy(q[q0:q1].copy()), rgb, torch.from_numpy(recs),
+                                  torch.from_numpy(tgts), S, L, SEED + f)
+            outs.append(rgb.numpy().copy())
+        frame.verify_replicas(image_only=True)
+        np.savez(os.path.join(out_dir, f"ded{rank}.npz"), wbar=shard_cache.oc.wbar, q0=q0, q1=q1,
+                 rgb=np.stack(outs) if outs and outs[0].size else np.zeros((F_DED, 0, 3)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dedicated_frame_equals_sequential(tmp_path):
+    """Dedicated mode (rank 0 trains, the other ranks query with the previous
+    frame's W-bar, then W-bar is broadcast): the queries of every frame and the
+    final W-bar equal the single-process frame sequence (query, then train)."""
+    world = 3
+    mp.spawn(_worker_dedicated, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    res = [np.load(tmp_path / f"ded{r}.npz") for r in range(world)]
+    q = nrc_inputs.records(500, seed=nrc_inputs.SEED_QUERY)
+    ref = OracleShard(seed=5)
+    want = []
+    for f in range(F_DED):
+        want.append(ref.oc.query(q))
+        recs, tgts = nrc_inputs.train_frame(f, n=N_TOTAL, noise=0.3)
+        ref.train_frame(torch.from_numpy(recs), torch.from_numpy(tgts), S, L, SEED + f)
+    assert int(res[0]["q1"]) - int(res[0]["q0"]) == 0
+    got = np.concatenate([r["rgb"] for r in res[1:]], axis=1)
+    np.testing.assert_array_equal(got, np.stack(want))
+    for r in res:
+        np.testing.assert_array_equal(r["wbar"], ref.oc.wbar)
