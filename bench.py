@@ -256,7 +256,7 @@ def run_nrc(args):
 
     # ---- inputs (synthetic, resident in HBM before timing)
     dedicated = world > 1 and args.train_mode == "dedicated"
-    if dedicated:  # rank 0 trains, ranks 1..N-1 split the query rows
+    if dedicated:  # rank 0 trains, ranks 1..N-1 split the query rows (rank 0's share set after calibration)
         q0, q1 = (0, 0) if rank == 0 else nrc.shard(N_QUERY, rank - 1, world - 1)
     else:
         q0, q1 = nrc.shard(N_QUERY, rank, world)
@@ -287,7 +287,7 @@ def run_nrc(args):
             # new query image from rank 0 to all
             if timed_query:
                 q_start.record(stream)
-            if rank > 0:
+            if recs_q.shape[0] > 0:
                 cache.query(recs_q, rgb)
                 launches += cache.last_launch_count
             if timed_query:
@@ -336,6 +336,33 @@ def run_nrc(args):
         frame(i)
     torch.cuda.synchronize()
     barrier()
+    if dedicated:
+        # balance: rank 0's query share from the measured training time (rank 0)
+        # and query time (rank 1), decided on rank 0 and broadcast
+        def dev_ms(fn, reps=5):
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream)
+            for _ in range(reps):
+                fn()
+            b_ev.record(stream)
+            torch.cuda.synchronize()
+            return a_ev.elapsed_time(b_ev) / reps
+        d_r0, d_t0 = frames[0][0], frames[0][1]
+        mine = dev_ms(lambda: cache.train_frame(d_r0, d_t0, TRAIN_S, TRAIN_L, 999)) if rank == 0 else \
+            dev_ms(lambda: cache.query(recs_q, rgb)) * (world - 1)
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        share = [nrc.DataParallelFrame.dedicated_share0(got[1], got[0], world)]
+        dist.broadcast_object_list(share, src=0)
+        q0, q1 = dpf.dedicated_query_rows(N_QUERY, share[0])
+        recs_q = torch.from_numpy(recs_q_all[q0:q1].copy()).to(dev)
+        nq_local = q1 - q0
+        rgb = torch.empty((nq_local, 3), dtype=torch.float32, device=dev)
+        ded_share0 = share[0]
+        for i in range(3):
+            frame(i)
+        torch.cuda.synchronize()
+        barrier()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     qt = []
@@ -393,7 +420,11 @@ def run_nrc(args):
 
     peak_tf, peak_bw, peak_src = peaks()
     traffic, traffic_src = ncu_traffic("nrc_query_ts_kernel")
-    nq_roof = (N_QUERY + world - 2) // (world - 1) if dedicated else nq_local  # the busiest query rank
+    nq_roof = nq_local
+    if world > 1:  # the busiest query rank
+        t = torch.tensor([nq_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        nq_roof = int(t[0])
     q_flops = FLOP_QUERY * nq_roof
     achieved = q_flops / (q_ms * 1e-3) / 1e12
     line = {
@@ -419,6 +450,8 @@ def run_nrc(args):
     }
     if replicas:
         line["replicas"] = replicas
+    if dedicated:
+        line["config"]["dedicated_rank0_query_share"] = ded_share0
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and not args.no_cpu_baseline:

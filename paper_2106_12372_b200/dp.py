@@ -70,12 +70,25 @@ class DataParallelFrame:
         e = self.cache.get_params("ema")
         return zlib.crc32(w.tobytes() + e.tobytes())
 
-    def dedicated_query_rows(self, n: int) -> Tuple[int, int]:
-        """Dedicated mode: rank 0 trains and queries nothing; ranks 1..P-1 split
-        the n query rows."""
+    def dedicated_query_rows(self, n: int, share0: float = 0.0) -> Tuple[int, int]:
+        """Dedicated mode: rank 0 trains and queries the first round(share0 n)
+        rows (0 by default; a small share balances P = 2, where the single
+        query rank would otherwise wait longest); ranks 1..P-1 split the rest."""
+        n0 = int(round(min(max(share0, 0.0), 1.0) * n))
         if self.rank == 0:
-            return 0, 0
-        return shard(n, self.rank - 1, self.world - 1)
+            return 0, n0
+        lo, hi = shard(n - n0, self.rank - 1, self.world - 1)
+        return n0 + lo, n0 + hi
+
+    @staticmethod
+    def dedicated_share0(query_time_one_gpu: float, train_time: float, world: int) -> float:
+        """Rank 0's query share that equalises t_train + f T_q (rank 0) with
+        (1 - f) T_q / (P - 1) (the other ranks); 0 when the training alone is
+        the longer part (P >= 3 at the paper's sizes)."""
+        if world < 2 or query_time_one_gpu <= 0:
+            return 0.0
+        f = (query_time_one_gpu - (world - 1) * train_time) / (world * query_time_one_gpu)
+        return float(min(max(f, 0.0), 0.9))
 
     def frame_dedicated(self, records_query_local: torch.Tensor, out: torch.Tensor, records: torch.Tensor,
                         targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
@@ -89,11 +102,13 @@ class DataParallelFrame:
         equal the single-GPU frame sequence bitwise (same kernels, same data)."""
         if self.world < 2:
             raise ValueError("the dedicated mode needs at least two ranks")
+        launches = 0
+        if records_query_local.shape[0] > 0:  # the previous frame's W-bar
+            self.cache.query(records_query_local, out, stream=stream)
+            launches += getattr(self.cache, "last_launch_count", 0)
         if self.rank == 0:
             self.cache.train_frame(records, targets, s, l, shuffle_seed, losses)
-        elif records_query_local.shape[0] > 0:
-            self.cache.query(records_query_local, out, stream=stream)
-        launches = getattr(self.cache, "last_launch_count", 0)
+            launches += getattr(self.cache, "last_launch_count", 0)
         dist.broadcast(self.cache.query_image(), src=0, group=self.group)
         self.last_launch_count = launches
         return out

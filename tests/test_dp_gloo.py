@@ -244,13 +244,13 @@ def test_verify_replicas_detects_divergence(tmp_path):
 F_DED = 3
 
 
-def _worker_dedicated(rank, world, port, out_dir):
+def _worker_dedicated(rank, world, port, out_dir, share0=0.0):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         shard_cache = OracleShard(seed=5)
         frame = dp.DataParallelFrame(shard_cache, dtype=torch.float64)
         q = nrc_inputs.records(500, seed=nrc_inputs.SEED_QUERY)
-        q0, q1 = frame.dedicated_query_rows(q.shape[0])
+        q0, q1 = frame.dedicated_query_rows(q.shape[0], share0)
         outs = []
         for f in range(F_DED):
             recs, tgts = nrc_inputs.train_frame(f, n=N_TOTAL, noise=0.3)
@@ -265,12 +265,13 @@ def _worker_dedicated(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-def test_dedicated_frame_equals_sequential(tmp_path):
-    """Dedicated mode (rank 0 trains, the other ranks query with the previous
-    frame's W-bar, then W-bar is broadcast): the queries of every frame and the
-    final W-bar equal the single-process frame sequence (query, then train)."""
-    world = 3
-    mp.spawn(_worker_dedicated, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+@pytest.mark.parametrize("world,share0", [(3, 0.0), (2, 0.25)])
+def test_dedicated_frame_equals_sequential(tmp_path, world, share0):
+    """Dedicated mode (rank 0 trains -- after querying its share0 of the rows,
+    if any -- the other ranks query with the previous frame's W-bar, then W-bar
+    is broadcast): the queries of every frame and the final W-bar equal the
+    single-process frame sequence (query, then train)."""
+    mp.spawn(_worker_dedicated, args=(world, _free_port(), str(tmp_path), share0), nprocs=world, join=True)
     res = [np.load(tmp_path / f"ded{r}.npz") for r in range(world)]
     q = nrc_inputs.records(500, seed=nrc_inputs.SEED_QUERY)
     ref = OracleShard(seed=5)
@@ -279,8 +280,15 @@ def test_dedicated_frame_equals_sequential(tmp_path):
         want.append(ref.oc.query(q))
         recs, tgts = nrc_inputs.train_frame(f, n=N_TOTAL, noise=0.3)
         ref.train_frame(torch.from_numpy(recs), torch.from_numpy(tgts), S, L, SEED + f)
-    assert int(res[0]["q1"]) - int(res[0]["q0"]) == 0
-    got = np.concatenate([r["rgb"] for r in res[1:]], axis=1)
+    assert int(res[0]["q1"]) - int(res[0]["q0"]) == round(share0 * 500)
+    got = np.concatenate([r["rgb"] for r in res], axis=1)
     np.testing.assert_array_equal(got, np.stack(want))
     for r in res:
         np.testing.assert_array_equal(r["wbar"], ref.oc.wbar)
+
+
+def test_dedicated_share0_balances():
+    # P = 2: 80 us of training against a 105 us query -> rank 0 takes 11.9 %
+    assert dp.DataParallelFrame.dedicated_share0(105.0, 80.0, 2) == pytest.approx(25.0 / 210.0)
+    assert dp.DataParallelFrame.dedicated_share0(105.0, 80.0, 8) == 0.0   # training dominates
+    assert dp.DataParallelFrame.dedicated_share0(105.0, 0.0, 2) == pytest.approx(0.5)
