@@ -9,20 +9,19 @@ forward / relative-L2 / backward step followed by Adam + EMA.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nrc|reference]
 
-N > 1 (launched with torch.distributed.run, one rank per GPU, NCCL): the same
-frame is split across ranks -- by function by default (--train-mode
-dedicated: rank 0 trains, ranks 1..N-1 shard the query rows, then the new
-query image is broadcast), or query rows sharded over all ranks with the
-training replicated after one all-gather of the frame's records
-(--train-mode replicated) or data-parallel (--train-mode dp:
-each rank takes l/N rows of every batch, one NCCL all-reduce of the gradient
-per step, identical Adam on every rank; --train-mode allreduce-peer: the same
-split with the all-reduce fused into the optimiser kernel over peer memory;
---train-mode peer: the record all-gather fused into the training kernel) --
-strong scaling, max-over-ranks device time.
+N > 1 (launched with torch.distributed.run, one rank per GPU, NCCL):
+north_star's partition -- query rows sharded over the ranks with no
+communication, training data-parallel: each rank takes l/N rows of every
+shuffled batch, one NCCL all-reduce of [gradient | loss sum] per step,
+identical Adam on every rank (--train-mode dp, the default).  Variants
+(SURVEY 8(f) N3): --train-mode replicated (one all-gather of the frame's
+records, then replicated training) and --train-mode allreduce-peer (the
+gradient all-reduce fused into the optimiser kernel over peer memory).
+Max-over-ranks device time.
 
 --impl reference: the fp64 CPU oracle (oracle/, as it stands) on the host
-cores, timed on a bounded sample of the same frame and scaled to the frame.
+cores, timing whole frames (2,073,600 queries + 4 sequential 16,384-record
+train steps).
 """
 from __future__ import annotations
 
@@ -110,55 +109,44 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# ============================================================================ reference arm (oracle)
-def oracle_frame_estimate(q_sample: int, t_sample: int, reps: int = 1):
-    """Times the fp64 oracle on q_sample queries and one train step of
-    t_sample records; scales to one 1080p frame.  Returns (ms_frame, detail)."""
-    import nrc_inputs
-    import oracle
-    oracle.build()
-    recs_q = nrc_inputs.records(q_sample, seed=nrc_inputs.SEED_QUERY)
-    recs_t, tg = nrc_inputs.train_frame(0, n=t_sample)
-    oc = oracle.OracleCache()
-    tq = tt = 0.0
-    for _ in range(reps):
+def stats_ms(xs):
+    """median, mean and p10/p50/p90 of a list of per-step times (ms)."""
+    xs = [float(x) for x in xs]
+    p10, p50, p90 = (float(v) for v in np.percentile(xs, [10, 50, 90]))
+    return {"median": p50, "mean": float(np.mean(xs)), "p10": p10, "p50": p50, "p90": p90}
+
+
+# ============================================================================ the oracle (reference arm, cpu_baseline)
+class OracleFrame:
+    """The fp64 CPU oracle on the bench's frame: query of the frame's records
+    with W-bar, then s sequential train steps on the LCG-shuffled batches
+    (the same generator seeds as the CUDA arm).  frac < 1 times the first
+    frac of the queries and of every batch (a bounded sample) and scales the
+    two phases back to the frame."""
+
+    def __init__(self):
+        import nrc_inputs
+        import oracle
+        oracle.build()
+        self.oracle = oracle
+        self.recs_q = nrc_inputs.records(N_QUERY, seed=nrc_inputs.SEED_QUERY)
+        self.recs_t, self.tg = nrc_inputs.train_frame(0, n=N_TRAIN, noise=0.3)
+        a, c, m = oracle.lcg_params(N_TRAIN, 1000)
+        self.perm = oracle.lcg_permute(N_TRAIN, a, c, m).astype(np.int64)
+        self.oc = oracle.OracleCache()
+
+    def frame(self, frac: float = 1.0):
+        nq = max(1, int(round(N_QUERY * frac)))
+        lt = max(1, int(round(TRAIN_L * frac)))
         t0 = time.perf_counter()
-        oc.query(recs_q)
+        self.oc.query(self.recs_q[:nq])
         t1 = time.perf_counter()
-        oc.train_step(recs_t, tg)
+        for j in range(TRAIN_S):
+            idx = self.perm[j * TRAIN_L:j * TRAIN_L + lt]
+            self.oc.train_step(self.recs_t[idx], self.tg[idx])
         t2 = time.perf_counter()
-        tq += t1 - t0
-        tt += t2 - t1
-    tq /= reps
-    tt /= reps
-    ms = 1e3 * (tq / q_sample * N_QUERY + tt / t_sample * N_TRAIN)
-    sample = (f"{q_sample} queries + one {t_sample}-record train step per rep, scaled to 2,073,600 queries + "
-              f"65,536 train records")
-    return ms, sample, tq, tt
-
-
-def frame_config(world: int, train_mode: str = "dp") -> dict:
-    return {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
-            "parallelism": f"{train_mode}{world}" if world > 1 else "single",
-            "l2": "flushed (256 MB write) between timed steps",
-            "train_kernel": ("fused cooperative (NRC_TRAIN_FUSED=1)" if os.environ.get("NRC_TRAIN_FUSED", "0") != "0"
-                             else "per step: partials + reduce/Adam/EMA, PDL-chained")}
-
-
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch of `kernel` from the newest committed
-    ncu --set full capture summary (profiles/rNN_traffic.json), else None."""
-    import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
-    for f in reversed(files):
-        try:
-            with open(f) as fh:
-                t = json.load(fh)
-            if kernel in t:
-                return float(t[kernel]["traffic_bytes"]), os.path.relpath(f, ROOT)
-        except Exception:
-            continue
-    return None, None
+        tq, tt = (t1 - t0) / (nq / N_QUERY), (t2 - t1) / (lt / TRAIN_L)
+        return 1e3 * (tq + tt), 1e3 * tq, 1e3 * tt
 
 
 def omp_threads():
@@ -176,52 +164,84 @@ def cpu_model() -> str:
 
 
 def oracle_single_thread_ms():
-    """The oracle on one host thread (SURVEY 8(d) oracle timing): a 4096-query
-    + 512-record sample in a subprocess with OMP_NUM_THREADS=1, scaled to the
-    frame; None if it fails."""
-    code = ("import sys; sys.path.insert(0, %r); import bench; "
-            "print(bench.oracle_frame_estimate(4096, 512)[0])" % ROOT)
+    """The oracle on one host thread (SURVEY 8(d) oracle timing): a 1/256
+    sample of the frame (8,100 queries + 4 x 64-record steps) in a subprocess
+    with OMP_NUM_THREADS=1, scaled to the frame; None if it fails."""
+    code = ("import sys; sys.path.insert(0, %r); import bench; f = bench.OracleFrame(); "
+            "print(f.frame(1.0 / 256)[0])" % ROOT)
     try:
         out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, OMP_NUM_THREADS="1"),
-                             capture_output=True, text=True, timeout=300)
+                             capture_output=True, text=True, timeout=600)
         return float(out.stdout.strip().splitlines()[-1])
     except Exception:
         return None
+
+
+def frame_config(world: int, train_mode: str = "dp") -> dict:
+    return {"workload": CONFIG_NAME, "global_batch": N_QUERY, "train_records": N_TRAIN,
+            "parallelism": f"{train_mode}{world}" if world > 1 else "single",
+            "query_partition": "rows sharded over ranks, no communication" if world > 1 else "one GPU",
+            "l2": "flushed (256 MB write) between timed steps",
+            "train_kernel": "per step: partials + reduce/Adam/EMA, PDL-chained"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    # bounded samples: size each step so that warm-up + timed steps take about
-    # REF_BUDGET_S of host time in total, from the oracle's measured per-record cost
-    budget = float(os.environ.get("NRC_REF_BUDGET_S", "120"))
-    _, _, tq, tt = oracle_frame_estimate(4096, 512)  # warm-up (build, page-in) + calibration
-    per_step = budget / max(1, args.steps + args.warmup)
-    per_q, per_t = tq / 4096, tt / 512
-    scale = per_step / max(per_q * 32768 + per_t * 4096, 1e-9)
-    q_sample = int(min(32768, max(1024, 32768 * scale)))
-    t_sample = int(min(4096, max(256, 4096 * scale)))
-    times = []
-    for _ in range(args.warmup):
-        oracle_frame_estimate(q_sample, t_sample)
+    budget = float(os.environ.get("NRC_REF_BUDGET_S", "600"))
+    of = OracleFrame()
+    # one whole frame first (page-in + the cost estimate); it counts as warm-up
+    t0 = time.perf_counter()
+    of.frame()
+    est = time.perf_counter() - t0
+    frac = 1.0
+    if est * (args.steps + args.warmup) > budget:  # shrink to a bounded sample of every phase
+        frac = max(budget / (args.steps + args.warmup) / est, 1.0 / 512)
+    for _ in range(max(0, args.warmup - 1)):
+        of.frame(frac)
+    times, tq, tt = [], [], []
     for _ in range(args.steps):
-        ms, sample, _, _ = oracle_frame_estimate(q_sample, t_sample)
+        ms, q, t = of.frame(frac)
         times.append(ms)
-    ms = float(np.mean(times))
+        tq.append(q)
+        tt.append(t)
+    st = stats_ms(times)
+    ms = st["median"]
+    q_ms, t_ms = float(np.median(tq)), float(np.median(tt))
+    sample = ("whole frames: 2,073,600 queries + 4 sequential 16,384-record train steps per step" if frac == 1.0 else
+              f"{frac:.4f} of every phase per step (budget {budget:.0f} s), scaled to the frame")
     line = {
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong" if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (nrc_inputs seeded records)",
         "config": frame_config(args.gpus, args.train_mode),
-        "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
+        "ms_mean": st["mean"], "ms_p10_p50_p90": [st["p10"], st["p50"], st["p90"]],
+        "query_ms": q_ms, "train_ms": t_ms,
+        "queries_per_s": N_QUERY / (q_ms * 1e-3), "records_per_s": N_TRAIN / (t_ms * 1e-3),
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": omp_threads(), "kind": "oracle", "sample": sample,
                          "cpu_model": cpu_model()},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from the newest committed
+    ncu --set full capture summary (profiles/rNN_traffic.json), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for f in reversed(files):
+        try:
+            with open(f) as fh:
+                t = json.load(fh)
+            if kernel in t:
+                return float(t[kernel]["traffic_bytes"]), os.path.relpath(f, ROOT)
+        except Exception:
+            continue
+    return None, None
 
 
 # ============================================================================ CUDA arm
@@ -247,151 +267,104 @@ def run_nrc(args):
         if shared:
             dist.init_process_group("gloo")
         else:
+            # communicator-init log lines (rank / nranks per communicator) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    mode = args.train_mode
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     # ---- inputs (synthetic, resident in HBM before timing)
-    dedicated = world > 1 and args.train_mode == "dedicated"
-    if dedicated:  # rank 0 trains, ranks 1..N-1 split the query rows (rank 0's share set after calibration)
-        q0, q1 = (0, 0) if rank == 0 else nrc.shard(N_QUERY, rank - 1, world - 1)
-    else:
-        q0, q1 = nrc.shard(N_QUERY, rank, world)
+    q0, q1 = nrc.shard(N_QUERY, rank, world)
     recs_q_all = nrc_inputs.records(N_QUERY, seed=nrc_inputs.SEED_QUERY)
     recs_q = torch.from_numpy(recs_q_all[q0:q1].copy()).to(dev)
     nq_local = q1 - q0
+    t_counts = [b - a for a, b in (nrc.shard(N_TRAIN, r, world) for r in range(world))]
+    t0_, t1_ = nrc.shard(N_TRAIN, rank, world)
     frames = []
     for f in range(2):
         r, t = nrc_inputs.train_frame(f, n=N_TRAIN, noise=0.3)
-        frames.append((torch.from_numpy(r).to(dev), torch.from_numpy(t).to(dev), r, t))
+        frames.append((torch.from_numpy(r).to(dev), torch.from_numpy(t).to(dev), r, t,
+                       torch.from_numpy(r[t0_:t1_].copy()).to(dev), torch.from_numpy(t[t0_:t1_].copy()).to(dev)))
     rgb = torch.empty((nq_local, 3), dtype=torch.float32, device=dev)
     cache = nrc.RadianceCache(nrc.Config(max_batch=max(N_QUERY, N_TRAIN)), device=local)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
-
-    # data-parallel frame for world > 1 (query rows sharded, one all-reduce per train step)
     dpf = nrc.DataParallelFrame(cache, device=dev) if world > 1 else None
 
-    q_start = torch.cuda.Event(enable_timing=True)
-    q_end = torch.cuda.Event(enable_timing=True)
-
-    def frame(fi, timed_query=False):
-        """One 1080p frame: query (EMA weights of the previous frame) + training."""
-        d_r, d_t, _, _ = frames[fi % 2]
-        launches = 0
-        if dedicated:
-            # rank 0: the frame's training; ranks >= 1: their query rows; then the
-            # new query image from rank 0 to all (SURVEY 8(e), N3)
-            if timed_query:
-                q_start.record(stream)
-            if recs_q.shape[0] > 0:
-                cache.query(recs_q, rgb)
-                launches += cache.last_launch_count
-            if timed_query:
-                q_end.record(stream)
-            if rank == 0:  # DataParallelFrame.frame_dedicated, with the query timed separately
-                cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
-                launches += cache.last_launch_count
-            dist.broadcast(cache.query_image(), src=0)
-            return launches
-        if timed_query:
-            q_start.record(stream)
+    def frame(fi, ev=None):
+        """One frame: query (EMA weights of the previous frame) + training.
+        ev = (start, query end, train end) events recorded on the stream."""
+        d_r, d_t, _, _, d_rl, d_tl = frames[fi % 2]
+        seed = 1000 + fi % 2
+        if ev:
+            ev[0].record(stream)
         cache.query(recs_q, rgb)
-        if timed_query:
-            q_end.record(stream)
-        launches += cache.last_launch_count
+        launches = cache.last_launch_count
+        if ev:
+            ev[1].record(stream)
         if world == 1:
-            cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
+            cache.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, seed)
             launches += cache.last_launch_count
-        elif args.train_mode == "peer":
-            # N3, all-gather fused into the kernel: rows gathered from the owners' memory
-            # (CUDA IPC / NVLink); the frame buffers are static and synchronised at setup
-            lo, hi = nrc.shard(N_TRAIN, rank, world)
-            dpf.train_frame_peer(d_r[lo:hi], d_t[lo:hi], TRAIN_S, TRAIN_L, 1000 + fi % 2, parts_ready=True)
-            launches += dpf.last_launch_count
-        elif args.train_mode == "allreduce-peer":
-            # SURVEY 8(e) mitigation 2 / N3 (ii): each rank's tiles of every batch, the
-            # gradient all-reduce fused into the optimiser over peer memory (no NCCL)
-            dpf.train_frame_allreduce_peer(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
-            launches += dpf.last_launch_count
-        elif args.train_mode == "replicated":
+        elif mode == "replicated":
             # N3 (i): this rank's screen-region records, one all-gather, replicated training
-            lo, hi = nrc.shard(N_TRAIN, rank, world)
-            dpf.train_frame_replicated(d_r[lo:hi], d_t[lo:hi], TRAIN_S, TRAIN_L, 1000 + fi % 2)
+            dpf.train_frame_replicated(d_rl, d_tl, TRAIN_S, TRAIN_L, seed, counts=t_counts)
+            launches += dpf.last_launch_count
+        elif mode == "allreduce-peer":
+            # SURVEY 8(e) mitigation 2 / N3 (ii): the gradient all-reduce fused into
+            # the optimiser over peer memory (no NCCL call)
+            dpf.train_frame_allreduce_peer(d_r, d_t, TRAIN_S, TRAIN_L, seed)
             launches += dpf.last_launch_count
         else:
-            # this rank's rows of every shuffled batch, gathered in-kernel (P:L487-491)
-            dpf.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi % 2)
+            # north_star: this rank's rows of every shuffled batch (gathered in-kernel,
+            # P:L487-491), one NCCL all-reduce per step, identical Adam on every rank
+            dpf.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, seed)
             launches += dpf.last_launch_count
+        if ev:
+            ev[2].record(stream)
         return launches
 
     torch.cuda.synchronize()
-    barrier()  # every rank's frame buffers are on the device (peer mode reads them remotely)
+    barrier()
     if world > 1:
-        dpf.verify_replicas(image_only=dedicated)  # the same seeded init on every rank
+        dpf.verify_replicas()  # the same seeded init on every rank
     for i in range(args.warmup):
         frame(i)
     torch.cuda.synchronize()
     barrier()
-    if dedicated:
-        # balance: rank 0's query share from the measured training time (rank 0)
-        # and query time (rank 1), decided on rank 0 and broadcast
-        def dev_ms(fn, reps=5):
-            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a_ev.record(stream)
-            for _ in range(reps):
-                fn()
-            b_ev.record(stream)
-            torch.cuda.synchronize()
-            return a_ev.elapsed_time(b_ev) / reps
-        d_r0, d_t0 = frames[0][0], frames[0][1]
-        mine = dev_ms(lambda: cache.train_frame(d_r0, d_t0, TRAIN_S, TRAIN_L, 999)) if rank == 0 else \
-            dev_ms(lambda: cache.query(recs_q, rgb)) * (world - 1)
-        got = [None] * world
-        dist.all_gather_object(got, mine)
-        share = [nrc.DataParallelFrame.dedicated_share0(got[1], got[0], world)]
-        dist.broadcast_object_list(share, src=0)
-        q0, q1 = dpf.dedicated_query_rows(N_QUERY, share[0])
-        recs_q = torch.from_numpy(recs_q_all[q0:q1].copy()).to(dev)
-        nq_local = q1 - q0
-        rgb = torch.empty((nq_local, 3), dtype=torch.float32, device=dev)
-        ded_share0 = share[0]
-        for i in range(3):
-            frame(i)
-        torch.cuda.synchronize()
-        barrier()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    qt = []
+    evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     launches = 0
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the timed events)
-            ev[i][0].record(stream)
-            launches += frame(i, timed_query=True)
-            ev[i][1].record(stream)
+            launches += frame(i, evs[i])
             torch.cuda.synchronize()
-            qt.append(q_start.elapsed_time(q_end))
         torch.cuda.synchronize()
         barrier()
-    step_ms = [s.elapsed_time(e) for s, e in ev]
+    step_ms = [a.elapsed_time(c) for a, b, c in evs]
+    q_list = [a.elapsed_time(b) for a, b, c in evs]
+    t_list = [b.elapsed_time(c) for a, b, c in evs]
     replicas = None
     if world > 1:  # SURVEY 8(e): bitwise-identical replicas after the timed frames (outside the timing)
-        replicas = "identical crc32 %08x" % dpf.verify_replicas(image_only=dedicated)
-    ms = float(np.mean(step_ms))
-    pct = [float(x) for x in np.percentile(step_ms, [10, 50, 90])]  # this rank's step distribution
-    q_ms = float(np.mean(qt))
-    if world > 1:
-        t = torch.tensor([ms, q_ms], dtype=torch.float64, device=dev)
+        replicas = "identical crc32 %08x" % dpf.verify_replicas()
+    st = stats_ms(step_ms)
+    ms, q_ms, t_ms = st["median"], float(np.median(q_list)), float(np.median(t_list))
+    pct = [st["p10"], st["p50"], st["p90"]]
+    if world > 1:  # max over ranks of every reported time
+        t = torch.tensor([ms, q_ms, t_ms, st["mean"]] + pct, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, q_ms = float(t[0]), float(t[1])
+        ms, q_ms, t_ms = float(t[0]), float(t[1]), float(t[2])
+        st["mean"] = float(t[3])
+        pct = [float(x) for x in t[4:7]]
 
-    # ---- end to end through the C ABI with host buffers (N = 1 path; for N > 1 rank-local)
+    # ---- end to end through the C ABI with host buffers (N = 1)
     e2e = None
     if world == 1 and not args.no_e2e:
         hq = torch.from_numpy(recs_q_all).pin_memory()
@@ -413,10 +386,14 @@ def run_nrc(args):
             cache.frame_host(hq_np, hrgb_np, ht_np, htg_np, TRAIN_S, TRAIN_L, 7, hl_np, scratch)
             e_ev[i][1].record(stream)
             torch.cuda.synchronize()
-        e_ms = float(np.mean([s.elapsed_time(e) for s, e in e_ev]))
-        e2e = {"value": e_ms, "unit": "ms", "h2d_bytes_per_step": N_QUERY * 64 + N_TRAIN * (64 + 12),
-               "d2h_bytes_per_step": N_QUERY * 12 + TRAIN_S * 4,
-               "note": "nrc_frame_host: pinned host records -> device, query + 4 train steps, RGB + losses -> host"}
+        e_ms = float(np.median([s.elapsed_time(e) for s, e in e_ev]))
+        h2d = N_QUERY * 64 + N_TRAIN * (64 + 12)
+        d2h = N_QUERY * 12 + TRAIN_S * 4
+        e2e = {"value": e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "pcie_gbs": (h2d + d2h) / (e_ms * 1e-3) / 1e9,
+               "note": "nrc_frame_host: pinned host records -> device (chunked, overlapped with the query), "
+                       "query + 4 train steps, RGB + losses -> host; bound by the PCIe copy of 137.7 MB in "
+                       "+ 24.9 MB out per frame"}
 
     peak_tf, peak_bw, peak_src = peaks()
     traffic, traffic_src = ncu_traffic("nrc_query_ts_kernel")
@@ -425,40 +402,50 @@ def run_nrc(args):
         t = torch.tensor([nq_local], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         nq_roof = int(t[0])
-    q_flops = FLOP_QUERY * nq_roof
-    achieved = q_flops / (q_ms * 1e-3) / 1e12
+    achieved = FLOP_QUERY * nq_roof / (q_ms * 1e-3) / 1e12
+    t_achieved = FLOP_TRAIN * N_TRAIN / max(world, 1) / (t_ms * 1e-3) / 1e12
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 Adam/EMA)", "data": "synthetic (nrc_inputs)",
-        "config": frame_config(world, args.train_mode),
-        "queries_per_s": N_QUERY / (ms * 1e-3), "records_per_s": N_TRAIN / (ms * 1e-3),
-        "query_ms": q_ms, "train_ms": ms - q_ms,
-        "ms_p10_p50_p90": pct,
+        "config": frame_config(world, mode),
+        "ms_stat": "median over the timed frames",
+        "ms_mean": st["mean"], "ms_p10_p50_p90": pct,
+        "query_ms": q_ms, "train_ms": t_ms,
+        # phase rates: queries over the query phase, records over the training phase
+        "queries_per_s": N_QUERY / (q_ms * 1e-3), "records_per_s": N_TRAIN / (t_ms * 1e-3),
+        "frame_queries_per_s": N_QUERY / (ms * 1e-3),
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "nrc_query_ts_kernel", "achieved": achieved, "peak": peak_tf,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic, "traffic_unit": "bytes/launch",
                      "traffic_source": traffic_src,
                      "algorithmic_bytes": BYTES_QUERY * nq_roof,
                      "peak_source": f"{peak_src} bf16 dense burst (fp16 same rate)",
-                     "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_roof} queries",
-                     # the same against the 2.25 PF dense fp16 spec, and the
-                     # kernel's HBM fraction (algorithmic bytes / time / HBM peak)
+                     "algorithmic": f"{FLOP_QUERY} FLOP/query x {nq_roof} queries / median query-phase time",
                      "frac_vs_spec_2250": achieved / 2250.0,
                      "hbm_frac": BYTES_QUERY * nq_roof / (q_ms * 1e-3) / 1e9 / peak_bw},
+        "train_roofline": {"bound": "latency (12 dependent MMA/epilogue rounds per step)",
+                           "achieved": t_achieved, "unit": "TFLOP/s", "frac": t_achieved / peak_tf,
+                           "algorithmic": f"{FLOP_TRAIN} FLOP/record x {N_TRAIN // max(world, 1)} records per rank"},
         "clocks": clk.summary(),
     }
     if replicas:
         line["replicas"] = replicas
-    if dedicated:
-        line["config"]["dedicated_rank0_query_share"] = ded_share0
     if e2e:
         line["e2e"] = e2e
-    if rank == 0 and not args.no_cpu_baseline:
-        cms, sample, _, _ = oracle_frame_estimate(16384, 2048)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        of = OracleFrame()
+        of.frame()  # page-in
+        reps = [of.frame() for _ in range(2)]
+        cms = float(np.median([r[0] for r in reps]))
         line["cpu_baseline"] = {"value": cms, "unit": "ms", "cores": omp_threads(), "kind": "oracle",
-                                "sample": sample, "cpu_model": cpu_model(),
-                                "single_thread_value": oracle_single_thread_ms()}
+                                "sample": "whole frames (2,073,600 queries + 4 sequential 16,384-record steps), "
+                                          "median of 2 after one untimed",
+                                "query_ms": float(np.median([r[1] for r in reps])),
+                                "train_ms": float(np.median([r[2] for r in reps])),
+                                "cpu_model": cpu_model(),
+                                "single_thread_value": oracle_single_thread_ms(),
+                                "single_thread_sample": "1/256 of every phase, scaled to the frame"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -477,22 +464,16 @@ def main():
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
-    ap.add_argument("--train-mode", choices=["dp", "replicated", "peer", "allreduce-peer", "dedicated"],
-                    default="dedicated",
-                    help="N > 1 training: split by function (dedicated, the default: rank 0 trains -- the "
-                         "latency-bound step fewer rows per GPU would not shorten -- while the other ranks "
-                         "query, then the new query image is broadcast), one all-gather of the frame's records "
-                         "per frame and replicated training (replicated, SURVEY N3 (i)), or "
-                         "data-parallel with one all-reduce per step (dp, north_star's description), or the "
-                         "all-gather fused into the training kernel over peer memory (peer), or data-parallel "
-                         "with the gradient all-reduce fused into the optimiser over peer memory "
-                         "(allreduce-peer), or split by function: rank 0 trains while the other ranks "
-                         "query, then the new query image is broadcast (dedicated)")
+    ap.add_argument("--train-mode", choices=["dp", "replicated", "allreduce-peer"], default="dp",
+                    help="N > 1 training: data-parallel with one NCCL all-reduce per step (dp, north_star's "
+                         "partition, the default), one all-gather of the frame's records then replicated "
+                         "training (replicated, SURVEY N3 (i)), or data-parallel with the gradient all-reduce "
+                         "fused into the optimiser over peer memory (allreduce-peer, N3 (ii))")
     args = ap.parse_args()
     if args.workload == "4k":
         global N_QUERY, METRIC, CONFIG_NAME
         N_QUERY = 3840 * 2160
-        METRIC = "NRC frame ms (4K: 8.29M queries + 4\u00d716384 train); queries/s, records/s"
+        METRIC = "NRC frame ms (4K: 8.29M queries + 4×16384 train); queries/s, records/s"
         CONFIG_NAME = "4K frame: 8,294,400 queries + 4x16384 train, width 64, 5 hidden layers"
     if args.warmup < 3:
         args.warmup = 3

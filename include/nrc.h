@@ -47,11 +47,16 @@
 extern "C" {
 #endif
 
-#define NRC_ABI_VERSION 1u
+#define NRC_ABI_VERSION 2u
 
 /* One cache query (Table 1): 16 fp32 = 64 bytes.
- * Arrays of records must be 16-byte aligned.  dir and normal need not be
- * unit length (they are renormalised; a zero vector reads as (0,0,1)). */
+ * Arrays of records must be 16-byte aligned.  Domain: pos is any finite point
+ * (inside or outside the AABB; the triangle waves are defined on all reals,
+ * R3/R4); dir and normal need not be unit length (they are renormalised, R7;
+ * |u|^2 must be a normal fp32 number or exactly 0, i.e. |u| in [1e-18, 1e18]
+ * or u = 0); a zero vector reads as (0,0,1) and is counted
+ * (nrc_get_stats); roughness < 0 reads as 0; reflectances are any finite
+ * values (alpha + beta = 0 gives a zero query and zero gradient). */
 typedef struct nrc_record {
     float pos[3];      /* x in world space; normalised by the config AABB (R3) */
     float dir[3];      /* scattered direction omega                              */
@@ -67,7 +72,7 @@ typedef enum nrc_status {
     NRC_ERR_UNSUPPORTED = 2,
     NRC_ERR_OUT_OF_MEMORY = 3, /* state arena too small */
     NRC_ERR_CUDA = 4,          /* a CUDA call failed; see nrc_last_error */
-    NRC_ERR_NCCL = 5,          /* reserved for the fused collective path */
+    NRC_ERR_NCCL = 5,          /* reserved; not returned by this version */
     NRC_ERR_STATE = 6          /* handle not initialised / wrong device  */
 } nrc_status;
 
@@ -101,7 +106,8 @@ typedef struct nrc_config {
                                 * at hidden_width 32 / 64 / 128 (training-kernel shared
                                 * memory), query and training alike; parameters
                                 * 64 W + (n-1) W^2 + 3 W                              */
-    uint32_t max_batch;        /* largest n accepted by query/train calls             */
+    uint32_t reserved0;        /* 0 (alignment of max_batch)                          */
+    uint64_t max_batch;        /* largest n accepted by query/train calls, <= 2^40    */
     float aabb_min[3];         /* position normalisation domain (R3)           */
     float aabb_max[3];
     float learning_rate;       /* 1e-2 (R11; paper: "high learning-rate")     */
@@ -158,23 +164,28 @@ nrc_status nrc_query_accumulate(nrc_handle* h, const nrc_record* d_rec, uint64_t
  * d_loss (optional, 1 fp32): the batch-mean loss.  n <= max_batch.  Two
  * kernel launches: the partials kernel (min(#SMs, ceil(n/128)) CTAs) and the
  * reduce + Adam + EMA kernel, chained with programmatic dependent launch.
- * With the environment variable NRC_TRAIN_FUSED=1 at nrc_init (width 64
- * only) one cooperative launch of the fused kernel instead; that launch must
- * not share the device with a concurrently running kernel holding its SMs
- * (it fails with NRC_ERR_CUDA if co-residency is impossible). */
+ * dL/dy is back-propagated in fp16 with a per-128-row power-of-two scale that
+ * is undone exactly in fp32 (R13, R25), so HDR targets cannot overflow it. */
 nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n, float* d_loss,
                           void* stream);
 
 /* Multi-GPU split of nrc_train_step.  nrc_train_backward writes the UN-
  * normalised gradient sum over the n_local records into d_grad
  * (nrc_param_count() fp32, logical layout: W0 Wx64, W1..W4 WxW, W5 3xW,
- * row-major [out][in]) and, if d_loss_sum != NULL, the loss sum (1 fp32).  The
- * caller all-reduces (SUM) d_grad across ranks, then nrc_train_apply runs
- * Adam + EMA with g = d_grad_sum / n_global.  Deterministic: equal inputs
- * give bitwise-equal replicas on every rank. */
+ * row-major [out][in]) and, if d_loss_sum != NULL, the loss sum (1 fp32).
+ * d_pred (optional, 3 n_local fp32): the training forward's (a4) factored
+ * prediction y * (alpha + beta) of each record, unclamped -- the quantity the
+ * loss sees (R9); with the same weights it equals nrc_query's radiance bit
+ * for bit when the query reads W_t without the clamp.  The caller all-reduces
+ * (SUM) d_grad (and the loss sum) across ranks, then nrc_train_apply runs
+ * Adam + EMA with g = d_grad_sum / n_global and, if d_loss_sum and d_loss are
+ * both given, writes the batch-mean loss *d_loss = *d_loss_sum / n_global
+ * (R10).  Deterministic: equal inputs give bitwise-equal replicas on every
+ * rank. */
 nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_local,
-                              float* d_grad, float* d_loss_sum, void* stream);
-nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, void* stream);
+                              float* d_grad, float* d_loss_sum, float* d_pred, void* stream);
+nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, const float* d_loss_sum,
+                           float* d_loss, void* stream);
 
 /* A frame's training: records are shuffled by the LCG
  * permutation of nrc_lcg_params(n_total, shuffle_seed) (R15) and split into
@@ -182,8 +193,7 @@ nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_gl
  * perm(j*l + k), k < l, gathered inside the kernel (nothing materialised).
  * If s*l > n_total, l shrinks to n_total / s.  d_losses: s fp32
  * (optional).  Equivalent (bitwise) to s nrc_train_step calls on the
- * gathered batches; two launches per step (one cooperative launch per 8
- * steps with NRC_TRAIN_FUSED=1). */
+ * gathered batches; two launches per step. */
 nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s,
                            uint32_t l, uint64_t shuffle_seed, float* d_losses, void* stream);
 
@@ -196,21 +206,6 @@ nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* 
 nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
                                     uint32_t l, uint64_t shuffle_seed, uint32_t j, uint32_t row_begin,
                                     uint32_t row_end, float* d_grad, float* d_loss_sum, void* stream);
-
-/* Replicated frame training over peer memory: the frame's
- * n_parts x n_per_part training records live on n_parts ranks (part p holds
- * records [p n_per_part, (p+1) n_per_part), e.g. each rank's screen region;
- * rec_parts / tgt_parts are HOST arrays of the parts' DEVICE pointers, peers'
- * opened with nrc_ipc_import).  The training kernel gathers every shuffled
- * batch row straight from its owner's buffer -- NVLink loads on a multi-GPU
- * box -- so the frame's record all-gather happens inside the kernel and no
- * collective runs.  Bitwise identical to nrc_train_frame on the concatenated
- * records, so every rank ends with the same state.  n_parts <= 8.  The caller
- * guarantees the parts are complete before the call and are not overwritten
- * until it has finished (e.g. a barrier per frame). */
-nrc_status nrc_train_frame_parts(nrc_handle* h, const nrc_record* const* rec_parts, const float* const* tgt_parts,
-                                 uint32_t n_parts, uint32_t n_per_part, uint32_t s, uint32_t l,
-                                 uint64_t shuffle_seed, float* d_losses, void* stream);
 
 /* Data-parallel frame training with the gradient all-reduce fused into the
  * optimiser over peer memory (SURVEY 8(e) mitigation 2, 8(f) N3 (ii); no NCCL
@@ -230,14 +225,14 @@ nrc_status nrc_train_frame_parts(nrc_handle* h, const nrc_record* const* rec_par
  * d_state at index rank; peers' mapped with nrc_ipc_import).  All ranks must
  * make the same sequence of calls; the hand-off gives up after ~20 s
  * (counted by nrc_dp_timeouts) instead of hanging.  d_losses: s fp32
- * (optional).  NRC_ERR_UNSUPPORTED with NRC_TRAIN_FUSED=1 or T > 128. */
+ * (optional).  NRC_ERR_UNSUPPORTED if T > 128. */
 nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
                                    uint32_t s, uint32_t l, uint64_t shuffle_seed, uint32_t rank, uint32_t world,
                                    void* const* peer_state, float* d_losses, void* stream);
 /* Number of nrc_train_frame_dp_peer hand-offs that timed out (synchronous). */
 nrc_status nrc_dp_timeouts(nrc_handle* h, uint64_t* count);
 
-/* CUDA IPC for nrc_train_frame_parts and nrc_train_frame_dp_peer.  nrc_ipc_export: the 64-byte handle of
+/* CUDA IPC for nrc_train_frame_dp_peer.  nrc_ipc_export: the 64-byte handle of
  * the device allocation that contains d_ptr and d_ptr's offset in it;
  * nrc_ipc_import (another process): maps it, *d_ptr = mapped base + offset;
  * nrc_ipc_close: unmaps (pass the imported pointer and its offset).  A
@@ -277,17 +272,13 @@ nrc_status nrc_assemble_targets(nrc_handle* h, const uint32_t* d_first, const ui
 nrc_status nrc_get_params(nrc_handle* h, nrc_param_set which, float* h_out, size_t n);
 nrc_status nrc_set_params(nrc_handle* h, nrc_param_set which, const float* h_in, size_t n);
 
-/* Adam step count t and the non-finite counters.  Synchronous. */
-nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets);
-
-/* The fp16 operand image nrc_query reads (the EMA weights W-bar, or W with
- * NRC_QUERY_RAW_WEIGHTS / ema_alpha = 0): its device address inside the
- * state arena and its size in bytes.  Multi-GPU use: a rank that only
- * queries receives it from the training rank (a broadcast of these bytes
- * between identically configured caches), SURVEY 8(e) / N3.  The bytes are
- * rewritten by every training call on this handle; a transfer must be
- * ordered after them and before the next query that should see it. */
-nrc_status nrc_query_image(nrc_handle* h, void** d_image, size_t* bytes);
+/* Adam step count t, the non-finite counters (gradient entries zeroed,
+ * records with a non-finite target masked) and the number of zero-length
+ * direction / normal vectors encoded so far by queries, training and
+ * nrc_encode (read as (0,0,1)).  Any output may be
+ * NULL.  Synchronous. */
+nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets,
+                         uint64_t* degenerate_vectors);
 
 /* 20,672 at width 64 (5*64*64 + 3*64; reading R1). */
 size_t nrc_param_count(const nrc_handle* h);

@@ -135,3 +135,71 @@ def training_paths(n_vertices: int = TRAIN_S * TRAIN_L, seed: int = SEED_PATHS, 
     vrec = records(n_vertices, seed=seed + 1)
     trec = records(length.size, seed=seed + 2)
     return first, length, flags, vert, vrec, trec
+
+
+# Off-default domain (Table 1's inputs are x in R^3, omega and n arbitrary
+# vectors renormalised by sph, r in R, reflectances in R):
+# an offset, non-unit AABB and records inside, outside and far outside it.
+DOMAIN_AABB_LO = (-3.7, 2.0, -100.0)
+DOMAIN_AABB_HI = (5.1, 9.0, 250.0)
+
+
+def _domain_vectors(rng: np.random.Generator, n: int) -> np.ndarray:
+    """Direction-like vectors covering the encoder's edge cases: unit, non-unit
+    (|u| in [1e-3, 1e3]), exact poles (0, 0, +-s), the phi seam (x < 0,
+    y = +0.0 or -0.0 exactly), tiny |y| next to the seam, and zero vectors."""
+    kind = rng.integers(0, 8, n)
+    v = _unit_vectors(rng, n).astype(np.float64)
+    mag = 10.0 ** rng.uniform(-3.0, 3.0, n)
+    v[kind == 1] *= mag[kind == 1, None]
+    s = mag * np.where(rng.random(n) < 0.5, 1.0, -1.0)
+    pole = kind == 2
+    v[pole] = 0.0
+    v[pole, 2] = s[pole]
+    seam = (kind == 3) | (kind == 4)
+    v[seam, 0] = -np.abs(v[seam, 0]) - 1e-3
+    v[seam, 1] = 0.0
+    tiny = kind == 5
+    v[tiny, 0] = -np.abs(v[tiny, 0]) - 1e-3
+    v[tiny, 1] = rng.choice([-1.0, 1.0], tiny.sum()) * 10.0 ** rng.uniform(-30, -8, tiny.sum())
+    v[kind == 6] = 0.0
+    out = v.astype(np.float32)
+    out[kind == 4, 1] = np.float32(-0.0)  # the other side of the seam: atan2(-0, x < 0) = -pi
+    return out
+
+
+def domain_records(n: int, seed: int = 0xD0, lo=DOMAIN_AABB_LO, hi=DOMAIN_AABB_HI) -> np.ndarray:
+    """n records over the off-default input domain, float32 [n, 16]:
+    positions inside the AABB, on its faces, outside it (up to twice its
+    extent) and far outside (|p| up to ~1e3); direction / normal edge cases
+    (_domain_vectors); roughness in [-2, 60] (negative reads as 0); diffuse
+    and specular in [-0.5, 2) (alpha + beta > 1), with alpha = beta = 0 on
+    1/16 of the records."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    lo = np.asarray(lo, np.float64)
+    hi = np.asarray(hi, np.float64)
+    ext = hi - lo
+    r = np.empty((n, REC_FLOATS), np.float32)
+    kind = rng.integers(0, 4, n)
+    p = lo + rng.random((n, 3)) * ext                               # inside
+    p[kind == 1] = lo + rng.uniform(-1.0, 2.0, ((kind == 1).sum(), 3)) * ext   # outside, near
+    far = kind == 2
+    p[far] = rng.uniform(-1000.0, 1000.0, (far.sum(), 3))           # far outside
+    face = kind == 3
+    p[face] = np.where(rng.random((face.sum(), 3)) < 0.5, lo, hi)   # faces / corners exactly
+    r[:, 0:3] = p.astype(np.float32)
+    r[:, 3:6] = _domain_vectors(rng, n)
+    r[:, 6:9] = _domain_vectors(rng, n)
+    r[:, 9] = rng.uniform(-2.0, 60.0, n).astype(np.float32)
+    r[rng.random(n) < 0.1, 9] = 0.0
+    r[:, 10:16] = rng.uniform(-0.5, 2.0, (n, 6)).astype(np.float32)
+    r[rng.random(n) < 1.0 / 16, 10:16] = 0.0
+    return r
+
+
+def hdr_targets(n: int, seed: int = 0xD1, lo_exp: float = -3.0, hi_exp: float = 4.0) -> np.ndarray:
+    """HDR training targets spanning 10^lo_exp .. 10^hi_exp per channel
+    (log-uniform): the bright-emitter / noisy-radiance regime the relative
+    loss is built for (P:L885-891)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return (10.0 ** rng.uniform(lo_exp, hi_exp, (n, 3))).astype(np.float32)

@@ -14,7 +14,8 @@ class NrcConfig(ctypes.Structure):
         ("abi_version", ctypes.c_uint32),
         ("hidden_width", ctypes.c_uint32),
         ("n_hidden_layers", ctypes.c_uint32),
-        ("max_batch", ctypes.c_uint32),
+        ("reserved0", ctypes.c_uint32),
+        ("max_batch", ctypes.c_uint64),
         ("aabb_min", ctypes.c_float * 3),
         ("aabb_max", ctypes.c_float * 3),
         ("learning_rate", ctypes.c_float),
@@ -35,8 +36,8 @@ SYMBOLS = [
     "nrc_train_backward", "nrc_train_apply", "nrc_train_frame", "nrc_train_frame_backward", "nrc_lcg_params", "nrc_encode", "nrc_get_params",
     "nrc_set_params", "nrc_get_stats", "nrc_param_count", "nrc_status_string", "nrc_last_error",
     "nrc_frame_scratch_bytes", "nrc_frame_host", "nrc_selftest_umma", "nrc_last_launch_count",
-    "nrc_assemble_targets", "nrc_query_accumulate", "nrc_train_frame_parts", "nrc_train_frame_dp_peer",
-    "nrc_dp_timeouts", "nrc_ipc_export", "nrc_ipc_import", "nrc_ipc_close", "nrc_query_image",
+    "nrc_assemble_targets", "nrc_query_accumulate", "nrc_train_frame_dp_peer",
+    "nrc_dp_timeouts", "nrc_ipc_export", "nrc_ipc_import", "nrc_ipc_close",
 ]
 
 
@@ -63,19 +64,16 @@ def load(build_if_missing: bool = True):
     L.nrc_destroy.restype = st; L.nrc_destroy.argtypes = [vp]
     L.nrc_query.restype = st; L.nrc_query.argtypes = [vp, vp, u64, vp, vp]
     L.nrc_train_step.restype = st; L.nrc_train_step.argtypes = [vp, vp, vp, u32, vp, vp]
-    L.nrc_train_backward.restype = st; L.nrc_train_backward.argtypes = [vp, vp, vp, u32, vp, vp, vp]
-    L.nrc_train_apply.restype = st; L.nrc_train_apply.argtypes = [vp, vp, u32, vp]
+    L.nrc_train_backward.restype = st; L.nrc_train_backward.argtypes = [vp, vp, vp, u32, vp, vp, vp, vp]
+    L.nrc_train_apply.restype = st; L.nrc_train_apply.argtypes = [vp, vp, u32, vp, vp, vp]
     L.nrc_train_frame.restype = st; L.nrc_train_frame.argtypes = [vp, vp, vp, u32, u32, u32, u64, vp, vp]
     L.nrc_train_frame_backward.restype = st
     L.nrc_train_frame_backward.argtypes = [vp, vp, vp, u32, u32, u64, u32, u32, u32, vp, vp, vp]
     L.nrc_lcg_params.restype = st; L.nrc_lcg_params.argtypes = [u64, u64, P(u64), P(u64), P(u64)]
     L.nrc_encode.restype = st; L.nrc_encode.argtypes = [vp, vp, u64, vp, vp]
-    L.nrc_train_frame_parts.restype = st
-    L.nrc_train_frame_parts.argtypes = [vp, vp, vp, u32, u32, u32, u32, u64, vp, vp]
     L.nrc_train_frame_dp_peer.restype = st
     L.nrc_train_frame_dp_peer.argtypes = [vp, vp, vp, u32, u32, u32, u64, u32, u32, vp, vp, vp]
     L.nrc_dp_timeouts.restype = st; L.nrc_dp_timeouts.argtypes = [vp, P(u64)]
-    L.nrc_query_image.restype = st; L.nrc_query_image.argtypes = [vp, P(vp), P(sz)]
     L.nrc_ipc_export.restype = st; L.nrc_ipc_export.argtypes = [vp, vp, P(u64)]
     L.nrc_ipc_import.restype = st; L.nrc_ipc_import.argtypes = [vp, u64, P(vp)]
     L.nrc_ipc_close.restype = st; L.nrc_ipc_close.argtypes = [vp, u64]
@@ -85,7 +83,7 @@ def load(build_if_missing: bool = True):
     L.nrc_assemble_targets.argtypes = [vp, vp, vp, vp, ctypes.c_uint32, vp, vp, vp, vp]
     L.nrc_get_params.restype = st; L.nrc_get_params.argtypes = [vp, st, vp, sz]
     L.nrc_set_params.restype = st; L.nrc_set_params.argtypes = [vp, st, vp, sz]
-    L.nrc_get_stats.restype = st; L.nrc_get_stats.argtypes = [vp, P(u64), P(u64), P(u64)]
+    L.nrc_get_stats.restype = st; L.nrc_get_stats.argtypes = [vp, P(u64), P(u64), P(u64), P(u64)]
     L.nrc_param_count.restype = sz; L.nrc_param_count.argtypes = [vp]
     L.nrc_status_string.restype = ctypes.c_char_p; L.nrc_status_string.argtypes = [st]
     L.nrc_last_error.restype = ctypes.c_char_p; L.nrc_last_error.argtypes = [vp]

@@ -19,44 +19,13 @@ using namespace nrc;
 
 namespace {
 
-// Query-kernel configurations <tile groups per CTA, tiles in flight per group>
-// (DESIGN.md 5.2).  Entry 0 is the default; NRC_QUERY_CFG=i selects another
-// one (tuning runs only).
+// Query-kernel launchers: the TMEM-activation kernel with G
+// tile groups per CTA and one tile in flight per group, per width / encoding.
 struct QueryEntry {
     cudaError_t (*set_smem)();
     void (*launch)(int, const QueryArgs&, cudaStream_t);
     int groups;
 };
-template <int G, int S>
-struct QueryLauncher {
-    static cudaError_t set_smem() {
-        return cudaFuncSetAttribute(nrc_query_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    query_smem_bytes<G, S>());
-    }
-    static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
-        nrc_query_kernel<G, S><<<grid, 128 * G, query_smem_bytes<G, S>(), st>>>(qa);
-    }
-};
-template <int G, int S>
-struct QueryLauncherTS {
-    static cudaError_t set_smem() {
-        return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    query_ts_smem_bytes_nh<G, S, 64>(TrainW<64>::kMaxNh));
-    }
-    static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
-        nrc_query_ts_kernel<G, S><<<grid, 128 * G, query_ts_smem_bytes_nh<G, S, 64>(int(qa.nh)), st>>>(qa);
-    }
-};
-#define NRC_QCFG(G, S) {&QueryLauncher<G, S>::set_smem, &QueryLauncher<G, S>::launch, G}
-#define NRC_QCFG_TS(G, S) {&QueryLauncherTS<G, S>::set_smem, &QueryLauncherTS<G, S>::launch, G}
-// Entry 0 (activations in TMEM, 5 groups x 1 tile) is the default; the
-// shared-memory-activation variants are kept for comparison.
-const QueryEntry kQueryCfgs[] = {NRC_QCFG_TS(5, 1), NRC_QCFG(4, 2), NRC_QCFG(3, 2), NRC_QCFG(2, 4),
-                                 NRC_QCFG(6, 1),    NRC_QCFG_TS(2, 2), NRC_QCFG_TS(1, 5), NRC_QCFG_TS(4, 1),
-                                 NRC_QCFG_TS(3, 1)};
-#undef NRC_QCFG
-#undef NRC_QCFG_TS
-constexpr int kNumQueryCfgs = int(sizeof(kQueryCfgs) / sizeof(kQueryCfgs[0]));
 // width ablation: one TMEM-activation configuration per width
 template <int G, int S, int W>
 struct QueryLauncherW {
@@ -78,6 +47,7 @@ struct QueryLauncherExact {
         nrc_query_ts_kernel<G, S, W, true><<<grid, 128 * G, query_ts_smem_bytes_nh<G, S, W>(int(qa.nh)), st>>>(qa);
     }
 };
+const QueryEntry kQuery64 = {&QueryLauncherW<5, 1, 64>::set_smem, &QueryLauncherW<5, 1, 64>::launch, 5};
 const QueryEntry kQueryExact = {&QueryLauncherExact<5, 1, 64>::set_smem, &QueryLauncherExact<5, 1, 64>::launch, 5};
 #ifndef NRC_W32_G
 #define NRC_W32_G 7  // 7 groups: 82 us vs 90 us with 5 at 1080p (scripts/try_w32.sh)
@@ -144,8 +114,8 @@ StateLayout layout(int W, int nh) {
     // training scratch: per-CTA fp32 gradient partials (padded layout of the width)
     L.partials = take(sizeof(float) * size_t(wi.padded) * kMaxPartials);
     L.loss_part = take(sizeof(float) * kMaxPartials);
-    // [0] non-finite gradients, [1] non-finite targets, [2]/[3] fused-kernel
-    // grid barriers, [4] fused peer all-reduce hand-off, [5] its timeouts
+    // [0] non-finite gradients, [1] non-finite targets, [2] zero-length
+    // omega / n vectors encoded, [4] fused peer all-reduce hand-off, [5] its timeouts
     L.counters = take(sizeof(unsigned long long) * 8);
     // nrc_train_frame_dp_peer: per step parity, kMaxDpTiles partial + loss pointers
     L.dp_tables = take(sizeof(const float*) * 2 * 2 * kMaxDpTiles);
@@ -171,12 +141,7 @@ struct nrc_handle {
     EncodeParams ep;
     std::string err;
     uint32_t launches;
-    int query_cfg;
     long long* dbg = nullptr;  // diagnostics only (nrc_debug_set_trace)
-    unsigned long long gbar = 0;  // arrivals so far on the train kernel's grid-barrier counter
-    unsigned long long gbarA = 0; // arrivals so far on its phase-A (W3..W5 partials written) counter
-    bool coop = true;             // cooperative launch of the fused train kernel (NRC_COOP=0: plain, diagnostics)
-    bool train_fused = false;     // width 64 through the fused cooperative kernel (NRC_TRAIN_FUSED=1, comparison)
     unsigned long long dp_expect = 0;  // hand-off counter value after the last nrc_train_frame_dp_peer step
     uint64_t dp_seq = 0;               // steps done by nrc_train_frame_dp_peer (partial-slot parity)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
@@ -249,23 +214,6 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
-// Cooperative launch (all CTAs co-resident; the fused train kernel has grid barriers).
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                               Args... args) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, args...);
-}
-
 template <int W>
 static void launch_images(nrc_handle* h, cudaStream_t st) {
     const int blocks = (h->wi.padded + 255) / 256;
@@ -318,8 +266,8 @@ static nrc_status validate_config(const nrc_config* c, std::string* why) {
         *why = "n_hidden_layers must be 5 (P:L694) or, for the depth variants, 1..8 / 1..7 / 1..5 at width 32 / 64 / 128";
         return NRC_ERR_UNSUPPORTED;
     }
-    if (c->max_batch == 0) {
-        *why = "max_batch must be > 0";
+    if (c->max_batch == 0 || c->max_batch > (1ull << 40)) {
+        *why = "max_batch must be in [1, 2^40]";
         return NRC_ERR_INVALID_ARGUMENT;
     }
     for (int i = 0; i < 3; ++i) {
@@ -429,26 +377,13 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
         h->err = "libnrc is built for sm_100a (B200); device compute capability major = " + std::to_string(major);
         return bail(NRC_ERR_UNSUPPORTED);
     }
-    h->query_cfg = 0;
-    if (const char* e = std::getenv("NRC_COOP")) h->coop = std::atoi(e) != 0;
-    if (const char* e = std::getenv("NRC_TRAIN_FUSED")) h->train_fused = std::atoi(e) != 0;
+    // diagnostics / probes only: cap the query or train grid
     if (const char* e = std::getenv("NRC_QUERY_CTAS")) h->query_ctas = std::atoi(e);
     if (const char* e = std::getenv("NRC_TRAIN_CTAS")) h->train_ctas = std::atoi(e);
-    if (const char* e = std::getenv("NRC_QUERY_CFG")) h->query_cfg = std::atoi(e);
-    if (h->query_cfg < 0 || h->query_cfg >= kNumQueryCfgs) h->query_cfg = 0;
-    for (int i = 0; i < kNumQueryCfgs; ++i)
-        if ((s = cuda_check(h, kQueryCfgs[i].set_smem(), "cudaFuncSetAttribute(query)")) != NRC_OK) return bail(s);
+    if ((s = cuda_check(h, kQuery64.set_smem(), "cudaFuncSetAttribute(query)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW32.set_smem(), "cudaFuncSetAttribute(query w32)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW128.set_smem(), "cudaFuncSetAttribute(query w128)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryExact.set_smem(), "cudaFuncSetAttribute(query exact)")) != NRC_OK) return bail(s);
-    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kTrainSmemBytes),
-                        "cudaFuncSetAttribute(train)")) != NRC_OK)
-        return bail(s);
-    if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kTrainSmemBytes),
-                        "cudaFuncSetAttribute(train exact)")) != NRC_OK)
-        return bail(s);
     if ((s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 TrainW<32>::smem_bytes(TrainW<32>::kMaxNh)),
                         "cudaFuncSetAttribute(train w32)")) != NRC_OK ||
@@ -494,15 +429,10 @@ nrc_status nrc_destroy(nrc_handle* h) {
     return NRC_OK;
 }
 
-// Training runs as one partials kernel + one reduce/Adam/EMA kernel per step
-// (nrc_train_w.cuh, PDL-chained) at every width: measured faster than the
-// fused cooperative kernel at width 64 (68.6 vs 74.8 us per 4-step frame,
-// DESIGN.md 5.2), which stays selectable with NRC_TRAIN_FUSED=1.
 static nrc_status check_train_width(nrc_handle* h) {
     if (width_supported(uint32_t(h->wi.W))) return NRC_OK;
     return fail(h, NRC_ERR_UNSUPPORTED, "unsupported hidden width for training");
 }
-static bool train_generic(const nrc_handle* h) { return h->wi.W != 64 || h->wi.nh != 5 || !h->train_fused; }
 static nrc_status check_handle(nrc_handle* h) {
     if (!h || !h->state) return NRC_ERR_STATE;
     int dev = -1;
@@ -526,20 +456,18 @@ static nrc_status query_impl(nrc_handle* h, const nrc_record* d_rec, uint64_t n,
     qa.thr = d_thr;
     qa.image = d_image;
     qa.nh = uint32_t(h->wi.nh);
-    // the fused accumulate epilogue and the depth variants exist in the TMEM
-    // kernels only (entry 0 and the width kernels)
-    const int cfg = (d_image || h->wi.nh != 5) ? 0 : h->query_cfg;
+    qa.degenerate = h->d_counters() + 2;
     const QueryEntry& qe = h->ep.exact        ? kQueryExact
                            : h->wi.W == 32   ? kQueryW32
                            : h->wi.W == 128  ? kQueryW128
-                                             : kQueryCfgs[cfg];
+                                             : kQuery64;
     const uint64_t ntiles = (n + kTile - 1) / kTile;
     const uint64_t G = uint64_t(qe.groups);
     const uint64_t ctas = (ntiles + G - 1) / G;  // one tile stream per group
     const uint64_t cap = h->query_ctas > 0 && h->query_ctas < h->num_sms ? uint64_t(h->query_ctas) : uint64_t(h->num_sms);
     const int grid = int(ctas < cap ? ctas : cap);
     qe.launch(grid, qa, static_cast<cudaStream_t>(stream));
-    NRC_LAUNCHED(h, "nrc_query_kernel");
+    NRC_LAUNCHED(h, "nrc_query_ts_kernel");
     return NRC_OK;
 }
 
@@ -570,9 +498,6 @@ nrc_status nrc_query_accumulate(nrc_handle* h, const nrc_record* d_rec, uint64_t
 struct Gather {
     bool on;
     uint64_t a, c, m, n, offset;
-    uint32_t n_parts = 0, part_n = 0;  // peer mode
-    const float* rec_parts[kMaxParts] = {};
-    const float* tgt_parts[kMaxParts] = {};
 };
 
 // Adam bias corrections and EMA coefficients of optimisation step t >= 1
@@ -597,10 +522,6 @@ static StepCoef step_coef(const nrc_config& c, uint64_t t) {
     return k;
 }
 
-// The train kernel over n rows per step.  nsteps == 0: one step, per-CTA
-// partials only (PDL launch; the caller reduces).  nsteps >= 1: fused
-// cooperative launch running nsteps optimisation steps (reduce + Adam + EMA
-// inside), batch-mean losses to d_losses[0..nsteps).  Returns #partials.
 static TrainArgs train_args(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
                             const Gather& gth) {
     TrainArgs ta{};
@@ -613,12 +534,6 @@ static TrainArgs train_args(nrc_handle* h, const nrc_record* d_rec, const float*
     ta.lcg_m = gth.m;
     ta.lcg_n = gth.n;
     ta.offset = gth.offset;
-    ta.n_parts = gth.n_parts;
-    ta.part_n = gth.part_n;
-    for (int p = 0; p < kMaxParts; ++p) {
-        ta.rec_parts[p] = gth.rec_parts[p];
-        ta.tgt_parts[p] = gth.tgt_parts[p];
-    }
     ta.wimg = h->d_wimg();
     ta.ep = h->ep;
     ta.flags = h->cfg.flags & NRC_FACTORIZE;
@@ -626,6 +541,7 @@ static TrainArgs train_args(nrc_handle* h, const nrc_record* d_rec, const float*
     ta.partials = h->d_partials();
     ta.loss_part = h->d_loss_part();
     ta.bad_targets = h->d_counters() + 1;
+    ta.degenerate = h->d_counters() + 2;
     ta.dbg = h->dbg;
     ta.nh = uint32_t(h->wi.nh);
     return ta;
@@ -648,10 +564,11 @@ static cudaError_t launch_train_w_grid(nrc_handle* h, const TrainArgs& ta, int g
         return launch_pdl(nrc_train_w_kernel<64, true>, dim3(grid), dim3(128), TrainW<64>::smem_bytes(nh), st, ta);
     return launch_pdl(nrc_train_w_kernel<64>, dim3(grid), dim3(128), TrainW<64>::smem_bytes(nh), st, ta);
 }
-// Width-generic partials kernel (nrc_train_w.cuh): one step over n rows.
+// One step's partials over n rows.
 static nrc_status launch_train_w(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
-                                 const Gather& gth, cudaStream_t st, int* nparts) {
+                                 const Gather& gth, cudaStream_t st, int* nparts, float* d_pred = nullptr) {
     TrainArgs ta = train_args(h, d_rec, d_tgt, n, gth);
+    ta.pred = d_pred;
     if (h->dbg) ta.dbg = h->dbg + 4096 * (h->step % 4);  // diagnostics: one 4096-slot block per step
     const int grid = train_grid(h, n);
     *nparts = grid;
@@ -695,87 +612,15 @@ static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t
     return NRC_OK;
 }
 
-static nrc_status launch_train(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
-                               const Gather& gth, cudaStream_t st, int* nparts, uint32_t nsteps = 0,
-                               float* d_losses = nullptr) {
-    if (train_generic(h) && nsteps == 0) return launch_train_w(h, d_rec, d_tgt, n, gth, st, nparts);
-    TrainArgs ta = train_args(h, d_rec, d_tgt, n, gth);
-    const int grid = train_grid(h, n);
-    *nparts = grid;
-    if (nsteps == 0) {
-        ta.fused = 0;
-        ta.nsteps = 1;
-        NRC_CUDA(h, launch_pdl(h->ep.exact ? nrc_train_kernel<true> : nrc_train_kernel<false>, dim3(grid),
-                               dim3(kTrainBlock), kTrainSmemBytes, st, ta));
-        NRC_LAUNCHED(h, "nrc_train_kernel");
-        return NRC_OK;
-    }
-    const nrc_config& c = h->cfg;
-    ta.fused = 1;
-    ta.nsteps = nsteps;
-    ta.inv_n = float(1.0 / double(n));
-    ta.lr = c.learning_rate;
-    ta.b1 = c.adam_beta1;
-    ta.b2 = c.adam_beta2;
-    ta.adam_eps = c.adam_eps;
-    for (uint32_t k = 0; k < nsteps; ++k) ta.coef[k] = step_coef(c, h->step + 1 + k);
-    ta.w = h->d_w();
-    ta.m = h->d_m();
-    ta.v = h->d_v();
-    ta.ema = h->d_ema();
-    ta.wimg_out = h->d_wimg();
-    ta.eimg = h->d_eimg();
-    ta.bad_grads = h->d_counters() + 0;
-    ta.losses = d_losses;
-    ta.gbar = h->d_counters() + 2;
-    ta.gbar_base = h->gbar;
-    ta.gbarA = h->d_counters() + 3;
-    ta.gbarA_base = h->gbarA;
-    if (h->coop)
-        NRC_CUDA(h, launch_coop(h->ep.exact ? nrc_train_kernel<true> : nrc_train_kernel<false>, dim3(grid),
-                                dim3(kTrainBlock), kTrainSmemBytes, st, ta));
-    else if (h->ep.exact)
-        nrc_train_kernel<true><<<grid, kTrainBlock, kTrainSmemBytes, st>>>(ta);
-    else
-        nrc_train_kernel<false><<<grid, kTrainBlock, kTrainSmemBytes, st>>>(ta);
-    NRC_LAUNCHED(h, "nrc_train_kernel");
-    h->gbar += 2ull * nsteps * uint64_t(grid);
-    h->gbarA += uint64_t(nsteps) * uint64_t(grid);
-    h->step += nsteps;
-    return NRC_OK;
-}
-
-static AdamArgs adam_args(nrc_handle* h) {
-    AdamArgs aa{};
-    const nrc_config& c = h->cfg;
-    aa.w = h->d_w();
-    aa.m = h->d_m();
-    aa.v = h->d_v();
-    aa.ema = h->d_ema();
-    aa.wimg = h->d_wimg();
-    aa.eimg = h->d_eimg();
-    aa.lr = c.learning_rate;
-    aa.b1 = c.adam_beta1;
-    aa.b2 = c.adam_beta2;
-    aa.eps = c.adam_eps;
-    const StepCoef k = step_coef(c, h->step);  // already incremented
-    aa.inv_bc1 = k.inv_bc1;
-    aa.inv_bc2 = k.inv_bc2;
-    aa.ema_c1 = k.ema_c1;
-    aa.ema_c2 = k.ema_c2;
-    aa.bad_grads = h->d_counters() + 0;
-    return aa;
-}
-
-static nrc_status train_step_impl(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
-                                  const Gather& gth, float* d_losses, uint32_t nsteps, cudaStream_t st) {
-    int np = 0;
-    if (!train_generic(h)) return launch_train(h, d_rec, d_tgt, n, gth, st, &np, nsteps, d_losses);
-    // width-generic: per step the partials kernel, then reduce + Adam + EMA
+// nsteps optimisation steps of n rows each (step k gathers rows offset + k n
+// when gathering): per step the partials kernel, then reduce + Adam + EMA.
+static nrc_status train_steps(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                              const Gather& gth, float* d_losses, uint32_t nsteps, cudaStream_t st) {
     uint32_t launches = 0;
     for (uint32_t k = 0; k < nsteps; ++k) {
         Gather g = gth;
-        g.offset = gth.offset + uint64_t(k) * n;  // step k of the batch sequence
+        g.offset = gth.offset + uint64_t(k) * n;
+        int np = 0;
         nrc_status s = launch_train_w(h, d_rec, d_tgt, n, g, st, &np);
         if (s != NRC_OK) return s;
         h->step += 1;
@@ -795,21 +640,15 @@ static nrc_status train_step_impl(nrc_handle* h, const nrc_record* d_rec, const 
 }
 // partials -> logical gradient sum + loss sum (multi-GPU backward)
 static nrc_status reduce_partials(nrc_handle* h, int np, float* d_grad, float* d_loss_sum, cudaStream_t st) {
-    if (train_generic(h)) {
-        AdamWArgs aa = adam_w_args(h);
-        aa.partials = h->d_partials();
-        aa.np = np;
-        aa.grad_out = d_grad;
-        aa.apply = 0;
-        aa.nloss = np;
-        aa.loss_scale = 1.0f;
-        aa.loss_out = d_loss_sum;
-        return launch_adam_w(h, aa, st);
-    }
-    nrc_reduce_kernel<<<kParamPadded / 32, kRedThreads, 0, st>>>(h->d_partials(), np, d_grad, h->d_loss_part(),
-                                                                  d_loss_sum);
-    NRC_LAUNCHED(h, "nrc_reduce_kernel");
-    return NRC_OK;
+    AdamWArgs aa = adam_w_args(h);
+    aa.partials = h->d_partials();
+    aa.np = np;
+    aa.grad_out = d_grad;
+    aa.apply = 0;
+    aa.nloss = np;
+    aa.loss_scale = 1.0f;
+    aa.loss_out = d_loss_sum;
+    return launch_adam_w(h, aa, st);
 }
 
 static nrc_status check_train_args(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint64_t n,
@@ -830,16 +669,17 @@ nrc_status nrc_train_step(nrc_handle* h, const nrc_record* d_rec, const float* d
     if ((s = check_train_args(h, d_rec, d_tgt, n, "nrc_train_step")) != NRC_OK) return s;
     if (d_loss && !aligned(d_loss, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "misaligned d_loss");
     Gather g{false, 0, 0, 0, 0, 0};
-    return train_step_impl(h, d_rec, d_tgt, n, g, d_loss, 1, static_cast<cudaStream_t>(stream));
+    return train_steps(h, d_rec, d_tgt, n, g, d_loss, 1, static_cast<cudaStream_t>(stream));
 }
 
 nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_local,
-                              float* d_grad, float* d_loss_sum, void* stream) {
+                              float* d_grad, float* d_loss_sum, float* d_pred, void* stream) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
     if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
     if (!d_grad || !aligned(d_grad, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_backward: bad d_grad");
+    if (d_pred && !aligned(d_pred, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_backward: bad d_pred");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (n_local == 0) {  // contributes a zero gradient to the all-reduce
         NRC_CUDA(h, cudaMemsetAsync(d_grad, 0, sizeof(float) * size_t(h->wi.logical), st));
@@ -849,7 +689,7 @@ nrc_status nrc_train_backward(nrc_handle* h, const nrc_record* d_rec, const floa
     if ((s = check_train_args(h, d_rec, d_tgt, n_local, "nrc_train_backward")) != NRC_OK) return s;
     int np = 0;
     Gather g{false, 0, 0, 0, 0, 0};
-    if ((s = launch_train(h, d_rec, d_tgt, n_local, g, st, &np)) != NRC_OK) return s;
+    if ((s = launch_train_w(h, d_rec, d_tgt, n_local, g, st, &np, d_pred)) != NRC_OK) return s;
     return reduce_partials(h, np, d_grad, d_loss_sum, st);
 }
 
@@ -874,57 +714,48 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
     Gather g{true, 0, 0, 0, n_total, uint64_t(j) * l + row_begin};
     nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
     int np = 0;
-    if ((s = launch_train(h, d_rec, d_tgt, n, g, st, &np)) != NRC_OK) return s;
+    if ((s = launch_train_w(h, d_rec, d_tgt, n, g, st, &np)) != NRC_OK) return s;
     return reduce_partials(h, np, d_grad, d_loss_sum, st);
 }
 
-nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, void* stream) {
+nrc_status nrc_train_apply(nrc_handle* h, const float* d_grad_sum, uint32_t n_global, const float* d_loss_sum,
+                           float* d_loss, void* stream) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
     if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
     if (n_global == 0) return NRC_OK;
     if (!d_grad_sum || !aligned(d_grad_sum, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply: bad grad");
+    if ((d_loss_sum && !aligned(d_loss_sum, 4)) || (d_loss && !aligned(d_loss, 4)))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply: misaligned loss pointer");
     h->step += 1;
-    if (train_generic(h)) {
-        AdamWArgs aw = adam_w_args(h);
-        aw.grad_logical = d_grad_sum;
-        aw.apply = 1;
-        aw.inv_n = float(1.0 / double(n_global));
-        return launch_adam_w(h, aw, static_cast<cudaStream_t>(stream));
+    AdamWArgs aw = adam_w_args(h);
+    aw.grad_logical = d_grad_sum;
+    aw.apply = 1;
+    aw.inv_n = float(1.0 / double(n_global));
+    if (d_loss_sum && d_loss) {  // batch-mean loss = all-reduced loss sum / n_global (R10)
+        aw.loss_part = d_loss_sum;
+        aw.nloss = 1;
+        aw.loss_scale = aw.inv_n;
+        aw.loss_out = d_loss;
+    } else {
+        aw.loss_part = nullptr;
+        aw.nloss = 0;
     }
-    AdamArgs aa = adam_args(h);
-    aa.src = d_grad_sum;
-    aa.nsrc = 1;
-    aa.src_logical = 1;
-    aa.inv_n = float(1.0 / double(n_global));
-    aa.loss_out = nullptr;
-    nrc_adam_kernel<<<kParamPadded / 32, kRedThreads, 0, static_cast<cudaStream_t>(stream)>>>(aa);
-    NRC_LAUNCHED(h, "nrc_adam_kernel");
-    return NRC_OK;
+    return launch_adam_w(h, aw, static_cast<cudaStream_t>(stream));
 }
 
 static nrc_status train_frame_impl(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
                                    uint32_t s_, uint32_t l, uint64_t shuffle_seed, float* d_losses, Gather g,
                                    cudaStream_t st) {
-    nrc_status s = NRC_OK;
     if (uint64_t(s_) * l > n_total) l = n_total / s_;  // batches shrink proportionally
     if (l == 0) return NRC_OK;
     if (l > h->cfg.max_batch) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: l > max_batch");
     g.on = true;
     g.n = n_total;
+    g.offset = 0;
     nrc_lcg_params(n_total, shuffle_seed, &g.a, &g.c, &g.m);
-    uint32_t total = 0;
-    for (uint32_t j = 0; j < s_; j += kMaxFusedSteps) {  // one launch per <= 8 steps
-        const uint32_t k = (s_ - j) < uint32_t(kMaxFusedSteps) ? (s_ - j) : uint32_t(kMaxFusedSteps);
-        g.offset = uint64_t(j) * l;
-        if ((s = train_step_impl(h, d_rec, d_tgt, l, g, d_losses ? d_losses + j : nullptr, k, st)) != NRC_OK)
-            return s;
-        total += h->launches;
-        h->launches = 0;
-    }
-    h->launches = total;
-    return NRC_OK;
+    return train_steps(h, d_rec, d_tgt, l, g, d_losses, s_, st);
 }
 
 nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total, uint32_t s_,
@@ -936,36 +767,12 @@ nrc_status nrc_train_frame(nrc_handle* h, const nrc_record* d_rec, const float* 
     if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
     if (!d_rec || !d_tgt || !aligned(d_rec, 16) || !aligned(d_tgt, 4))
         return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: NULL or misaligned pointer");
+    if (d_losses && !aligned(d_losses, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame: misaligned d_losses");
     Gather g{true, 0, 0, 0, n_total, 0};
     return train_frame_impl(h, d_rec, d_tgt, n_total, s_, l, shuffle_seed, d_losses, g,
                             static_cast<cudaStream_t>(stream));
 }
 
-nrc_status nrc_train_frame_parts(nrc_handle* h, const nrc_record* const* rec_parts, const float* const* tgt_parts,
-                                 uint32_t n_parts, uint32_t n_per_part, uint32_t s_, uint32_t l,
-                                 uint64_t shuffle_seed, float* d_losses, void* stream) {
-    nrc_status s = check_handle(h);
-    if (s != NRC_OK) return s;
-    if ((s = check_train_width(h)) != NRC_OK) return s;
-    h->launches = 0;
-    if (!rec_parts || !tgt_parts || n_parts == 0 || n_parts > uint32_t(kMaxParts))
-        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_parts: 1..8 parts required");
-    const uint64_t n_total = uint64_t(n_parts) * n_per_part;
-    if (n_total == 0 || s_ == 0 || l == 0) return NRC_OK;
-    if (n_total > 0xFFFFFFFFull) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_parts: too many records");
-    Gather g{true, 0, 0, 0, n_total, 0};
-    g.n_parts = n_parts;
-    g.part_n = n_per_part;
-    for (uint32_t p = 0; p < n_parts; ++p) {
-        if (!rec_parts[p] || !tgt_parts[p] || !aligned(rec_parts[p], 16) || !aligned(tgt_parts[p], 4))
-            return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_parts: NULL or misaligned part pointer");
-        g.rec_parts[p] = reinterpret_cast<const float*>(rec_parts[p]);
-        g.tgt_parts[p] = tgt_parts[p];
-    }
-    // d_rec / d_tgt are unused in peer mode (every row resolves to a part)
-    return train_frame_impl(h, rec_parts[0], tgt_parts[0], uint32_t(n_total), s_, l, shuffle_seed, d_losses, g,
-                            static_cast<cudaStream_t>(stream));
-}
 
 nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
                                    uint32_t s_, uint32_t l, uint64_t shuffle_seed, uint32_t rank, uint32_t world,
@@ -974,7 +781,7 @@ nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const
     if (s != NRC_OK) return s;
     if ((s = check_train_width(h)) != NRC_OK) return s;
     h->launches = 0;
-    if (world == 0 || world > uint32_t(kMaxParts) || rank >= world || !peer_state)
+    if (world == 0 || world > uint32_t(kMaxRanks) || rank >= world || !peer_state)
         return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_dp_peer: 1..8 ranks, rank < world, peer_state");
     if (peer_state[rank] != h->state)
         return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_frame_dp_peer: peer_state[rank] must be this cache's arena");
@@ -989,8 +796,6 @@ nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const
     const uint32_t T = (l + kTile - 1) / kTile;  // tiles per step
     if (T > uint32_t(kMaxDpTiles) || int(T) > h->num_sms)
         return fail(h, NRC_ERR_UNSUPPORTED, "nrc_train_frame_dp_peer: at most 128 tiles (16,384 rows) per step");
-    if (train_generic(h) == false)
-        return fail(h, NRC_ERR_UNSUPPORTED, "nrc_train_frame_dp_peer: not with NRC_TRAIN_FUSED=1");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto t_lo = [&](uint32_t k) { return k * T / world; };  // rank k owns tiles [t_lo(k), t_lo(k + 1))
     Gather g{true, 0, 0, 0, n_total, 0};
@@ -1114,10 +919,10 @@ nrc_status nrc_encode(nrc_handle* h, const nrc_record* d_rec, uint64_t n, uint16
     const unsigned blocks = unsigned((n + 127) / 128);
     if (h->ep.exact)
         nrc_encode_kernel<true><<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-            reinterpret_cast<const float*>(d_rec), n, h->ep, reinterpret_cast<uint4*>(d_out));
+            reinterpret_cast<const float*>(d_rec), n, h->ep, reinterpret_cast<uint4*>(d_out), h->d_counters() + 2);
     else
         nrc_encode_kernel<false><<<blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-            reinterpret_cast<const float*>(d_rec), n, h->ep, reinterpret_cast<uint4*>(d_out));
+            reinterpret_cast<const float*>(d_rec), n, h->ep, reinterpret_cast<uint4*>(d_out), h->d_counters() + 2);
     NRC_LAUNCHED(h, "nrc_encode_kernel");
     return NRC_OK;
 }
@@ -1185,17 +990,8 @@ nrc_status nrc_set_params(nrc_handle* h, nrc_param_set which, const float* h_in,
     return NRC_OK;
 }
 
-nrc_status nrc_query_image(nrc_handle* h, void** d_image, size_t* bytes) {
-    nrc_status s = check_handle(h);
-    if (s != NRC_OK) return s;
-    if (!d_image || !bytes) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_query_image: NULL output");
-    const bool raw = (h->cfg.flags & NRC_QUERY_RAW_WEIGHTS) || h->cfg.ema_alpha == 0.0f;
-    *d_image = raw ? h->d_wimg() : h->d_eimg();
-    *bytes = size_t(h->wi.img);
-    return NRC_OK;
-}
-
-nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets) {
+nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grads, uint64_t* nonfinite_targets,
+                         uint64_t* degenerate_vectors) {
     nrc_status s = check_handle(h);
     if (s != NRC_OK) return s;
     unsigned long long c[4] = {0, 0, 0, 0};
@@ -1204,6 +1000,7 @@ nrc_status nrc_get_stats(nrc_handle* h, uint64_t* step, uint64_t* nonfinite_grad
     if (step) *step = h->step;
     if (nonfinite_grads) *nonfinite_grads = c[0];
     if (nonfinite_targets) *nonfinite_targets = c[1];
+    if (degenerate_vectors) *degenerate_vectors = c[2];
     return NRC_OK;
 }
 

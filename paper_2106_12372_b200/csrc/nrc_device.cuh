@@ -376,32 +376,14 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ float rsqrt_approx(float x) {
-    float r;
-    asm("rsqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
 __device__ __forceinline__ float ex2_approx(float x) {
     float r;
     asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-// acos(z), |error| <= 2.4e-7 rad in fp32 (Abramowitz & Stegun 4.4.46, 8 terms).
-__device__ __forceinline__ float acos_fast(float z) {
-    const float a = fabsf(z);
-    float p = -0.0012624911f;
-    p = fmaf(p, a, 0.0066700901f);
-    p = fmaf(p, a, -0.0170881256f);
-    p = fmaf(p, a, 0.0308918810f);
-    p = fmaf(p, a, -0.0501743046f);
-    p = fmaf(p, a, 0.0889789874f);
-    p = fmaf(p, a, -0.2145988016f);
-    p = fmaf(p, a, 1.5707963050f);
-    const float r = sqrt_approx(1.0f - a) * p;
-    return z < 0.0f ? 3.14159265358979323846f - r : r;
-}
-// atan2(y, x) with IEEE sign conventions (atan2(+-0, x<0) = +-pi), |error| <=
-// 1.2e-7 rad: atan(a) = a P(a^2) on [0,1] (degree-7 minimax fit, fp32 Horner).
+// atan2(y, x) with IEEE sign conventions (atan2(+-0, x<0) = +-pi, atan2(+-0,
+// -0) = +-pi: the sign bit of x decides), |error| <= 1.2e-7 rad: atan(a) =
+// a P(a^2) on [0,1] (degree-7 minimax fit, fp32 Horner).
 __device__ __forceinline__ float atan2_fast(float y, float x) {
     const float ax = fabsf(x), ay = fabsf(y);
     const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
@@ -417,25 +399,27 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
     p = fmaf(p, s, 0.9999993443489075f);
     float r = a * p;
     if (ay > ax) r = 1.57079632679489662f - r;
-    if (x < 0.0f) r = 3.14159265358979323846f - r;
+    if (__float_as_uint(x) >> 31) r = 3.14159265358979323846f - r;
     return copysignf(r, y);
 }
-// sph (Table 1 caption; reading R7): (acos(z)/pi, (atan2(y,x)+pi)/(2 pi))
-__device__ __forceinline__ void sph_f(float x, float y, float z, float& th, float& ph) {
-    const float l2 = x * x + y * y + z * z;
-    if (!(l2 > 0.0f)) {
+// sph (Table 1 caption; reading R7): (acos(u_z / |u|)/pi,
+// (atan2(u_y, u_x) + pi)/(2 pi)), computed without normalising u:
+// acos(z / |u|) = atan2(sqrt(x^2 + y^2), z) for u != 0 (the same angle, but
+// well conditioned at the poles, where acos of a rounded z / |u| is not:
+// d acos / dz = -1 / sin(theta)).  Returns 1 for a zero-length (degenerate)
+// vector, read as (0,0,1) and counted.
+__device__ __forceinline__ uint32_t sph_f(float x, float y, float z, float& th, float& ph) {
+    const float r2 = x * x + y * y;
+    const float l2 = fmaf(z, z, r2);
+    const uint32_t degenerate = !(l2 > 0.0f) ? 1u : 0u;
+    if (degenerate) {
         x = 0.0f;
         y = 0.0f;
         z = 1.0f;
-    } else {
-        const float il = rsqrt_approx(l2);
-        x *= il;
-        y *= il;
-        z *= il;
     }
-    z = fminf(fmaxf(z, -1.0f), 1.0f);
-    th = acos_fast(z) * 0.318309886183790672f;                                  // 1/pi
+    th = atan2_fast(sqrt_approx(degenerate ? 0.0f : r2), z) * 0.318309886183790672f;  // 1/pi
     ph = (atan2_fast(y, x) + 3.14159265358979323846f) * 0.159154943091895336f;  // 1/(2 pi)
+    return degenerate;
 }
 
 // Encodes one record into 64 fp16 features packed as 32 f16x2 words, in the
@@ -444,7 +428,7 @@ __device__ __forceinline__ void sph_f(float x, float y, float z, float& th, floa
 // Exact primitives (readings R21/R22): sin(pi 2^d v) with
 // sinpif's exact range reduction (2^d v is exact in fp32), and the Gaussian
 // one-blob exp(-x^2/2)/sqrt(2 pi) at the bin centres.
-__device__ __forceinline__ void encode_record_exact(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
+__device__ __forceinline__ uint32_t encode_record_exact(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
     float e[64];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -462,10 +446,10 @@ __device__ __forceinline__ void encode_record_exact(const float* rec, const Enco
         }
     };
     float th, ph;
-    sph_f(rec[3], rec[4], rec[5], th, ph);
+    uint32_t deg = sph_f(rec[3], rec[4], rec[5], th, ph);
     ob(th, e + 36);
     ob(ph, e + 40);
-    sph_f(rec[6], rec[7], rec[8], th, ph);
+    deg += sph_f(rec[6], rec[7], rec[8], th, ph);
     ob(th, e + 44);
     ob(ph, e + 48);
     ob(1.0f - ex2_approx(-1.44269504088896341f * fmaxf(rec[9], 0.0f)), e + 52);
@@ -475,20 +459,22 @@ __device__ __forceinline__ void encode_record_exact(const float* rec, const Enco
     e[63] = 1.0f;
 #pragma unroll
     for (int j = 0; j < 32; ++j) h[j] = pack_h2(e[2 * j], e[2 * j + 1]);
+    return deg;
 }
 
-__device__ __forceinline__ void encode_record_cheap(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]);
+__device__ __forceinline__ uint32_t encode_record_cheap(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]);
 // EXACT selects the primitives at compile time (kernels are instantiated per
 // variant, so the cheap path carries no trace of the exact one).
+// Returns the number (0..2) of zero-length direction / normal vectors (R7).
 template <bool EXACT = false>
-__device__ __forceinline__ void encode_record(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
+__device__ __forceinline__ uint32_t encode_record(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
     if constexpr (EXACT) {
-        encode_record_exact(rec, ep, h);
+        return encode_record_exact(rec, ep, h);
     } else {
-        encode_record_cheap(rec, ep, h);
+        return encode_record_cheap(rec, ep, h);
     }
 }
-__device__ __forceinline__ void encode_record_cheap(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
+__device__ __forceinline__ uint32_t encode_record_cheap(const float* rec, const EncodeParams& ep, uint32_t (&h)[32]) {
     float e[64];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -505,10 +491,10 @@ __device__ __forceinline__ void encode_record_cheap(const float* rec, const Enco
         }
     }
     float th, ph;
-    sph_f(rec[3], rec[4], rec[5], th, ph);
+    uint32_t deg = sph_f(rec[3], rec[4], rec[5], th, ph);
     one_blob4(th, e + 36);
     one_blob4(ph, e + 40);
-    sph_f(rec[6], rec[7], rec[8], th, ph);
+    deg += sph_f(rec[6], rec[7], rec[8], th, ph);
     one_blob4(th, e + 44);
     one_blob4(ph, e + 48);
     one_blob4(1.0f - ex2_approx(-1.44269504088896341f * fmaxf(rec[9], 0.0f)), e + 52);  // 1 - e^{-r}
@@ -518,6 +504,7 @@ __device__ __forceinline__ void encode_record_cheap(const float* rec, const Enco
     e[63] = 1.0f;
 #pragma unroll
     for (int j = 0; j < 32; ++j) h[j] = pack_h2(e[2 * j], e[2 * j + 1]);
+    return deg;
 }
 
 // Writes a packed 64-feature row into line `row` of a SWIZZLE_128B tile.

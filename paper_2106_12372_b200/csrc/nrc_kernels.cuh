@@ -1,96 +1,23 @@
 // nrc_kernels.cuh -- the sm_100a kernels of libnrc.
 //
-//   nrc_query_kernel   fused encode -> 6 x tcgen05 layer -> factorised output
-//                      (P:L602-628 fully fused MLP; Table 1)
-//   nrc_train_kernel   fused encode -> forward (stash kept in SMEM) -> relative
-//                      L2 loss gradient (Eq. 5) -> dgrad -> wgrad (both on
-//                      tcgen05, accumulators in TMEM) -> per-CTA fp32 partials
-//                      (where the paper used CUTLASS split-k)
-//   nrc_adam_kernel    deterministic partial reduction + Adam + EMA (Eq. 2) +
-//                      fp16 operand images
-//   helpers            encode-only, partial reduction, image refresh, selftest
+//   nrc_query_ts_kernel  fused encode -> tcgen05 layers (activations in TMEM)
+//                        -> factorised output (P:L602-628 fully fused MLP;
+//                        P:L874-878; Table 1)             nrc_query_ts.cuh
+//   nrc_train_w_kernel   LCG gather -> encode -> forward (stash in SMEM) ->
+//                        relative L2 loss gradient (Eq. 5) -> dgrad + wgrad on
+//                        tcgen05 -> per-CTA fp32 partials (where
+//                        the paper used CUTLASS split-k)   nrc_train_w.cuh
+//   nrc_adam_w_kernel    deterministic partial reduction + Adam + EMA (Eq. 2)
+//                        + fp16 operand images nrc_train_w.cuh
+//   helpers (here)       image refresh, self-training targets, encode-only,
+//                        tcgen05 layout selftest
 #pragma once
 #include "nrc_device.cuh"
-#include "nrc_fused_query.cuh"
+#include "nrc_common.cuh"
 #include "nrc_query_ts.cuh"
-#include "nrc_train.cuh"
 #include "nrc_train_w.cuh"
 
 namespace nrc {
-
-// ============================================================================ Adam + EMA
-struct AdamArgs {
-    const float* src;        // gradient source
-    int nsrc;                // number of padded partials (src_logical == 0)
-    int src_logical;         // 1: src is a single logical-layout gradient sum
-    float inv_n;             // 1 / N (batch mean, R10/R13)
-    float *w, *m, *v, *ema;  // fp32 padded arrays
-    uint8_t *wimg, *eimg;    // fp16 operand images
-    float lr, b1, b2, eps, inv_bc1, inv_bc2;
-    float ema_c1, ema_c2;    // W-bar = c1 W + c2 W-bar (Eq. 2 / R12)
-    unsigned long long* bad_grads;
-    const float* loss_part;  // optional: loss partial sums
-    int nloss;
-    float loss_scale;
-    float* loss_out;
-};
-
-__device__ __forceinline__ int logical_index(int layer, int row, int col) {
-    if (layer < 5) return layer_off(layer) + row * 64 + col;
-    return row < 3 ? 20480 + row * 64 + col : -1;
-}
-
-// Block-level fixed-order sum of partials[p][j] over p < np for the 32
-// parameters j = 32*blockIdx.x + lane: warp w sums p = w, w+8, ... in
-// ascending order, then warp 0 adds the 8 warp sums in warp order.  The same
-// order in nrc_adam_kernel and nrc_reduce_kernel keeps nrc_train_step and
-// nrc_train_backward + nrc_train_apply bitwise identical.
-constexpr int kRedThreads = 256;
-constexpr int kRedWarps = kRedThreads / 32;
-__device__ __forceinline__ float block_partial_sum(const float* __restrict__ partials, int np, int j) {
-    __shared__ float sred[kRedWarps][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float s = 0.0f;
-    const float* p0 = partials + j;
-#pragma unroll 4
-    for (int p = w; p < np; p += kRedWarps) s += __ldcg(p0 + size_t(p) * kParamPadded);
-    sred[w][lane] = s;
-    __syncthreads();
-    float t = 0.0f;
-    if (w == 0) {
-#pragma unroll
-        for (int k = 0; k < kRedWarps; ++k) t += sred[k][lane];
-    }
-    return t;
-}
-__device__ __forceinline__ float warp_loss_sum(const float* __restrict__ part, int np) {
-    float s = 0.0f;
-    for (int p = threadIdx.x & 31; p < np; p += 32) s += part[p];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    return s;
-}
-
-// grid = kParamPadded / 32 blocks of kRedThreads; warp 0 updates 32 parameters.
-__global__ void __launch_bounds__(kRedThreads) nrc_adam_kernel(AdamArgs a) {
-    pdl_wait();  // launched as a programmatic dependent of the train kernel
-    const int j = blockIdx.x * 32 + (threadIdx.x & 31);
-    int layer, row, col;
-    padded_coords(j, layer, row, col);
-    float g = 0.0f;
-    if (!a.src_logical) g = block_partial_sum(a.src, a.nsrc, partial_index(layer, row, col));
-    if (threadIdx.x >= 32) return;
-    if (blockIdx.x == 0 && a.loss_out != nullptr) {
-        const float s = warp_loss_sum(a.loss_part, a.nloss);
-        if (threadIdx.x == 0) *a.loss_out = s * a.loss_scale;
-    }
-    if (a.src_logical) {
-        const int li = logical_index(layer, row, col);
-        g = li >= 0 ? a.src[li] : 0.0f;
-    }
-    const OptParams op{a.lr, a.b1, a.b2, a.eps, a.inv_bc1, a.inv_bc2, a.ema_c1, a.ema_c2};
-    adam_ema_update(j, g * a.inv_n, op, a.w, a.m, a.v, a.ema, a.wimg, a.eimg, a.bad_grads);
-}
 
 // fp32 padded array -> fp16 operand image at hidden width W and depth nh.
 template <int W>
@@ -101,27 +28,6 @@ __global__ void nrc_image_w_kernel(const float* __restrict__ w, uint8_t* __restr
     const int i = D.layer_of(j);
     const int rel = j - D.pad_off(i), r = rel / D.cols(i), c = rel % D.cols(i);
     *reinterpret_cast<__half*>(img + D.img_byte(i, r, c)) = __float2half_rn(w[j]);
-}
-
-// Sum the per-CTA partials in fixed order into a logical-layout gradient
-// (nrc_train_backward), plus the loss sum.
-// grid = kParamPadded / 32 blocks of kRedThreads (same order as Adam's sum).
-__global__ void __launch_bounds__(kRedThreads) nrc_reduce_kernel(const float* __restrict__ partials, int np,
-                                                                 float* __restrict__ grad,
-                                                                 const float* __restrict__ loss_part,
-                                                                 float* loss_sum) {
-    pdl_wait();
-    const int j = blockIdx.x * 32 + (threadIdx.x & 31);
-    int layer, row, col;
-    padded_coords(j, layer, row, col);
-    const float g = block_partial_sum(partials, np, partial_index(layer, row, col));
-    if (threadIdx.x >= 32) return;
-    if (blockIdx.x == 0 && loss_sum != nullptr) {
-        const float s = warp_loss_sum(loss_part, np);
-        if (threadIdx.x == 0) *loss_sum = s;
-    }
-    const int li = logical_index(layer, row, col);
-    if (li >= 0) grad[li] = g;
 }
 
 // Self-training targets (nrc_assemble_targets): one thread per training path,
@@ -150,15 +56,22 @@ __global__ void nrc_targets_kernel(const uint32_t* __restrict__ first, const uin
 
 // Encoding only (nrc_encode): one thread per record, logical feature order.
 template <bool EXACT>
-__global__ void nrc_encode_kernel(const float* __restrict__ rec, uint64_t n, EncodeParams ep, uint4* __restrict__ out) {
+__global__ void nrc_encode_kernel(const float* __restrict__ rec, uint64_t n, EncodeParams ep, uint4* __restrict__ out,
+                                  unsigned long long* degenerate) {
+    __shared__ uint32_t scratch;
+    if (threadIdx.x == 0) scratch = 0;
+    __syncthreads();
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float r[16];
-    load_record_global(rec + i * kRecFloats, r);
-    uint32_t h[32];
-    encode_record<EXACT>(r, ep, h);
+    uint32_t deg = 0;
+    if (i < n) {
+        float r[16];
+        load_record_global(rec + i * kRecFloats, r);
+        uint32_t h[32];
+        deg = encode_record<EXACT>(r, ep, h);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) out[i * 8 + c] = make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+        for (int c = 0; c < 8; ++c) out[i * 8 + c] = make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+    }
+    block_count_add(degenerate, deg, &scratch);
 }
 
 // ============================================================================ selftest

@@ -3,8 +3,8 @@
 //
 // Why: with the A operand in shared memory, every 128-row layer moves
 // 40 KB through the SM's shared-memory port (MMA reads A 16 KB + W 8 KB, the
-// epilogue writes A 16 KB), ~250 KB per tile, which bounds the SMEM variant
-// (nrc_fused_query.cuh) at ~2k cycles per tile.  Here the encoder and the
+// epilogue writes A 16 KB), ~250 KB per tile, which bounded a round-1 SMEM
+// variant at ~2k cycles per tile.  Here the encoder and the
 // ReLU epilogue write the fp16 activations straight into tensor memory
 // (tcgen05.st) and the MMA reads A from TMEM (".kind::f16 [d], [a], b_desc"),
 // so shared memory only feeds the 8 KB weight tile per layer.
@@ -14,7 +14,7 @@
 // columns.  Layer L reads A at column a and writes D; its epilogue reads D
 // and writes the next A over the dead A (same columns).
 #pragma once
-#include "nrc_fused_query.cuh"
+#include "nrc_common.cuh"
 
 namespace nrc {
 
@@ -85,8 +85,11 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     uint64_t* mma_bar = &bars[1 + (S + 1) * g];  // [S]
     uint64_t* rec_bar = &bars[1 + (S + 1) * g + S];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + (S + 1) * G);
+    uint32_t* deg_scratch = tmem_slot + 1;
+    uint32_t deg = 0;  // zero-length omega / n vectors this thread encoded
 
     if (tid == 0) {
+        *deg_scratch = 0;
         for (int i = 0; i < 1 + (S + 1) * G; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
@@ -190,7 +193,8 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
         for (int c = 0; c < 3; ++c) fac[s][c] = (args.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
         {
             uint32_t h[32];
-            encode_record<EXACT>(rec, args.ep, h);
+            const uint32_t dg = encode_record<EXACT>(rec, args.ep, h);
+            deg += valid ? dg : 0u;
             tmem_st32(a_col(s) + lane_off, h);  // includes tcgen05.wait::st
         }
         fence_async_smem();  // record reads before the next TMA overwrite
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
         for (int s = 1; s < S; ++s) any = any || active[s];
     }
     tc_fence_before();
-    __syncthreads();
+    block_count_add(args.degenerate, deg, deg_scratch);  // includes __syncthreads
     if (warp == 0) tmem_dealloc(tmem_base, 512);
 #undef TQ
 #undef TQI

@@ -1,11 +1,10 @@
-// nrc_train_w.cuh -- training at hidden width W in {32, 64, 128} (width
-// ablation, BASELINE.json configs[3] "32/64/128-neuron hidden layers at 1080p
-// query+train").  The same rows a0, a1, a4-a8 of SURVEY 8(a) as
-// nrc_train.cuh (LCG gather P:L487-491 -> encode -> forward with the stash in
-// SMEM -> Eq. 5 loss gradient P:L886-894 -> dgrad + wgrad on tcgen05,
-// P:L662-667), as one partials kernel per step followed by the reduce + Adam +
-// EMA kernel (Eq. 2).  The width-64 product path keeps its fused
-// persistent kernel; this one trades the grid barriers for width generality.
+// nrc_train_w.cuh -- the training step at hidden width W in {32, 64, 128}
+// (64 = the paper's network; 32 / 128 = the width ablation, BASELINE.json
+// configs[3]): rows a0, a1, a4-a8 of SURVEY 8(a) (LCG gather
+// P:L487-491 -> encode -> forward with the stash in SMEM -> Eq. 5 loss
+// gradient P:L886-894 -> dgrad + wgrad on tcgen05), as one
+// partials kernel per step followed by the reduce + Adam + EMA kernel
+// (Eq. 2).
 //
 // Layout per CTA (one 128-row tile at a time, 4 row warps, warp 0 issues):
 //  * stash: h0 (128 x 64 fp16) and h1..h5 (128 x W fp16, W/64 blocks of
@@ -27,7 +26,7 @@
 //               M = 128 (W = 128, j < 5) else 64 (rows beyond W / 16 are 0)
 //               N = 64 (j = 0) else max(W, 64) (columns beyond W are 0)
 #pragma once
-#include "nrc_train.cuh"
+#include "nrc_common.cuh"
 
 namespace nrc {
 
@@ -44,7 +43,7 @@ struct TrainW {
     }
     __host__ __device__ static constexpr int stash_bytes(int nh) { return kTileBytes + nh * kKB * kTileBytes; }
     __host__ __device__ static constexpr int smem_bytes(int nh) {
-        return 1024 + w_bytes(nh) + stash_bytes(nh) + kTileBytes + 64;
+        return 1024 + w_bytes(nh) + stash_bytes(nh) + kTileBytes + 96;
     }
     static constexpr uint32_t kTmemCols = 3 * kNW <= 256 ? 256u : 512u;
     __host__ __device__ static constexpr int slot_off(int i) { return i == 0 ? 0 : kTileBytes + (i - 1) * kKB * kTileBytes; }
@@ -59,20 +58,14 @@ static_assert(TrainW<32>::smem_bytes(TrainW<32>::kMaxNh) <= 232448 &&
 // between 64-wide MN blocks of an MN-major operand, SBO = 8 lines = 1024 B).
 __device__ __forceinline__ uint64_t desc_mn_lbo(uint32_t saddr, uint32_t lbo) { return make_sdesc(saddr, lbo, 1024u); }
 
-// record + target of batch row `row` (zeros past the batch; LCG gather or
-// peer parts as in nrc_train_kernel)
+// record + target of batch row `row` (zeros past the batch; row k of the
+// step reads record lcg_perm(offset + k) when gathering, R15)
 __device__ __forceinline__ void train_gather_row(const TrainArgs& a, uint32_t row, float (&rec)[16], float (&tg)[3]) {
     if (row < a.n) {
         const uint64_t k = row;
         const uint64_t idx = a.gather ? lcg_perm(a.offset + k, a.lcg_n, a.lcg_a, a.lcg_c, a.lcg_m) : k;
         const float* rsrc = a.rec + idx * kRecFloats;
         const float* tsrc = a.tgt + idx * 3;
-        if (a.n_parts > 0) {
-            const uint32_t p = uint32_t(idx / a.part_n);
-            const uint64_t o = idx - uint64_t(p) * a.part_n;
-            rsrc = a.rec_parts[p] + o * kRecFloats;
-            tsrc = a.tgt_parts[p] + o * 3;
-        }
         load_record_global(rsrc, rec);
 #pragma unroll
         for (int c = 0; c < 3; ++c) tg[c] = __ldg(tsrc + c);
@@ -111,8 +104,11 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     uint64_t* mma_bar = &bars[1];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
     float* red = reinterpret_cast<float*>(bars + 3);  // 4 floats + 4 u32
+    uint32_t* gmax = reinterpret_cast<uint32_t*>(bars + 7);  // per-warp max |dL/dy| (fp32 bits)
+    uint32_t* deg_scratch = reinterpret_cast<uint32_t*>(bars + 9);
 
     if (tid == 0) {
+        *deg_scratch = 0;
         mbar_init(wbar, 1);
         mbar_init(mma_bar, 1);
         fence_mbar_init();
@@ -219,7 +215,9 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         __syncwarp();
     };
     float* part = a.partials + size_t(blockIdx.x) * D.padded();
-    // drain G_j (TMEM) into this CTA's partial (plain store on the first tile, else add)
+    // drain G_j (TMEM) into this CTA's partial (plain store on the first tile,
+    // else add), undoing the tile's power-of-two dL/dy scale (exact in fp32)
+    float inv_s = 1.0f;
     auto flush_g = [&](int j, bool first) {
         const int M = wg_m(j);
         const int o = M == 128 ? int(r) : int(warp) * 16 + int(lane);
@@ -235,8 +233,8 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
                 float4* dst = reinterpret_cast<float4*>(part + D.pad_off(j) + o * D.cols(j) + 32 * p);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    float4 x = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                           __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                    float4 x = make_float4(__uint_as_float(v[4 * q]) * inv_s, __uint_as_float(v[4 * q + 1]) * inv_s,
+                                           __uint_as_float(v[4 * q + 2]) * inv_s, __uint_as_float(v[4 * q + 3]) * inv_s);
                     if (!first) {
                         const float4 y = dst[q];
                         x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
@@ -264,7 +262,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     };
 
     float loss_sum = 0.0f;
-    uint32_t bad = 0;
+    uint32_t bad = 0, deg = 0;
     const uint32_t ntiles = (a.n + kTile - 1) / kTile;
     pdl_trigger();  // the optimiser kernel may launch (its griddepcontrol.wait covers this grid)
     bool first = true;
@@ -277,7 +275,8 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         train_gather_row(a, row, rec, tg);
         {
             uint32_t h[32];
-            encode_record<EXACT>(rec, a.ep, h);
+            const uint32_t dg = encode_record<EXACT>(rec, a.ep, h);
+            deg += valid ? dg : 0u;
             store_row_swz(slot(0), r, h);
         }
         if (first) {
@@ -337,6 +336,29 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
                 gy[c] = use ? 2.0f * d * f[c] * inv3den : 0.0f;
             }
             if (use) loss_sum += l * inv3den;
+            if (a.pred != nullptr && valid) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) a.pred[size_t(row) * 3 + c] = yh[c];
+            }
+            // Per-tile power-of-two scale of dL/dy before the fp16 rounding
+            // (R13, R25): the tile's largest |dL/dy| maps into [2^7, 2^8), so
+            // HDR residuals (|dL/dy| up to ~1e7 at eps = 0.01) cannot overflow
+            // fp16 and small ones keep full precision; undone exactly in fp32
+            // when the weight gradients are drained (flush_g).
+            {
+                const uint32_t mx = __reduce_max_sync(
+                    0xffffffffu, max(max(__float_as_uint(fabsf(gy[0])), __float_as_uint(fabsf(gy[1]))),
+                                     __float_as_uint(fabsf(gy[2]))));
+                if (lane == 0) gmax[warp] = mx;
+                named_bar_sync(1, 128);
+                const uint32_t tm = max(max(gmax[0], gmax[1]), max(gmax[2], gmax[3]));
+                const int ex = int(tm >> 23);                  // biased exponent of the tile max
+                const int k = min(max(134 - ex, -120), 120);   // 2^k * max in [2^7, 2^8)
+                const float sc = __uint_as_float(uint32_t(127 + k) << 23);
+                inv_s = __uint_as_float(uint32_t(127 - k) << 23);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) gy[c] *= sc;
+            }
             st_shared_v4(sG6_a + swz(r, 0), pack_h2(gy[0], gy[1]), pack_h2(gy[2], 0.0f), 0u, 0u);
         }
         sync_rows();
@@ -394,6 +416,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         if (nb) atomicAdd(a.bad_targets, (unsigned long long)nb);
     }
     NRC_WTRC(6);
+    block_count_add(a.degenerate, deg, deg_scratch);
     if (warp == 0) tmem_dealloc(tmem_base, T::kTmemCols);
 }
 #undef NRC_WTRC
@@ -544,7 +567,7 @@ __global__ void __launch_bounds__(kAdamGroups * 256, 2) nrc_adam_w_kernel(AdamWA
 // have published step `target / world` (acquire).  Bounded: after ~20 s it
 // gives up and counts a timeout instead of hanging the GPU.
 struct DpPeers {
-    unsigned long long* ctr[kMaxParts];  // every rank's hand-off counter (own included)
+    unsigned long long* ctr[kMaxRanks];  // every rank's hand-off counter (own included)
 };
 __global__ void nrc_dp_exchange_kernel(DpPeers peers, int world, unsigned long long* own, unsigned long long target,
                                        unsigned long long* timeouts) {

@@ -59,66 +59,19 @@ class DataParallelFrame:
         self.loss_sum = self.buf[NPARAM:]
         self.last_launch_count = 0
 
-    def replica_checksum(self, image_only: bool = False) -> int:
-        """CRC32 of this rank's fp32 training and EMA parameters (host copy), or
-        of the fp16 image the query reads (image_only: the state a query-only
-        rank of the dedicated mode keeps in sync)."""
+    def replica_checksum(self) -> int:
+        """CRC32 of this rank's fp32 training and EMA parameters (host copy)."""
         import zlib
-        if image_only:
-            return zlib.crc32(self.cache.query_image().cpu().numpy().tobytes())
         w = self.cache.get_params("train")
         e = self.cache.get_params("ema")
         return zlib.crc32(w.tobytes() + e.tobytes())
 
-    def dedicated_query_rows(self, n: int, share0: float = 0.0) -> Tuple[int, int]:
-        """Dedicated mode: rank 0 trains and queries the first round(share0 n)
-        rows (0 by default; a small share balances P = 2, where the single
-        query rank would otherwise wait longest); ranks 1..P-1 split the rest."""
-        n0 = int(round(min(max(share0, 0.0), 1.0) * n))
-        if self.rank == 0:
-            return 0, n0
-        lo, hi = shard(n - n0, self.rank - 1, self.world - 1)
-        return n0 + lo, n0 + hi
-
-    @staticmethod
-    def dedicated_share0(query_time_one_gpu: float, train_time: float, world: int) -> float:
-        """Rank 0's query share that equalises t_train + f T_q (rank 0) with
-        (1 - f) T_q / (P - 1) (the other ranks); 0 when the training alone is
-        the longer part (P >= 3 at the paper's sizes)."""
-        if world < 2 or query_time_one_gpu <= 0:
-            return 0.0
-        f = (query_time_one_gpu - (world - 1) * train_time) / (world * query_time_one_gpu)
-        return float(min(max(f, 0.0), 0.9))
-
-    def frame_dedicated(self, records_query_local: torch.Tensor, out: torch.Tensor, records: torch.Tensor,
-                        targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
-                        losses: Optional[torch.Tensor] = None, stream=None):
-        """One frame with the work split by function: rank 0
-        runs the whole frame's training (the latency-bound part, which more
-        GPUs cannot shorten), ranks 1..P-1 run the frame's query on their row
-        shards with the previous frame's W-bar -- the order of the paper's frame
-        (the query reads W-bar from before this frame's training) --
-        and then rank 0's new query image is broadcast to every rank.  Results
-        equal the single-GPU frame sequence bitwise (same kernels, same data)."""
-        if self.world < 2:
-            raise ValueError("the dedicated mode needs at least two ranks")
-        launches = 0
-        if records_query_local.shape[0] > 0:  # the previous frame's W-bar
-            self.cache.query(records_query_local, out, stream=stream)
-            launches += getattr(self.cache, "last_launch_count", 0)
-        if self.rank == 0:
-            self.cache.train_frame(records, targets, s, l, shuffle_seed, losses)
-            launches += getattr(self.cache, "last_launch_count", 0)
-        dist.broadcast(self.cache.query_image(), src=0, group=self.group)
-        self.last_launch_count = launches
-        return out
-
-    def verify_replicas(self, image_only: bool = False) -> int:
+    def verify_replicas(self) -> int:
         """every rank holds a bitwise-identical replica (same seeded
         init, identical reduced gradients or identical gathered data, the same
         deterministic kernels).  Gathers every rank's checksum and raises if
         any differs; returns the common checksum."""
-        mine = self.replica_checksum(image_only)
+        mine = self.replica_checksum()
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine, group=self.group)
         if any(c != mine for c in everyone):
@@ -133,68 +86,51 @@ class DataParallelFrame:
         return self.cache.query(records_local, out, stream=stream)
 
     def train_frame_replicated(self, records_local: torch.Tensor, targets_local: torch.Tensor, s: int, l: int,
-                               shuffle_seed: int, losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+                               shuffle_seed: int, losses: Optional[torch.Tensor] = None,
+                               counts=None) -> Optional[torch.Tensor]:
         """SURVEY 8(f) N3 variant (i): each rank owns the training records of its
-        screen region; one all-gather per frame (rank order) assembles the
-        frame's records on every rank, then every rank runs the whole frame's
-        training (fused nrc_train_frame) on identical data -- bitwise-identical
+        screen region; one all-gather per frame assembles the frame's records
+        in rank order on every rank, then every rank runs the whole frame's
+        training (nrc_train_frame) on identical data -- bitwise-identical
         replicas with no per-step collective (the kernels are deterministic).
-        Every rank must pass the same number of records."""
+        Ranks may hold different record counts (e.g. 65,536 over 3 ranks): the
+        counts are exchanged, every part is padded to the largest for the
+        collective, and the padding is dropped before training.  `counts`
+        (every rank's record count, identical on all ranks -- e.g. from the
+        screen partition) skips the count exchange."""
         n_loc = int(records_local.shape[0])
-        rec = torch.empty((n_loc * self.world, records_local.shape[1]), dtype=records_local.dtype,
-                          device=records_local.device)
-        tgt = torch.empty((n_loc * self.world, 3), dtype=targets_local.dtype, device=targets_local.device)
+        counts = self._counts(n_loc) if counts is None else [int(c) for c in counts]
+        if len(counts) != self.world or counts[self.rank] != n_loc:
+            raise ValueError(f"counts {counts} do not match this rank's {n_loc} records")
+        nmax = max(counts)
+        nrec = records_local.shape[1]
+        if n_loc < nmax:  # pad to the collective's common size (dropped below)
+            pad_r = torch.zeros((nmax - n_loc, nrec), dtype=records_local.dtype, device=records_local.device)
+            pad_t = torch.zeros((nmax - n_loc, 3), dtype=targets_local.dtype, device=targets_local.device)
+            records_local = torch.cat([records_local, pad_r])
+            targets_local = torch.cat([targets_local, pad_t])
+        rec = torch.empty((nmax * self.world, nrec), dtype=records_local.dtype, device=records_local.device)
+        tgt = torch.empty((nmax * self.world, 3), dtype=targets_local.dtype, device=targets_local.device)
         if dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(rec, records_local.contiguous(), group=self.group)
             dist.all_gather_into_tensor(tgt, targets_local.contiguous(), group=self.group)
         else:  # gloo (CPU tests): list form
             dist.all_gather(list(rec.chunk(self.world)), records_local.contiguous(), group=self.group)
             dist.all_gather(list(tgt.chunk(self.world)), targets_local.contiguous(), group=self.group)
+        if min(counts) != nmax:  # drop the padding, keep rank order
+            rec = torch.cat([rec[r * nmax:r * nmax + c] for r, c in enumerate(counts)])
+            tgt = torch.cat([tgt[r * nmax:r * nmax + c] for r, c in enumerate(counts)])
         out = self.cache.train_frame(rec, tgt, s, l, shuffle_seed, losses)
         self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
         return out
 
-    def train_frame_peer(self, records_local: torch.Tensor, targets_local: torch.Tensor, s: int, l: int,
-                         shuffle_seed: int, losses: Optional[torch.Tensor] = None,
-                         parts_ready: bool = False) -> Optional[torch.Tensor]:
-        """SURVEY 8(f) N3, the all-gather fused into the training kernel: every
-        rank exports its record / target buffers once (CUDA IPC handles over
-        the process group), maps the peers', and nrc_train_frame_parts reads
-        each shuffled batch row from its owner's memory (NVLink loads).  No
-        collective per frame; bitwise the same result as train_frame_replicated.
-        The caller keeps the local buffers alive and unchanged across the call
-        on every rank (here: a barrier before the kernel, skipped with
-        parts_ready=True when the caller already knows every part is final,
-        e.g. buffers written once and synchronised at setup)."""
-        from .nrc import ipc_export, ipc_import
-        key = (records_local.data_ptr(), targets_local.data_ptr(), int(records_local.shape[0]))
-        self._peer_cache = getattr(self, "_peer_cache", {})
-        if key not in self._peer_cache:
-            mine = (ipc_export(records_local), ipc_export(targets_local), int(records_local.shape[0]))
-            everyone = [None] * self.world
-            dist.all_gather_object(everyone, mine, group=self.group)
-            if any(e[2] != mine[2] for e in everyone):
-                raise ValueError("every rank must hold the same number of records")
-            self._peer_maps = getattr(self, "_peer_maps", {})
-            rec_ptrs, tgt_ptrs = [], []
-            for r, (rh, th, _) in enumerate(everyone):
-                if r == self.rank:
-                    rec_ptrs.append(records_local.data_ptr())
-                    tgt_ptrs.append(targets_local.data_ptr())
-                    continue
-                for hnd, lst in ((rh, rec_ptrs), (th, tgt_ptrs)):
-                    if hnd not in self._peer_maps:
-                        self._peer_maps[hnd] = ipc_import(*hnd)
-                    lst.append(self._peer_maps[hnd])
-            self._peer_cache[key] = (rec_ptrs, tgt_ptrs)
-        if not parts_ready:
-            torch.cuda.current_stream().synchronize()
-            dist.barrier(group=self.group)  # every part is complete
-        rec_ptrs, tgt_ptrs = self._peer_cache[key]
-        out = self.cache.train_frame_parts(rec_ptrs, tgt_ptrs, int(records_local.shape[0]), s, l, shuffle_seed,
-                                           losses)
-        self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
-        return out
+    def _counts(self, n_loc: int):
+        """Every rank's record count.  The exchange runs on every call (one
+        small all-gather of Python ints), so a rank whose count changed can
+        never leave the others in a different collective."""
+        got = [None] * self.world
+        dist.all_gather_object(got, n_loc, group=self.group)
+        return [int(c) for c in got]
 
     def train_frame_allreduce_peer(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int,
                                    shuffle_seed: int, losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
@@ -236,9 +172,9 @@ class DataParallelFrame:
             self.cache.train_frame_backward(records, targets, l, shuffle_seed, j, lo, hi, self.grad, self.loss_sum)
             launches += getattr(self.cache, "last_launch_count", 0)
             dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=self.group)
-            self.cache.train_apply(self.grad, l)
+            # Adam + EMA on grad / l; the batch-mean loss = loss sum / l is
+            # computed by the library too (nrc_train_apply)
+            self.cache.train_apply(self.grad, l, self.loss_sum, None if losses is None else losses[j:j + 1])
             launches += getattr(self.cache, "last_launch_count", 0)
-            if losses is not None:
-                losses[j] = self.loss_sum[0] / l
         self.last_launch_count = launches
         return losses

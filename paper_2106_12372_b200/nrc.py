@@ -229,8 +229,10 @@ class RadianceCache:
         return loss
 
     def train_backward(self, records: torch.Tensor, targets: torch.Tensor, grad: Optional[torch.Tensor] = None,
-                       loss_sum: Optional[torch.Tensor] = None, stream=None):
-        """Un-normalised gradient sum (logical layout) and loss sum over the records."""
+                       loss_sum: Optional[torch.Tensor] = None, pred: Optional[torch.Tensor] = None, stream=None):
+        """Un-normalised gradient sum (logical layout) and loss sum over the
+        records; `pred` ([n, 3] fp32, optional) receives the training forward's
+        factored prediction y * (alpha + beta) (a4, unclamped)."""
         records = self._rec(records)
         n = records.shape[0]
         self._f32(targets, (n, 3), "targets")
@@ -238,14 +240,23 @@ class RadianceCache:
             grad = torch.empty(self.nparam, dtype=torch.float32, device=self.device)
         if loss_sum is None:
             loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
+        if pred is not None:
+            self._f32(pred, (n, 3), "pred")
         self._check(self.L.nrc_train_backward(self.h, _ptr(records), _ptr(targets), n, _ptr(grad), _ptr(loss_sum),
-                                              _stream(stream)), "nrc_train_backward")
+                                              _ptr(pred), _stream(stream)), "nrc_train_backward")
         return grad, loss_sum
 
-    def train_apply(self, grad_sum: torch.Tensor, n_global: int, stream=None):
-        """Adam + EMA with g = grad_sum / n_global (after an all-reduce)."""
+    def train_apply(self, grad_sum: torch.Tensor, n_global: int, loss_sum: Optional[torch.Tensor] = None,
+                    loss: Optional[torch.Tensor] = None, stream=None):
+        """Adam + EMA with g = grad_sum / n_global (after an all-reduce); with
+        loss_sum and loss given, also loss[0] = loss_sum[0] / n_global."""
         self._f32(grad_sum, (self.nparam,), "grad_sum")
-        self._check(self.L.nrc_train_apply(self.h, _ptr(grad_sum), int(n_global), _stream(stream)), "nrc_train_apply")
+        if loss_sum is not None:
+            self._f32(loss_sum, tuple(loss_sum.shape), "loss_sum")
+        if loss is not None:
+            self._f32(loss, tuple(loss.shape), "loss")
+        self._check(self.L.nrc_train_apply(self.h, _ptr(grad_sum), int(n_global), _ptr(loss_sum), _ptr(loss),
+                                           _stream(stream)), "nrc_train_apply")
 
     def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int = 4, l: int = 16384,
                     shuffle_seed: int = 0, losses: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
@@ -258,22 +269,6 @@ class RadianceCache:
         self._check(self.L.nrc_train_frame(self.h, _ptr(records), _ptr(targets), n, int(s), int(l),
                                            int(shuffle_seed) & (2 ** 64 - 1), _ptr(losses), _stream(stream)),
                     "nrc_train_frame")
-        return losses
-
-    def train_frame_parts(self, rec_ptrs, tgt_ptrs, n_per_part: int, s: int = 4, l: int = 16384,
-                          shuffle_seed: int = 0, losses: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-        """nrc_train_frame over records split into parts that may live in peer
-        GPUs' memory (device pointers as ints; see DataParallelFrame)."""
-        n = len(rec_ptrs)
-        if n != len(tgt_ptrs) or not 1 <= n <= 8:
-            raise NRCError("1..8 record / target parts required")
-        rp = (ctypes.c_void_p * n)(*rec_ptrs)
-        tp = (ctypes.c_void_p * n)(*tgt_ptrs)
-        if losses is None:
-            losses = torch.zeros(max(int(s), 1), dtype=torch.float32, device=self.device)
-        self._check(self.L.nrc_train_frame_parts(self.h, rp, tp, n, int(n_per_part), int(s), int(l),
-                                                 int(shuffle_seed) & (2 ** 64 - 1), _ptr(losses), _stream(stream)),
-                    "nrc_train_frame_parts")
         return losses
 
     @property
@@ -299,14 +294,6 @@ class RadianceCache:
                                                    int(shuffle_seed) & (2 ** 64 - 1), int(rank), int(world), ps,
                                                    _ptr(losses), _stream(stream)), "nrc_train_frame_dp_peer")
         return losses
-
-    def query_image(self) -> torch.Tensor:
-        """The fp16 operand image nrc_query reads, as a uint8 view of the state
-        arena (for broadcasting it from a training rank)."""
-        ptr, nb = ctypes.c_void_p(), ctypes.c_size_t()
-        self._check(self.L.nrc_query_image(self.h, ctypes.byref(ptr), ctypes.byref(nb)), "nrc_query_image")
-        off = int(ptr.value) - self.state.data_ptr()
-        return self.state[off:off + int(nb.value)]
 
     def dp_timeouts(self) -> int:
         c = ctypes.c_uint64()
@@ -397,9 +384,11 @@ class RadianceCache:
                     "nrc_set_params")
 
     def stats(self) -> dict:
-        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-        self._check(self.L.nrc_get_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), "nrc_get_stats")
-        return {"step": a.value, "nonfinite_grads": b.value, "nonfinite_targets": c.value}
+        a, b, c, d = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(self.L.nrc_get_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
+                    "nrc_get_stats")
+        return {"step": a.value, "nonfinite_grads": b.value, "nonfinite_targets": c.value,
+                "degenerate_vectors": d.value}
 
     def frame_host(self, query_rec: np.ndarray, rgb_out: np.ndarray, train_rec: np.ndarray, train_tgt: np.ndarray,
                    s: int, l: int, shuffle_seed: int, losses_out: np.ndarray, scratch: torch.Tensor, stream=None):

@@ -2,8 +2,7 @@
 query of 2,073,600 records + a 4 x 16,384-record training frame -- at hidden
 width 32 / 64 / 128 (input 64, depth 5): CUDA events, L2 flushed between reps,
 tensor-roofline fractions of the query and of the training.  Training runs
-through the per-step partials + Adam kernels at every width; W = 64 is also
-timed through the fused cooperative kernel (NRC_TRAIN_FUSED=1).
+through the per-step partials + Adam kernels at every width.
 Writes one JSON line per configuration."""
 import json
 import os
@@ -43,11 +42,8 @@ def timeit(fn, reps=50):
     return float(np.median(ts))
 
 
-for hw, fused in ((32, False), (64, False), (64, True), (128, False)):
-    if fused:
-        os.environ["NRC_TRAIN_FUSED"] = "1"
+for hw in (32, 64, 128):
     c = nrc.RadianceCache(nrc.Config(hidden_width=hw))
-    os.environ.pop("NRC_TRAIN_FUSED", None)
     q_ms = timeit(lambda: c.query(recs, out))
     t_ms = timeit(lambda: c.train_frame(tr, tg, 4, 16384, 1), reps=30)
     fq = 2 * (64 * hw + 4 * hw * hw + 3 * hw)          # query FLOP per record
@@ -55,7 +51,7 @@ for hw, fused in ((32, False), (64, False), (64, True), (128, False)):
     q_tf = fq * n / (q_ms * 1e-3) / 1e12
     t_tf = ft * n_train / (t_ms * 1e-3) / 1e12
     print(json.dumps({"config": "C4 width ablation, 1080p frame (query + 4x16384 train)", "hidden_width": hw,
-                      "train_kernel": "fused cooperative" if fused else "partials + adam (PDL)",
+                      "train_kernel": "partials + adam (PDL)",
                       "query_ms": q_ms, "train_ms": t_ms, "frame_ms": q_ms + t_ms,
                       "queries_per_s": n / (q_ms * 1e-3), "records_per_s": n_train / (t_ms * 1e-3),
                       "flop_per_query": fq, "flop_per_train_record": ft,

@@ -47,7 +47,7 @@ def main(tag, d):
     print("\n".join(lines))
     tp = os.path.join(prof, f"{tag}_traffic.json")
     traffic = json.load(open(tp)) if os.path.exists(tp) else {}  # keep kernels not re-captured this time
-    for name, rep in [("nrc_query_ts_kernel", "prof_query.ncu-rep"), ("nrc_train_kernel", "prof_train.ncu-rep"),
+    for name, rep in [("nrc_query_ts_kernel", "prof_query.ncu-rep"), ("nrc_train_w_kernel", "prof_train.ncu-rep"),
                       ("nrc_train_w_kernel<64>", "prof_train_w.ncu-rep"), ("nrc_adam_w_kernel<64>", "prof_adam_w.ncu-rep")]:
         p = os.path.join(d, rep)
         if os.path.exists(p):

@@ -1,8 +1,7 @@
 """Small end-to-end workload for compute-sanitizer runs: query, train_step,
 train_frame, train_backward/apply, encode, assemble_targets, query_accumulate
 on small sizes at hidden width 64 (default training path), training at width
-32 and 128, and (NRC_SANITIZE_FUSED=1) the fused cooperative train kernel
-(diagnostics).  NRC_SANITIZE_MIN=1: query + one train step only (memcheck)."""
+32 and 128.  NRC_SANITIZE_MIN=1: query + one train step only (memcheck)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -32,10 +31,5 @@ for hw, nh in ((32, 5), (128, 5), (64, 2), (32, 8)):  # width / depth variants (
     cw.query(dev(recs))
 cd = nrc.RadianceCache()  # fused peer all-reduce path at world 1 (hand-off kernel, table-driven optimiser)
 cd.train_frame_dp_peer(dev(tr), dev(tg), 2, 1024, 7, 0, 1, [cd.state_ptr])
-if os.environ.get("NRC_SANITIZE_FUSED", "1") == "1":  # the grid-barrier kernel (not under racecheck)
-    os.environ["NRC_TRAIN_FUSED"] = "1"
-    cf = nrc.RadianceCache()
-    cf.train_step(dev(tr[:1000]), dev(tg[:1000]))
-    cf.train_frame(dev(tr), dev(tg), 4, 1024, 3)
 torch.cuda.synchronize()
 print("sanitize workload ok", float(q.sum()), float(t.sum()), float(img.sum()))

@@ -75,3 +75,19 @@ def fp16_ulp(x):
     x = np.abs(np.asarray(x, np.float64))
     e = np.floor(np.log2(np.maximum(x, 2.0 ** -14)))
     return 2.0 ** (e - 10)
+
+
+def assert_support_sets(got, ref):
+    """One-blob support sets of the encodings (columns 36..55) agree in both
+    directions: every bin the oracle puts clearly inside the kernel's support
+    (value > 2^-12) is active on the GPU, and every bin active on the GPU is
+    inside the oracle's support (value > 0).  Between the two thresholds lie
+    the |x| = 1 ties, where the quartic is ~0 and the fp16 value may round
+    either way (reading R17)."""
+    got = np.asarray(got, np.float64)[:, 36:56]
+    ref = np.asarray(ref, np.float64)[:, 36:56]
+    act_gpu = got > 0
+    miss = (ref > 2.0 ** -12) & ~act_gpu
+    extra = act_gpu & ~(ref > 0)
+    assert not miss.any(), f"{int(miss.sum())} oracle-active bins inactive on the GPU, first at {np.argwhere(miss)[:3]}"
+    assert not extra.any(), f"{int(extra.sum())} GPU-active bins outside the oracle support, first at {np.argwhere(extra)[:3]}"

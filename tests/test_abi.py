@@ -51,7 +51,7 @@ def test_default_config_and_state_bytes(libnrc):
     from paper_2106_12372_b200 import _lib
     c = _lib.NrcConfig()
     libnrc.nrc_default_config(ctypes.byref(c))
-    assert c.abi_version == 1 and c.hidden_width == 64 and c.n_hidden_layers == 5
+    assert c.abi_version == 2 and c.hidden_width == 64 and c.n_hidden_layers == 5
     assert c.loss_eps == pytest.approx(0.01) and c.ema_alpha == pytest.approx(0.99)
     assert c.learning_rate == pytest.approx(1e-2) and c.flags == 3
     nb = libnrc.nrc_state_bytes(ctypes.byref(c))
@@ -62,6 +62,27 @@ def test_default_config_and_state_bytes(libnrc):
     assert libnrc.nrc_state_bytes(ctypes.byref(bad)) == 0
     bad.aabb_max[1] = 1.0; bad.abi_version = 7
     assert libnrc.nrc_state_bytes(ctypes.byref(bad)) == 0
+    bad.abi_version = 2; bad.max_batch = 0
+    assert libnrc.nrc_state_bytes(ctypes.byref(bad)) == 0
+    bad.max_batch = 3840 * 2160 * 4  # 64-bit max_batch beyond 2^32 is accepted
+    bad.max_batch = 2 ** 33
+    assert libnrc.nrc_state_bytes(ctypes.byref(bad)) == nb
+
+
+def test_config_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of nrc_config has the C struct's size and field
+    offsets (compiled from include/nrc.h with the host compiler)."""
+    from paper_2106_12372_b200 import _lib
+    fields = [f for f, _ in _lib.NrcConfig._fields_]
+    src = tmp_path / "off.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"nrc.h\"\nint main(void){\n"
+                   + f'printf("%zu\\n", sizeof(nrc_config));\n'
+                   + "".join(f'printf("%zu\\n", offsetof(nrc_config, {f}));\n' for f in fields) + "return 0;}\n")
+    exe = tmp_path / "off"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(_lib.NrcConfig)
+    assert got[1:] == [getattr(_lib.NrcConfig, f).offset for f in fields]
 
 
 def test_init_rejects_bad_arguments_without_gpu(libnrc):

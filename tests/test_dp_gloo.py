@@ -54,11 +54,13 @@ class OracleShard:
         grad.copy_(torch.from_numpy(G))
         loss_sum[0] = ls
 
-    def train_apply(self, grad_sum, n):
+    def train_apply(self, grad_sum, n, loss_sum=None, loss=None):
         oc = self.oc
         oc.t += 1
         oracle.adam(oc.w, oc.m, oc.v, grad_sum.numpy().astype(np.float64) / n, oc.t)
         oracle.ema(oc.wbar, oc.w, oc.t)
+        if loss_sum is not None and loss is not None:  # nrc_train_apply's batch-mean loss (R10)
+            loss[0] = loss_sum[0] / n
 
     def train_frame(self, records, targets, s, l, seed, losses=None):
         recs, tg = records.numpy(), targets.numpy()
@@ -78,11 +80,6 @@ class OracleShard:
 
     def get_params(self, which="train"):
         return (self.oc.w if which == "train" else self.oc.wbar).astype(np.float32)
-
-    def query_image(self):
-        """Stand-in for the query's fp16 image: a view of the fp64 W-bar the
-        stand-in query reads (so a broadcast into it changes later queries)."""
-        return torch.from_numpy(self.oc.wbar)
 
 
 N_TOTAL, S, L, SEED = 3 * 1001 + 5, 3, 1001, 77
@@ -106,7 +103,7 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-def _worker_replicated(rank, world, port, out_dir, n_total):
+def _worker_replicated(rank, world, port, out_dir, n_total, pass_counts=False):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         recs, tgts = nrc_inputs.train_frame(0, n=n_total, noise=0.3)
@@ -115,8 +112,9 @@ def _worker_replicated(rank, world, port, out_dir, n_total):
         frame = dp.DataParallelFrame(shard_cache, dtype=torch.float64)
         losses = torch.zeros(S, dtype=torch.float64)
         frame.verify_replicas()  # identical seeded init on every rank
+        counts = [b - a for a, b in (dp.shard(n_total, r, world) for r in range(world))] if pass_counts else None
         frame.train_frame_replicated(torch.from_numpy(recs[lo:hi].copy()), torch.from_numpy(tgts[lo:hi].copy()),
-                                     S, L, SEED, losses)
+                                     S, L, SEED, losses, counts=counts)
         frame.verify_replicas()  # and bitwise identical after the replicated frame
         np.savez(os.path.join(out_dir, f"rep{rank}.npz"), w=shard_cache.oc.w, losses=losses.numpy())
     finally:
@@ -157,15 +155,19 @@ def test_data_parallel_frame_equals_single_process(tmp_path):
     np.testing.assert_allclose(got, full, rtol=1e-9, atol=1e-12)
 
 
-def test_replicated_frame_after_allgather(tmp_path):
+@pytest.mark.parametrize("world,N,pass_counts", [(2, 3 * 1000 + 6, False), (3, 3 * 1001 + 5, True),
+                                                 (3, 3 * 1001 + 5, False)])
+def test_replicated_frame_after_allgather(tmp_path, world, N, pass_counts):
     """N3 variant (i): one all-gather of the frame's records per frame, then
     replicated training: every rank ends bitwise identical and equal to the
-    single-process training on the gathered (rank-ordered) records."""
-    world = 2
-    N = 3 * 1000 + 6  # divisible by the world size
-    mp.spawn(_worker_replicated, args=(world, _free_port(), str(tmp_path), N), nprocs=world, join=True)
+    single-process training on the gathered (rank-ordered) records -- also
+    when the record count does not divide by the world size (3,008 over 3
+    ranks: parts padded for the collective, padding dropped), with the counts
+    exchanged or passed by the caller."""
+    mp.spawn(_worker_replicated, args=(world, _free_port(), str(tmp_path), N, pass_counts), nprocs=world, join=True)
     res = [np.load(tmp_path / f"rep{r}.npz") for r in range(world)]
-    np.testing.assert_array_equal(res[0]["w"], res[1]["w"])
+    for r in range(1, world):
+        np.testing.assert_array_equal(res[0]["w"], res[r]["w"])
     recs, tgts = nrc_inputs.train_frame(0, n=N, noise=0.3)
     ref = OracleShard(seed=5)
     ref_losses = torch.zeros(S, dtype=torch.float64)
@@ -239,56 +241,3 @@ def test_verify_replicas_detects_divergence(tmp_path):
     mp.spawn(_worker_diverged, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     for r in range(world):
         assert bool(np.load(tmp_path / f"div{r}.npy")[0])
-
-
-F_DED = 3
-
-
-def _worker_dedicated(rank, world, port, out_dir, share0=0.0):
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    try:
-        shard_cache = OracleShard(seed=5)
-        frame = dp.DataParallelFrame(shard_cache, dtype=torch.float64)
-        q = nrc_inputs.records(500, seed=nrc_inputs.SEED_QUERY)
-        q0, q1 = frame.dedicated_query_rows(q.shape[0], share0)
-        outs = []
-        for f in range(F_DED):
-            recs, tgts = nrc_inputs.train_frame(f, n=N_TOTAL, noise=0.3)
-            rgb = torch.zeros((q1 - q0, 3), dtype=torch.float64)
-            frame.frame_dedicated(torch.from_numpy(q[q0:q1].copy()), rgb, torch.from_numpy(recs),
-                                  torch.from_numpy(tgts), S, L, SEED + f)
-            outs.append(rgb.numpy().copy())
-        frame.verify_replicas(image_only=True)
-        np.savez(os.path.join(out_dir, f"ded{rank}.npz"), wbar=shard_cache.oc.wbar, q0=q0, q1=q1,
-                 rgb=np.stack(outs) if outs and outs[0].size else np.zeros((F_DED, 0, 3)))
-    finally:
-        dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("world,share0", [(3, 0.0), (2, 0.25)])
-def test_dedicated_frame_equals_sequential(tmp_path, world, share0):
-    """Dedicated mode (rank 0 trains -- after querying its share0 of the rows,
-    if any -- the other ranks query with the previous frame's W-bar, then W-bar
-    is broadcast): the queries of every frame and the final W-bar equal the
-    single-process frame sequence (query, then train)."""
-    mp.spawn(_worker_dedicated, args=(world, _free_port(), str(tmp_path), share0), nprocs=world, join=True)
-    res = [np.load(tmp_path / f"ded{r}.npz") for r in range(world)]
-    q = nrc_inputs.records(500, seed=nrc_inputs.SEED_QUERY)
-    ref = OracleShard(seed=5)
-    want = []
-    for f in range(F_DED):
-        want.append(ref.oc.query(q))
-        recs, tgts = nrc_inputs.train_frame(f, n=N_TOTAL, noise=0.3)
-        ref.train_frame(torch.from_numpy(recs), torch.from_numpy(tgts), S, L, SEED + f)
-    assert int(res[0]["q1"]) - int(res[0]["q0"]) == round(share0 * 500)
-    got = np.concatenate([r["rgb"] for r in res], axis=1)
-    np.testing.assert_array_equal(got, np.stack(want))
-    for r in res:
-        np.testing.assert_array_equal(r["wbar"], ref.oc.wbar)
-
-
-def test_dedicated_share0_balances():
-    # P = 2: 80 us of training against a 105 us query -> rank 0 takes 11.9 %
-    assert dp.DataParallelFrame.dedicated_share0(105.0, 80.0, 2) == pytest.approx(25.0 / 210.0)
-    assert dp.DataParallelFrame.dedicated_share0(105.0, 80.0, 8) == 0.0   # training dominates
-    assert dp.DataParallelFrame.dedicated_share0(105.0, 0.0, 2) == pytest.approx(0.5)

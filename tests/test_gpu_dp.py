@@ -1,7 +1,7 @@
 """The N > 1 data-parallel path (paper_2106_12372_b200.dp) on one GPU with a
 world-size-1 NCCL group: the all-reduce is the identity, so the frame trained
 through nrc_train_frame_backward + all-reduce + nrc_train_apply must agree
-with the fused nrc_train_frame (same gradient up to fp32 summation order) and
+with the single-GPU nrc_train_frame (same gradient up to fp32 summation order) and
 with the fp64 oracle on the gathered batches."""
 import socket
 
@@ -32,7 +32,7 @@ def group():
     dist.destroy_process_group()
 
 
-def test_dp_frame_world1_matches_fused_frame_and_oracle(group, orc):
+def test_dp_frame_world1_matches_single_gpu_frame_and_oracle(group, orc):
     import paper_2106_12372_b200 as nrc
     n, s, l, seed = 8192 + 3, 4, 2048, 21
     recs, tg = nrc_inputs.train_frame(2, n=n, noise=0.3)

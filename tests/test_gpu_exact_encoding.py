@@ -54,15 +54,11 @@ def test_exact_training_runs(nrc):
     assert np.mean(losses[-1]) < np.mean(losses[0])
 
 
-@pytest.mark.parametrize("fused", [False, True])
-def test_exact_gradient_parity(nrc, orc, monkeypatch, fused):
+def test_exact_gradient_parity(nrc, orc):
     """Training with NRC_EXACT_ENCODING encodes the training records with the
     same exact primitives as the query: train_backward's gradient against
     orc_grad_batch_exact (per matrix within 3e-2, loss within 1e-2) and away
-    from the cheap-encoding gradient -- for the default per-step kernels and
-    the fused cooperative kernel (NRC_TRAIN_FUSED=1)."""
-    if fused:
-        monkeypatch.setenv("NRC_TRAIN_FUSED", "1")
+    from the cheap-encoding gradient."""
     c = nrc.RadianceCache(nrc.Config(flags=nrc.FACTORIZE | nrc.CLAMP_QUERY | nrc.EXACT_ENCODING))
     recs = nrc_inputs.records(3000, seed=502)
     tg = nrc_inputs.targets(recs, noise=0.3, seed=3)

@@ -189,21 +189,6 @@ def test_width_backward_apply_equals_step_and_determinism(nrc, hw):
     np.testing.assert_array_equal(a.get_params("train"), r2.get_params("train"))
 
 
-def test_generic64_matches_fused64(nrc, orc, monkeypatch):
-    """Width 64 through the generic kernels vs the fused cooperative kernel
-    (NRC_TRAIN_FUSED=1): losses and queries agree after a 4-step frame."""
-    recs, tg = nrc_inputs.train_frame(3, n=65536, noise=0.3)
-    g, _ = make(nrc, "64g", monkeypatch)
-    monkeypatch.setenv("NRC_TRAIN_FUSED", "1")
-    f = nrc.RadianceCache()
-    monkeypatch.delenv("NRC_TRAIN_FUSED")
-    lg = g.train_frame(dev(recs), dev(tg), 4, 16384, 9).cpu().numpy()
-    lf = f.train_frame(dev(recs), dev(tg), 4, 16384, 9).cpu().numpy()
-    np.testing.assert_allclose(lg, lf, rtol=1e-2)
-    q = nrc_inputs.records(4000, seed=79)
-    assert max(radiance_err(g.query(dev(q)).cpu().numpy(), f.query(dev(q)).cpu().numpy())) <= TOL_RADIANCE
-
-
 @pytest.mark.parametrize("hw", [32, 128])
 def test_width_empty_and_nonfinite(nrc, hw):
     c, w = make(nrc, hw)
