@@ -478,7 +478,10 @@ __device__ __forceinline__ uint32_t encode_record_cheap(const float* rec, const 
     float e[64];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const float v = __fmul_rn(__fsub_rn(rec[a], ep.lo[a]), ep.inv[a]);
+        // tri is even (tri(-x) = tri(x)), so work on |v|: then v - 2 floor(v / 2)
+        // is exact in fp32 (for v < 0 it is not: the result may need a finer
+        // ulp than v, and the doublings below would amplify the rounding)
+        const float v = fabsf(__fmul_rn(__fsub_rn(rec[a], ep.lo[a]), ep.inv[a]));
         // m_d = 2^d v mod 2 by exact doubling: m_{d+1} = 2 (m_d - [m_d >= 1]);
         // tri(2^d v) = 2 |m_d - 1| - 1, bit-identical to the direct form.
         float m = v - 2.0f * floorf(v * 0.5f);

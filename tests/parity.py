@@ -51,20 +51,33 @@ def per_matrix_err(a, b, off=OFF):
     return out
 
 
-def post_adam_err(w_gpu, w_ref, g_gpu, g_ref, off=OFF):
+ADAM_EPS = 1e-8
+
+
+def post_adam_err(w_gpu, w_ref, g_gpu, g_ref, off=OFF, ill_frac_max=0.01):
     """Per-matrix post-Adam error over sign-agreeing entries, plus the sign-flip
-    statistics (fraction, and worst |G_ref| / max|G_ref| among the flips)."""
+    statistics (fraction, and worst |G_ref| / max|G_ref| among the flips).
+
+    g_gpu / g_ref are batch-MEAN gradients.  Entries whose mean gradient is
+    within 10 eps_A of zero are excluded as well (reading R26): there the
+    first Adam step lr g / (|g| + eps_A) has slope up to lr / eps_A = 1e6 in g,
+    so a gradient difference at fp16 rounding level (~1e-9) moves w by up to
+    ~lr -- an ill-conditioned comparison, not a kernel error.  Their fraction
+    must stay <= ill_frac_max; the flips keep SURVEY 8(c)'s bounds."""
     w_gpu = np.asarray(w_gpu, np.float64); w_ref = np.asarray(w_ref, np.float64)
     g_gpu = np.asarray(g_gpu, np.float64); g_ref = np.asarray(g_ref, np.float64)
     OFF = off
+    ill = np.abs(g_ref) <= 10 * ADAM_EPS
+    assert ill.mean() <= ill_frac_max, f"{ill.mean():.4f} of the entries have |g| <= 10 eps_A"
     errs, flips, worst = [], 0, 0.0
-    for i in range(6):
+    for i in range(len(OFF) - 1):
         s = slice(OFF[i], OFF[i + 1])
-        agree = np.sign(g_gpu[s]) == np.sign(g_ref[s])
-        flips += int((~agree).sum())
+        agree = (np.sign(g_gpu[s]) == np.sign(g_ref[s])) & ~ill[s]
         gmax = max(np.max(np.abs(g_ref[s])), 1e-30)
-        if (~agree).any():
-            worst = max(worst, float(np.max(np.abs(g_ref[s][~agree])) / gmax))
+        flip = (np.sign(g_gpu[s]) != np.sign(g_ref[s])) & ~ill[s]
+        flips += int(flip.sum())
+        if flip.any():
+            worst = max(worst, float(np.max(np.abs(g_ref[s][flip])) / gmax))
         d = np.abs(w_gpu[s] - w_ref[s])[agree]
         errs.append(float(d.max() / max(np.max(np.abs(w_ref[s])), 1e-30)) if d.size else 0.0)
     return errs, flips / float(len(w_ref)), worst
