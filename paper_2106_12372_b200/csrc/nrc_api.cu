@@ -601,7 +601,7 @@ static AdamWArgs adam_w_args(nrc_handle* h) {
     return aa;
 }
 static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t st) {
-    const dim3 grid(unsigned((h->wi.padded / 32 + kAdamGroups - 1) / kAdamGroups)), block(256 * kAdamGroups);
+    const dim3 grid(unsigned(h->wi.padded / 128)), block(kAdamThreads);  // 128 parameters per block
     if (h->wi.W == 32)
         NRC_CUDA(h, launch_pdl(nrc_adam_w_kernel<32>, grid, block, 0, st, aa));
     else if (h->wi.W == 128)

@@ -47,7 +47,7 @@ struct TrainArgs {
     EncodeParams ep;
     uint32_t flags;
     float loss_eps;
-    float* partials;       // [gridDim.x][padded] fp32 un-normalised gradient sums
+    float* partials;       // [gridDim.x][padded] fp32 un-normalised gradient sums (chunk-major, part_index)
     float* loss_part;      // [gridDim.x] loss sums
     unsigned long long* bad_targets;
     unsigned long long* degenerate;  // zero-length omega / n vectors encoded (R7)
@@ -71,7 +71,6 @@ __device__ __forceinline__ uint32_t relu_mask(uint32_t h2bits) {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
 __device__ __forceinline__ long long global_ns() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -30,6 +30,16 @@
 
 namespace nrc {
 
+// Chunk-major layout of an fp32 gradient vector (CTA partials): layer i's
+// block starts at pad_off(i) and holds element (o, c) at
+// (c / 4) rows(i) + o float4s in, component c % 4.  A warp draining 16 / 32
+// TMEM lanes (rows o) then stores one contiguous run per instruction, and the
+// optimiser reads each float4 element of all partials with coalesced loads.
+template <int W>
+__device__ __forceinline__ int part_index(const NetRt<W>& D, int i, int o, int c) {
+    return D.pad_off(i) + ((c >> 2) * D.rows(i) + o) * 4 + (c & 3);
+}
+
 template <int W>
 struct TrainW {
     static constexpr bool kStream = W > 64;        // per-layer weight streaming
@@ -101,6 +111,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     const uint32_t sG6_a = sH_a + uint32_t(stash_bytes);  // dL/dy tile (columns 0..2 used)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + wbytes + stash_bytes + kTileBytes);
     uint64_t* wbar = &bars[0];
+    uint64_t* wbar1 = &bars[10];  // resident image: W1 .. W_nh
     uint64_t* mma_bar = &bars[1];
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
     float* red = reinterpret_cast<float*>(bars + 3);  // 4 floats + 4 u32
@@ -110,6 +121,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     if (tid == 0) {
         *deg_scratch = 0;
         mbar_init(wbar, 1);
+        mbar_init(wbar1, 1);
         mbar_init(mma_bar, 1);
         fence_mbar_init();
     }
@@ -138,13 +150,21 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
 
     uint32_t phase = 0, w_phase = 0;
     // weight bytes of layer L (streamed) or the whole image (resident), issued by thread 0
-    auto fetch = [&](int L) {
-        const uint32_t off = T::kStream ? uint32_t(D.img_off(L)) : 0u;
-        const uint32_t bytes = T::kStream ? uint32_t(D.img_off(L + 1) - D.img_off(L)) : uint32_t(D.img());
-        mbar_arrive_expect_tx(wbar, bytes);
+    // weight bytes of layer L (streamed), issued by thread 0; resident image
+    // (L = 0): W0 on wbar and W1.. on wbar1, so layer 0 starts once its 8 KB land
+    auto copy = [&](uint32_t off, uint32_t bytes, uint64_t* bar) {
+        mbar_arrive_expect_tx(bar, bytes);
         for (uint32_t o = 0; o < bytes; o += 8192u) {
             const uint32_t b = bytes - o < 8192u ? bytes - o : 8192u;
-            bulk_g2s(smem + o, a.wimg + off + o, b, wbar);
+            bulk_g2s(smem + (T::kStream ? 0u : off) + o, a.wimg + off + o, b, bar);
+        }
+    };
+    auto fetch = [&](int L) {
+        if (T::kStream) {
+            copy(uint32_t(D.img_off(L)), uint32_t(D.img_off(L + 1) - D.img_off(L)), wbar);
+        } else {
+            copy(0u, uint32_t(D.img_off(1)), wbar);
+            copy(uint32_t(D.img_off(1)), uint32_t(D.img() - D.img_off(1)), wbar1);
         }
     };
     auto wwait = [&]() {  // warp 0 only (the MMA issuer reads the weights)
@@ -216,7 +236,9 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     };
     float* part = a.partials + size_t(blockIdx.x) * D.padded();
     // drain G_j (TMEM) into this CTA's partial (plain store on the first tile,
-    // else add), undoing the tile's power-of-two dL/dy scale (exact in fp32)
+    // else add), undoing the tile's power-of-two dL/dy scale (exact in fp32);
+    // chunk-major layout: for each store instruction the warp's rows write
+    // consecutive 16-B chunks (one contiguous 256 / 512-B run)
     float inv_s = 1.0f;
     auto flush_g = [&](int j, bool first) {
         const int M = wg_m(j);
@@ -230,16 +252,17 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
             uint32_t v[32];
             tmem_ld32(t_g(j) + lane_off + 32u * p, v);
             if (valid) {
-                float4* dst = reinterpret_cast<float4*>(part + D.pad_off(j) + o * D.cols(j) + 32 * p);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
+                    const int idx = part_index(D, j, o, 32 * p + 4 * q);
                     float4 x = make_float4(__uint_as_float(v[4 * q]) * inv_s, __uint_as_float(v[4 * q + 1]) * inv_s,
                                            __uint_as_float(v[4 * q + 2]) * inv_s, __uint_as_float(v[4 * q + 3]) * inv_s);
+                    float4* dst = reinterpret_cast<float4*>(part + idx);
                     if (!first) {
-                        const float4 y = dst[q];
+                        const float4 y = *dst;
                         x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
                     }
-                    dst[q] = x;
+                    *dst = x;
                 }
             }
         }
@@ -293,6 +316,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
         for (int L = 0; L <= nh; ++L) {
             if (warp == 0) {
                 if (T::kStream || (L == 0 && first)) wwait();
+                if (!T::kStream && L == 1 && first) mbar_wait(wbar1, 0);  // one launch = one image load
                 issue_fwd(L);
             }
             mma_wait();
@@ -421,19 +445,44 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
 }
 #undef NRC_WTRC
 
-// Reduce + Adam + EMA at width W: thread j owns padded parameter j.
-//   partials != nullptr: g = sum over p < np of partials[p][j] (ascending p);
-//   else g = grad_logical[j] (logical layout = padded prefix; W5 pad rows 0).
+// Reduce + Adam + EMA at width W.  Partials use the chunk-major layout
+// (part_index): thread t of block b owns float4 element e = 32 b + lane of
+// that layout, i.e. parameters (o, 4 c4 .. 4 c4 + 3) of one layer.
+//   partials != nullptr: g = sum over p < np of partials[p][e] (ascending p
+//   within each of the 8 warps, p = w mod 8, then the 8 warp sums in warp
+//   order: deterministic for a given np);
+//   tile_part != nullptr: the same over the peer table;
+//   else g = grad_logical (logical layout = padded prefix; W5 pad rows 0).
 //   grad_out: the reduced sum in the logical layout (nrc_train_backward).
 //   apply: Adam (R11) + EMA (Eq. 2, R12) on g * inv_n, writing
 //   the fp32 state and both fp16 operand images.
 constexpr int kMaxDpTiles = 128;  // tiles per step in the fused peer all-reduce path
-constexpr int kAdamGroups = 4;    // 32-parameter groups (256 threads each) per optimiser block
+constexpr int kAdamThreads = 256;  // 8 warps: 32 float4 elements (128 parameters) per block
 // a peer's (or our own) partial, read at system scope, not cached on this SM
 __device__ __forceinline__ float ld_sys_f32(const float* p) {
     float v;
     asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ float4 ld_sys_v4(const float* p) {
+    float4 v;
+    asm volatile("ld.relaxed.sys.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+// L2 load kept in program order (not sunk below the partial loads)
+__device__ __forceinline__ float4 ld_cg_v4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 struct AdamWArgs {
     const float* partials;
@@ -461,104 +510,103 @@ struct AdamWArgs {
     const float* const* tile_loss;
 };
 
-// grid = kPadded / 32 blocks of 256 threads: block b owns parameters
-// 32 b + lane; warp w sums partials p = w, w + 8, ... (all its loads in
-// flight), warp 0 adds the 8 warp sums in warp order (deterministic) and
-// applies the update.
 template <int W>
-__global__ void __launch_bounds__(kAdamGroups * 256, 2) nrc_adam_w_kernel(AdamWArgs a) {
-    const NetRt<W> D(a.nh);  // kPadded(nh) is a multiple of 32 for every width
-    __shared__ float sred_all[kAdamGroups][8][32];
-    pdl_wait();  // launched as a programmatic dependent of the partials kernel
-    pdl_trigger();
+__global__ void __launch_bounds__(kAdamThreads, 3) nrc_adam_w_kernel(AdamWArgs a) {
+    const NetRt<W> D(a.nh);  // padded(nh) is a multiple of 128 for every width and depth
+    __shared__ float4 sred[8][32];
+    const int lane = int(threadIdx.x & 31), wp = int(threadIdx.x >> 5);
+    const int e = int(blockIdx.x) * 32 + lane;  // float4 element of the chunk-major layout
+    const int k = 4 * e;
+    const int i = D.layer_of(k);  // one layer per block (layer sizes are multiples of 128)
+    pdl_wait();     // launched as a programmatic dependent of the partials kernel
+    pdl_trigger();  // the next step's partials kernel may become resident (its griddepcontrol.wait covers this grid)
     const bool trc = a.dbg != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x + 1 == gridDim.x);
-    // (trace: group 0 of the first / last block)
     if (trc) a.dbg[4088 + 2 * (blockIdx.x != 0)] = global_ns();
-    // kAdamGroups independent 256-thread groups per block (fewer, larger
-    // blocks: block dispatch, not the work, bounded the 672-block launch on
-    // some boxes); group q owns parameters 32 (kAdamGroups block + q) + lane
-    const int q = int(threadIdx.x >> 8), lt = int(threadIdx.x & 255);
-    const int lane = lt & 31, wp = lt >> 5;
-    const int grp = int(blockIdx.x) * kAdamGroups + q;
-    const bool live = grp * 32 < D.padded();
-    const int j = live ? grp * 32 + lane : lane;  // dead groups read valid addresses, write nothing
-    float (&sred)[8][32] = sred_all[q];
-    float g = 0.0f;
+
+    const int R = D.rows(i), C = D.cols(i);
+    const int local = (k - D.pad_off(i)) >> 2;
+    const int c4 = local / R, o = local - c4 * R;
+    const int j0 = D.pad_off(i) + o * C + 4 * c4;  // row-major padded index of the 4 parameters
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
     // warp 0's optimiser state, loaded under the partial loads (one L2 round trip)
-    float m = 0.0f, v = 0.0f, w = 0.0f, e = 0.0f;
+    float4 m = g, v = g, w = g, em = g;
     if (wp == 0 && a.apply) {
-        m = ld_global_f32(a.m + j), v = ld_global_f32(a.v + j);
-        w = ld_global_f32(a.w + j), e = ld_global_f32(a.ema + j);
+        m = ld_cg_v4(a.m + j0);
+        v = ld_cg_v4(a.v + j0);
+        w = ld_cg_v4(a.w + j0);
+        em = ld_cg_v4(a.ema + j0);
     }
-    if (a.tile_part != nullptr) {
-        // fused all-reduce: partial p read from its owner's arena (NVLink loads
-        // for peers), the same order as the local sum below
-        const int pidx = j;
-        float s = 0.0f;
+    if (a.tile_part != nullptr || a.partials != nullptr) {
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        const size_t stride = size_t(D.padded()) / 4;
+        const float4* src = reinterpret_cast<const float4*>(a.partials) + e;
 #pragma unroll 1
-        for (int p0 = wp; p0 < a.np; p0 += 8 * 16) {
-            float x[16];
+        for (int p0 = wp; p0 < a.np; p0 += 8 * 8) {
+            float4 x[8];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) x[u] = (p0 + 8 * u < a.np) ? ld_sys_f32(a.tile_part[p0 + 8 * u] + pidx) : 0.0f;
+            for (int u = 0; u < 8; ++u) {
+                const int p = p0 + 8 * u;
+                x[u] = p >= a.np ? make_float4(0.f, 0.f, 0.f, 0.f)
+                       : a.tile_part != nullptr ? ld_sys_v4(a.tile_part[p] + k)  // fused all-reduce: NVLink loads for peers
+                                                : __ldcg(src + size_t(p) * stride);
+            }
 #pragma unroll
-            for (int u = 0; u < 16; ++u) s += x[u];
+            for (int u = 0; u < 8; ++u) s = f4_add(s, x[u]);
         }
         sred[wp][lane] = s;
         __syncthreads();
+        if (trc) a.dbg[4084 + (blockIdx.x != 0)] = global_ns();
         if (wp == 0) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) g += sred[k][lane];
+            for (int q = 0; q < 8; ++q) g = f4_add(g, sred[q][lane]);
         }
-    } else if (a.partials != nullptr) {
-        const float* src = a.partials + j;
-        float s = 0.0f;
-#pragma unroll 1
-        for (int p0 = wp; p0 < a.np; p0 += 8 * 16) {
-            float x[16];
+    } else if (wp == 0) {
+        float gg[4];
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
-                x[u] = (p0 + 8 * u < a.np) ? __ldcg(src + size_t(p0 + 8 * u) * D.padded()) : 0.0f;
-#pragma unroll
-            for (int u = 0; u < 16; ++u) s += x[u];
-        }
-        sred[wp][lane] = s;
-        __syncthreads();
-        if (wp == 0) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) g += sred[k][lane];
-        }
-    } else {
-        g = j < D.logical() ? a.grad_logical[j] : 0.0f;
+        for (int q = 0; q < 4; ++q) gg[q] = j0 + q < D.logical() ? a.grad_logical[j0 + q] : 0.0f;
+        g = make_float4(gg[0], gg[1], gg[2], gg[3]);
     }
-    if (wp != 0 || !live) return;
-    if (blockIdx.x == 0 && q == 0 && a.loss_out != nullptr) {
+    if (wp != 0) return;
+    if (blockIdx.x == 0 && a.loss_out != nullptr) {
         float s = 0.0f;
-        for (int p = lane; p < a.nloss; p += 32) s += a.tile_part != nullptr ? ld_sys_f32(a.tile_loss[p]) : a.loss_part[p];
+        for (int p = lane; p < a.nloss; p += 32) s += a.tile_part != nullptr ? ld_sys_f32(a.tile_loss[p]) : __ldcg(a.loss_part + p);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane == 0) *a.loss_out = s * a.loss_scale;
     }
-    if (a.grad_out != nullptr && j < D.logical()) a.grad_out[j] = g;
-    if (!a.apply) return;
-    g *= a.inv_n;
-    if (!isfinite(g)) {  // non-finite gradient entries are zeroed and counted
-        g = 0.0f;
-        atomicAdd(a.bad_grads, 1ull);
+    float gq[4] = {g.x, g.y, g.z, g.w};
+    if (a.grad_out != nullptr) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (j0 + q < D.logical()) a.grad_out[j0 + q] = gq[q];
     }
-    m = a.b1 * m + (1.0f - a.b1) * g;
-    v = a.b2 * v + (1.0f - a.b2) * g * g;
-    w = w - a.lr * (m * a.inv_bc1) / (sqrtf(v * a.inv_bc2) + a.eps);
-    e = a.ema_c1 * w + a.ema_c2 * e;
-    a.m[j] = m;
-    a.v[j] = v;
-    a.w[j] = w;
-    a.ema[j] = e;
-    const int i = D.layer_of(j);
-    const int rel = j - D.pad_off(i), row = rel / D.cols(i), col = rel % D.cols(i);
-    const uint32_t off = D.img_byte(i, row, col);
-    *reinterpret_cast<__half*>(a.wimg + off) = __float2half_rn(w);
-    *reinterpret_cast<__half*>(a.eimg + off) = __float2half_rn(e);
+    if (!a.apply) return;
+    float mq[4] = {m.x, m.y, m.z, m.w}, vq[4] = {v.x, v.y, v.z, v.w}, wq[4] = {w.x, w.y, w.z, w.w},
+          eq[4] = {em.x, em.y, em.z, em.w};
+    uint32_t nbad = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float gg = gq[q] * a.inv_n;
+        if (!isfinite(gg)) {  // non-finite gradient entries are zeroed and counted
+            gg = 0.0f;
+            ++nbad;
+        }
+        mq[q] = a.b1 * mq[q] + (1.0f - a.b1) * gg;
+        vq[q] = a.b2 * vq[q] + (1.0f - a.b2) * gg * gg;
+        wq[q] = wq[q] - a.lr * (mq[q] * a.inv_bc1) / (sqrtf(vq[q] * a.inv_bc2) + a.eps);
+        eq[q] = a.ema_c1 * wq[q] + a.ema_c2 * eq[q];
+    }
+    if (nbad) atomicAdd(a.bad_grads, (unsigned long long)nbad);
+    *reinterpret_cast<float4*>(a.m + j0) = make_float4(mq[0], mq[1], mq[2], mq[3]);
+    *reinterpret_cast<float4*>(a.v + j0) = make_float4(vq[0], vq[1], vq[2], vq[3]);
+    *reinterpret_cast<float4*>(a.w + j0) = make_float4(wq[0], wq[1], wq[2], wq[3]);
+    *reinterpret_cast<float4*>(a.ema + j0) = make_float4(eq[0], eq[1], eq[2], eq[3]);
+    // 4 consecutive columns = 8 contiguous bytes of one 16-B chunk of the image
+    const uint32_t off = D.img_byte(i, o, 4 * c4);
+    *reinterpret_cast<uint2*>(a.wimg + off) = make_uint2(pack_h2(wq[0], wq[1]), pack_h2(wq[2], wq[3]));
+    *reinterpret_cast<uint2*>(a.eimg + off) = make_uint2(pack_h2(eq[0], eq[1]), pack_h2(eq[2], eq[3]));
     if (trc) a.dbg[4089 + 2 * (blockIdx.x != 0)] = global_ns();
+
 }
 
 // Fused peer all-reduce hand-off (nrc_train_frame_dp_peer), one thread: after

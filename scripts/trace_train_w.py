@@ -56,5 +56,6 @@ for k in range(4):
     for i, nm in names.items():
         col = g[:, i] - t0
         print(f"  {nm:14s} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}")
-    print(f"  adam blk0 {blk[4088] - t0:7d} -> {blk[4089] - t0:7d}   last blk {blk[4090] - t0:7d} -> {blk[4091] - t0:7d}")
+    print(f"  adam blk0 {blk[4088] - t0:7d} -> sum {blk[4084] - t0:7d} -> {blk[4089] - t0:7d}   "
+          f"last blk {blk[4090] - t0:7d} -> sum {blk[4085] - t0:7d} -> {blk[4091] - t0:7d}")
 c.L.nrc_debug_set_trace(c.h, None)

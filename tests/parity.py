@@ -2,9 +2,10 @@
 
 Radiance: per channel max_i |q_gpu - q_ref| / max_i |q_ref|          <= 1e-2
 Gradients: per matrix max |G_gpu - G_ref| / max |G_ref|              <= 3e-2
-Post-Adam: per matrix, over entries whose gradient signs agree,
+Post-Adam: per matrix, over entries whose gradients agree in sign (and,
+           within 100 eps_A of zero, within half their magnitude; R26),
            max |w_gpu - w_ref| / max |w_ref|                         <= 3e-2
-           (sign-flipped entries: <= 1% and each |G_ref| <= 3e-2 max|G_ref|)
+           (other entries: <= 1% and each |G_ref| <= 3e-2 max|G_ref|)
 The tolerances are north_star's (BASELINE.json)."""
 import numpy as np
 
@@ -51,33 +52,38 @@ def per_matrix_err(a, b, off=OFF):
     return out
 
 
-ADAM_EPS = 1e-8
+ADAM_EPS = 1e-8  # reading R11
 
 
-def post_adam_err(w_gpu, w_ref, g_gpu, g_ref, off=OFF, ill_frac_max=0.01):
-    """Per-matrix post-Adam error over sign-agreeing entries, plus the sign-flip
-    statistics (fraction, and worst |G_ref| / max|G_ref| among the flips).
+def post_adam_err(w_gpu, w_ref, g_gpu, g_ref, off=OFF):
+    """Per-matrix post-Adam error over agreeing entries, plus the statistics of
+    the others (fraction, and worst |G_ref| / max|G_ref| among them).
 
-    g_gpu / g_ref are batch-MEAN gradients.  Entries whose mean gradient is
-    within 10 eps_A of zero are excluded as well (reading R26): there the
-    first Adam step lr g / (|g| + eps_A) has slope up to lr / eps_A = 1e6 in g,
-    so a gradient difference at fp16 rounding level (~1e-9) moves w by up to
-    ~lr -- an ill-conditioned comparison, not a kernel error.  Their fraction
-    must stay <= ill_frac_max; the flips keep SURVEY 8(c)'s bounds."""
+    g_gpu / g_ref are batch-MEAN gradients.  Adam's first step is sign-like,
+    dw = -lr g / (|g| + eps_A): where both |g| exceed 100 eps_A the two steps
+    differ by < 0.01 lr whenever the signs agree, but where one side is within
+    100 eps_A of zero the step is a steep function of g.  So an entry counts
+    with the sign flips (reading R26) if the signs differ, or if one side is
+    within 100 eps_A of zero and the two gradients differ by more than half
+    of the oracle's (a near-cancellation, possible only where |g_ref| is
+    within the gradient tolerance of zero); those keep SURVEY 8(c)'s bounds
+    (<= 1% of the entries, each |G_ref| <= 3e-2 max|G_ref|).  Entries with an
+    exactly zero gradient on both sides (inactive one-blob bins, dead ReLUs)
+    agree."""
     w_gpu = np.asarray(w_gpu, np.float64); w_ref = np.asarray(w_ref, np.float64)
     g_gpu = np.asarray(g_gpu, np.float64); g_ref = np.asarray(g_ref, np.float64)
     OFF = off
-    ill = np.abs(g_ref) <= 10 * ADAM_EPS
-    assert ill.mean() <= ill_frac_max, f"{ill.mean():.4f} of the entries have |g| <= 10 eps_A"
     errs, flips, worst = [], 0, 0.0
     for i in range(len(OFF) - 1):
         s = slice(OFF[i], OFF[i + 1])
-        agree = (np.sign(g_gpu[s]) == np.sign(g_ref[s])) & ~ill[s]
-        gmax = max(np.max(np.abs(g_ref[s])), 1e-30)
-        flip = (np.sign(g_gpu[s]) != np.sign(g_ref[s])) & ~ill[s]
+        a, b = g_gpu[s], g_ref[s]
+        near = np.minimum(np.abs(a), np.abs(b)) <= 100 * ADAM_EPS
+        flip = (np.sign(a) != np.sign(b)) | (near & (np.abs(a - b) > 0.5 * np.abs(b)))
+        agree = ~flip
+        gmax = max(np.max(np.abs(b)), 1e-30)
         flips += int(flip.sum())
         if flip.any():
-            worst = max(worst, float(np.max(np.abs(g_ref[s][flip])) / gmax))
+            worst = max(worst, float(np.max(np.abs(b[flip])) / gmax))
         d = np.abs(w_gpu[s] - w_ref[s])[agree]
         errs.append(float(d.max() / max(np.max(np.abs(w_ref[s])), 1e-30)) if d.size else 0.0)
     return errs, flips / float(len(w_ref)), worst

@@ -88,7 +88,8 @@ def test_query_domain_parity(nrc, orc, n):
     recs = nrc_inputs.domain_records(n, seed=0xD5 + n)
     cache = domain_cache(nrc)
     tr = nrc_inputs.domain_records(8192, seed=0xD6)
-    tg = nrc_inputs.targets(tr, seed=3)
+    with np.errstate(over="ignore", invalid="ignore"):  # the analytic field at non-unit omega / n
+        tg = nrc_inputs.targets(tr, seed=3)
     tg = np.nan_to_num(tg, nan=0.5, posinf=1.0, neginf=0.0)
     cache.train_frame(dev(tr), dev(tg), 4, 2048, 5)
     q = cache.query(dev(recs)).cpu().numpy()
