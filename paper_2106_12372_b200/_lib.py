@@ -50,11 +50,14 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_missing:
-        _build.build()
-    if not os.path.exists(_build.LIB):
-        raise RuntimeError(f"libnrc.so not found at {_build.LIB}; run paper_2106_12372_b200.build.build()")
-    L = ctypes.CDLL(_build.LIB)
+    path = os.environ.get("NRC_LIB_VARIANT")  # diagnostics only: an A/B build of the same sources
+    if path is None:
+        if build_if_missing:
+            _build.build()
+        path = _build.LIB
+    if not os.path.exists(path):
+        raise RuntimeError(f"libnrc.so not found at {path}; run paper_2106_12372_b200.build.build()")
+    L = ctypes.CDLL(path)
     vp, u32, u64, st = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
     sz = ctypes.c_size_t
     P = ctypes.POINTER

@@ -26,35 +26,35 @@ struct QueryEntry {
     void (*launch)(int, const QueryArgs&, cudaStream_t);
     int groups;
 };
-// width ablation: one TMEM-activation configuration per width
-template <int G, int S, int W>
+// One TMEM-activation configuration per width and encoding (N4):
+// G groups; the paper's depth (5 hidden layers) is compiled straight-line, the
+// depth variants (N4) run the same kernel with a run-time layer loop.
+template <int G, int W, bool EXACT = false>
 struct QueryLauncherW {
     static cudaError_t set_smem() {
-        return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    query_ts_smem_bytes_nh<G, S, W>(TrainW<W>::kMaxNh));
+        const int bytes = query_ts_smem_bytes_nh<G, W>(TrainW<W>::kMaxNh);
+        cudaError_t e = cudaFuncSetAttribute(nrc_query_ts_kernel<G, W, 5, EXACT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return e;
+        return cudaFuncSetAttribute(nrc_query_ts_kernel<G, W, 0, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    bytes);
     }
     static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
-        nrc_query_ts_kernel<G, S, W><<<grid, 128 * G, query_ts_smem_bytes_nh<G, S, W>(int(qa.nh)), st>>>(qa);
+        const int smem = query_ts_smem_bytes_nh<G, W>(int(qa.nh));
+        if (qa.nh == 5)
+            nrc_query_ts_kernel<G, W, 5, EXACT><<<grid, 128 * G, smem, st>>>(qa);
+        else
+            nrc_query_ts_kernel<G, W, 0, EXACT><<<grid, 128 * G, smem, st>>>(qa);
     }
 };
-template <int G, int S, int W>
-struct QueryLauncherExact {
-    static cudaError_t set_smem() {
-        return cudaFuncSetAttribute(nrc_query_ts_kernel<G, S, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    query_ts_smem_bytes_nh<G, S, W>(TrainW<W>::kMaxNh));
-    }
-    static void launch(int grid, const QueryArgs& qa, cudaStream_t st) {
-        nrc_query_ts_kernel<G, S, W, true><<<grid, 128 * G, query_ts_smem_bytes_nh<G, S, W>(int(qa.nh)), st>>>(qa);
-    }
-};
-const QueryEntry kQuery64 = {&QueryLauncherW<5, 1, 64>::set_smem, &QueryLauncherW<5, 1, 64>::launch, 5};
-const QueryEntry kQueryExact = {&QueryLauncherExact<5, 1, 64>::set_smem, &QueryLauncherExact<5, 1, 64>::launch, 5};
+const QueryEntry kQuery64 = {&QueryLauncherW<5, 64>::set_smem, &QueryLauncherW<5, 64>::launch, 5};
+const QueryEntry kQueryExact = {&QueryLauncherW<5, 64, true>::set_smem, &QueryLauncherW<5, 64, true>::launch, 5};
 #ifndef NRC_W32_G
-#define NRC_W32_G 7  // 7 groups: 82 us vs 90 us with 5 at 1080p (scripts/try_w32.sh)
+#define NRC_W32_G 7  // 7 groups: 82 us vs 90 us with 5 at 1080p (round 1, 5 / 7 groups at width 32)
 #endif
-const QueryEntry kQueryW32 = {&QueryLauncherW<NRC_W32_G, 1, 32>::set_smem, &QueryLauncherW<NRC_W32_G, 1, 32>::launch,
+const QueryEntry kQueryW32 = {&QueryLauncherW<NRC_W32_G, 32>::set_smem, &QueryLauncherW<NRC_W32_G, 32>::launch,
                               NRC_W32_G};
-const QueryEntry kQueryW128 = {&QueryLauncherW<2, 1, 128>::set_smem, &QueryLauncherW<2, 1, 128>::launch, 2};
+const QueryEntry kQueryW128 = {&QueryLauncherW<2, 128>::set_smem, &QueryLauncherW<2, 128>::launch, 2};
 constexpr int kMaxPartials = 256; // train-kernel grid cap (>= SM count)
 
 // Runtime view of NetRt<W> (nrc_device.cuh) for the host code: width W,

@@ -19,7 +19,7 @@ struct QueryArgs {
     const uint8_t* wimg; // fp16 operand image, EMA or raw
     EncodeParams ep;
     uint32_t flags;      // NRC_FACTORIZE | NRC_CLAMP_QUERY
-    long long* dbg;      // per-round clock64 trace (builds with -DNRC_TRACE_QUERY only), else unused
+    long long* dbg;      // unused by the query kernel (diagnostics hook of the training kernels)
     // fused pixel reconstruction (nrc_query_accumulate): if image != nullptr,
     // image[3 pix[i] + c] += thr[3 i + c] * q_c instead of out
     const uint32_t* pix;

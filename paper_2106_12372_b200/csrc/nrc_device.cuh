@@ -357,6 +357,12 @@ struct EncodeParams {
     uint32_t exact;  // 1: sin / Gaussian primitives (NRC_EXACT_ENCODING, N4) instead of tri / quartic
 };
 
+// 1.0f if a >= b else 0.0f (one FSET)
+__device__ __forceinline__ float set_ge(float a, float b) {
+    float r;
+    asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
 // quartic(x) = 15/16 (1 - x^2)^2 on |x| <= 1, else 0: clamping
 // 1 - x^2 at 0 gives the compact support without a compare; 1 - x^2 <= 1, so
 // the clamp is a saturate folded into the FFMA (FFMA.SAT, same value).
@@ -482,15 +488,17 @@ __device__ __forceinline__ uint32_t encode_record_cheap(const float* rec, const 
         // is exact in fp32 (for v < 0 it is not: the result may need a finer
         // ulp than v, and the doublings below would amplify the rounding)
         const float v = fabsf(__fmul_rn(__fsub_rn(rec[a], ep.lo[a]), ep.inv[a]));
-        // m_d = 2^d v mod 2 by exact doubling: m_{d+1} = 2 (m_d - [m_d >= 1]);
-        // tri(2^d v) = 2 |m_d - 1| - 1, bit-identical to the direct form.
-        float m = v - 2.0f * floorf(v * 0.5f);
+        // m_d = 2^d v mod 2 by exact doubling: m_{d+1} = 2 u_d with
+        // u_d = m_d - [m_d >= 1] (exact); tri(2^d v) = 2 |m_d - 1| - 1
+        // (P:L678), bit-identical to the direct form.  Per value: t = RN(2 u - 1)
+        // (= RN(m - 1)), e, the 0/1 step [u >= 1/2] (one FSET) and u' = 2 u - step.
+        const float m0 = v - 2.0f * floorf(v * 0.5f);
+        float u = m0 - set_ge(m0, 1.0f);
 #pragma unroll
         for (int d = 0; d < 12; ++d) {
-            const float t = m - 1.0f;
+            const float t = d == 0 ? m0 - 1.0f : fmaf(2.0f, u, -1.0f);
             e[12 * a + d] = fmaf(2.0f, fabsf(t), -1.0f);
-            m = t >= 0.0f ? t : m;
-            m = m + m;
+            if (d > 0) u = fmaf(2.0f, u, -set_ge(u, 0.5f));
         }
     }
     float th, ph;

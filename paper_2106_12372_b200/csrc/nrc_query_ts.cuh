@@ -29,14 +29,9 @@ __host__ __device__ constexpr int ts_max_slots() {
     return 512 / ts_slot_cols<W>();
 }
 
-template <int G, int S, int W = 64>
-__host__ __device__ constexpr int query_ts_smem_bytes() {
-    return 1024 + NetDims<W>::kImg + G * kRecTileBytes + 8 * (1 + (S + 1) * G) + 16;
-}
-// with nh hidden layers (depth variants)
-template <int G, int S, int W = 64>
+template <int G, int W = 64>
 __host__ __device__ int query_ts_smem_bytes_nh(int nh) {
-    return 1024 + NetRt<W>(nh).img() + G * kRecTileBytes + 8 * (1 + (S + 1) * G) + 16;
+    return 1024 + NetRt<W>(nh).img() + G * kRecTileBytes + 8 * (1 + 2 * G) + 16;
 }
 
 // One layer's K chain (K/16 MMAs, A in TMEM at a + 8 k, B K-major blocks of
@@ -62,12 +57,18 @@ __device__ __forceinline__ void umma_ta_chain_commit(uint32_t d, uint32_t a, uin
     umma_commit(bar);
 }
 
-// G independent 4-warp groups, S tiles in flight per group, hidden width W,
-// EXACT: sin / Gaussian encoding primitives (N4).
-template <int G, int S, int W = 64, bool EXACT = false>
+// G independent 4-warp groups per CTA, one 128-row tile in flight per group,
+// hidden width W, NH hidden layers fixed at compile time (0: args.nh at run
+// time, the depth variants), EXACT: sin / Gaussian encoding primitives (N4).
+// Per tile a group runs straight-line code: encode -> TMEM A; then per layer
+// L the issuer lane's K chain + commit, the group waits, drains the fp32
+// accumulator and writes relu(fp16) back as the next A, group barrier; the
+// output layer's epilogue writes RGB.  The other groups' tiles fill the MMA
+// round trips.
+template <int G, int W = 64, int NH = 5, bool EXACT = false>
 __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args) {
-    static_assert(G * S <= ts_max_slots<W>(), "TMEM holds 512 columns");
-    const NetRt<W> D(int(args.nh));  // layer shapes / offsets at this depth
+    static_assert(G <= ts_max_slots<W>(), "TMEM holds 512 columns");
+    const NetRt<W> D(NH > 0 ? NH : int(args.nh));  // layer shapes / offsets at this depth
     const int nh = D.nh, img = D.img();
     constexpr uint32_t kACols = (W > 64 ? W : 64) / 2;
     extern __shared__ uint8_t smem_raw[];
@@ -82,15 +83,15 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     const float* sRec = reinterpret_cast<const float*>(smem + img + g * kRecTileBytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + img + G * kRecTileBytes);
     uint64_t* wbar = &bars[0];
-    uint64_t* mma_bar = &bars[1 + (S + 1) * g];  // [S]
-    uint64_t* rec_bar = &bars[1 + (S + 1) * g + S];
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + (S + 1) * G);
+    uint64_t* mma_bar = &bars[1 + 2 * g];
+    uint64_t* rec_bar = &bars[2 + 2 * g];
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 1 + 2 * G);
     uint32_t* deg_scratch = tmem_slot + 1;
     uint32_t deg = 0;  // zero-length omega / n vectors this thread encoded
 
     if (tid == 0) {
         *deg_scratch = 0;
-        for (int i = 0; i < 1 + (S + 1) * G; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < 1 + 2 * G; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -108,11 +109,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
 
     const uint64_t n = args.n;
     const uint64_t ntiles = (n + kTile - 1) / kTile;
-    const uint64_t q0 = uint64_t(blockIdx.x) * G + g;  // this group's k-th tile is q0 + k * Q
-    const uint64_t Q = uint64_t(gridDim.x) * G;
-    uint64_t k_next = 0;
-    uint32_t rec_phase = 0;
-
+    const uint64_t Q = uint64_t(gridDim.x) * G;  // this group's tiles: blockIdx.x G + g + k Q
     auto issue_records = [&](uint64_t t) {
         const uint64_t row0 = t * kTile;
         const uint64_t nv = (n - row0) < uint64_t(kTile) ? (n - row0) : uint64_t(kTile);
@@ -120,184 +117,131 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
         mbar_arrive_expect_tx(rec_bar, bytes);
         bulk_g2s(const_cast<float*>(sRec), args.rec + row0 * kRecFloats, bytes, rec_bar);
     };
-    if (issuer && q0 < ntiles) issue_records(q0);
+    uint64_t t = uint64_t(blockIdx.x) * G + g;
+    if (issuer && t < ntiles) issue_records(t);
     mbar_wait(wbar, 0);
 
     const uint32_t sW_a = smem_u32(sW);
     const uint32_t lane_off = (wq * 32u) << 16;
-    // D regions first (W columns each), then the A regions
-    auto d_col = [&](int s) -> uint32_t { return tmem_base + uint32_t(W) * uint32_t(g * S + s); };
-    auto a_col = [&](int s) -> uint32_t {
-        return tmem_base + uint32_t(W * G * S) + kACols * uint32_t(g * S + s);
-    };
+    const uint32_t t_d = tmem_base + uint32_t(W) * g;               // fp32 accumulator
+    const uint32_t t_a = tmem_base + uint32_t(W * G) + kACols * g;  // fp16 A operand
     // called by the whole issuer warp (converged)
-    auto issue_layer = [&](int s, int L) {
+    auto issue_layer = [&](int L) {
         const uint32_t wl = sW_a + uint32_t(D.img_off(L));
         const uint32_t idesc = make_idesc(128, D.rows(L), 0, 0);
-        const uint32_t d = warp_uniform(d_col(s)), a = warp_uniform(a_col(s));
+        const uint32_t d = warp_uniform(t_d), a = warp_uniform(t_a);
         const uint64_t b0 = warp_uniform(desc_kmajor(wl, 0));
         const uint64_t b1 = warp_uniform(desc_kmajor(wl + uint32_t(D.rows(L)) * 128u, 0));
         tc_fence_after();
         if (elect_one()) {
             if (D.cols(L) == 32)
-                umma_ta_chain_commit<2>(d, a, b0, b1, idesc, &mma_bar[s]);
+                umma_ta_chain_commit<2>(d, a, b0, b1, idesc, mma_bar);
             else if (D.cols(L) == 64)
-                umma_ta_chain_commit<4>(d, a, b0, b1, idesc, &mma_bar[s]);
+                umma_ta_chain_commit<4>(d, a, b0, b1, idesc, mma_bar);
             else
-                umma_ta_chain_commit<8>(d, a, b0, b1, idesc, &mma_bar[s]);
+                umma_ta_chain_commit<8>(d, a, b0, b1, idesc, mma_bar);
         }
         __syncwarp();
     };
-
-#ifdef NRC_TRACE_QUERY
-    // dbg[4096 + 8 (4 k + wq) + f] for the k-th round of CTA 0 group 0; f: 0 before
-    // the MMA wait, 1 MMA done, 2 epilogue done, 4 slot*16+layer, 5 encode start,
-    // 6 encode done; dbg[4096 + 3072 + 2k (+1)]: issue start / end
-    uint32_t kr = 0;
-    const bool trc = args.dbg != nullptr && blockIdx.x == 0 && g == 0 && (tid & 31) == 0;
-#define TQ(f) \
-    if (trc && kr < 96) args.dbg[4096 + 8 * (4 * kr + wq) + (f)] = clock64()
-#define TQI(f) \
-    if (trc && kr < 96 && issuer) args.dbg[4096 + 3072 + 2 * kr + (f)] = clock64()
-#define TQK() ++kr
-#else
-#define TQ(f)
-#define TQI(f)
-#define TQK()
-#endif
-    uint64_t row[S];
-    float fac[S][3];
-    int layer[S];
-    bool active[S];
-    uint32_t phase[S];
-
-    auto start_tile = [&](int s) -> bool {
-        const uint64_t t = q0 + k_next * Q;
-        if (t >= ntiles) return false;
-        TQ(5);
-        mbar_wait(rec_bar, rec_phase);
-        rec_phase ^= 1;
-        row[s] = t * kTile + r;
-        const bool valid = row[s] < n;
-        float rec[16];
-        const float4* src = reinterpret_cast<const float4*>(sRec + r * kRecFloats);
+    uint32_t rec_phase = 0, phase = 0;
+    auto mma_wait = [&]() {
+        mbar_wait(mma_bar, phase);
+        phase ^= 1u;
+        tc_fence_after();
+    };
+    // h_{L+1} = relu(acc) -> fp16, written over h_L in the group's TMEM A
+    auto hidden_epilogue = [&]() {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const float4 v = valid ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-            rec[4 * c + 0] = v.x;
-            rec[4 * c + 1] = v.y;
-            rec[4 * c + 2] = v.z;
-            rec[4 * c + 3] = v.w;
+        for (int part = 0; part < W / 32; ++part) {
+            uint32_t v[32];
+            tmem_ld32(t_d + lane_off + 32 * part, v);
+            uint32_t hp[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) hp[q] = pack_h2_relu(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+            tmem_st16_nowait(t_a + lane_off + 16 * part, hp);
         }
+        tmem_wait_st();
+        tc_fence_before();
+        named_bar_sync(1 + g, 128);
+    };
+
+#pragma unroll 1
+    for (; t < ntiles; t += Q) {
+        mbar_wait(rec_bar, rec_phase);
+        rec_phase ^= 1u;
+        const uint64_t row = t * kTile + r;
+        const bool valid = row < n;
+        float rec[16];
+        {
+            const float4* src = reinterpret_cast<const float4*>(sRec + r * kRecFloats);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) fac[s][c] = (args.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
+            for (int c = 0; c < 4; ++c) {
+                const float4 v = valid ? src[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+                rec[4 * c + 0] = v.x;
+                rec[4 * c + 1] = v.y;
+                rec[4 * c + 2] = v.z;
+                rec[4 * c + 3] = v.w;
+            }
+        }
+        float fac[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) fac[c] = (args.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
         {
             uint32_t h[32];
             const uint32_t dg = encode_record<EXACT>(rec, args.ep, h);
             deg += valid ? dg : 0u;
-            tmem_st32(a_col(s) + lane_off, h);  // includes tcgen05.wait::st
+            tmem_st32(t_a + lane_off, h);  // includes tcgen05.wait::st
         }
         fence_async_smem();  // record reads before the next TMA overwrite
         tc_fence_before();
-        TQ(6);
-        named_bar_sync(1 + g, 128);  // A written; records consumed; previous TMEM reads of slot s done
-        ++k_next;
+        named_bar_sync(1 + g, 128);  // A written; records consumed; the previous tile's TMEM reads done
         if (issuer_warp) {
-            const uint64_t tn = q0 + k_next * Q;
-            if (issuer && tn < ntiles) issue_records(tn);
+            if (issuer && t + Q < ntiles) issue_records(t + Q);
             __syncwarp();
-            issue_layer(s, 0);
+            issue_layer(0);
         }
-        return true;
-    };
-
+        if constexpr (NH > 0) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-        phase[s] = 0;
-        layer[s] = 0;
-        active[s] = start_tile(s);
-    }
-    bool any = active[0];
-#pragma unroll
-    for (int s = 1; s < S; ++s) any = any || active[s];
-
+            for (int L = 0; L < NH; ++L) {
+                mma_wait();
+                hidden_epilogue();
+                if (issuer_warp) issue_layer(L + 1);
+            }
+        } else {
 #pragma unroll 1
-    while (any) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            if (!active[s]) continue;
-            TQ(0);
-            mbar_wait(&mma_bar[s], phase[s]);
-            TQ(1);
-#ifdef NRC_TRACE_QUERY
-            if (trc && kr < 96) args.dbg[4096 + 8 * (4 * kr + wq) + 4] = s * 16 + layer[s];
-#endif
-            phase[s] ^= 1;
-            tc_fence_after();
-            const uint32_t t_d = d_col(s) + lane_off;
-            if (layer[s] < nh) {
-                // h_{L+1} = relu(acc) -> fp16, written over h_L in the slot's TMEM A
-#pragma unroll
-                for (int part = 0; part < W / 32; ++part) {
-                    uint32_t v[32];
-                    tmem_ld32(t_d + 32 * part, v);
-                    uint32_t hp[16];
-#pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        hp[q] = pack_h2_relu(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
-                    tmem_st16_nowait(a_col(s) + lane_off + 16 * part, hp);
-                }
-                tmem_wait_st();
-
-                tc_fence_before();
-                TQ(2);
-                named_bar_sync(1 + g, 128);
-                ++layer[s];
-                if (issuer_warp) {
-                    TQI(0);
-                    issue_layer(s, layer[s]);
-                    TQI(1);
-                }
-                TQK();
-            } else {
-                // output: q = max(0, y * (alpha + beta))
-                uint32_t v[4];
-                tmem_ld4(t_d, v);
-                tc_fence_before();
-                if (row[s] < n) {
-                    float qv[3];
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        qv[c] = __uint_as_float(v[c]) * fac[s][c];
-                        if (args.flags & 2u) qv[c] = fmaxf(qv[c], 0.0f);
-                    }
-                    if (args.image == nullptr) {
-                        float* o = args.out + row[s] * 3;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) o[c] = qv[c];
-                    } else {  // pixel += throughput * radiance
-                        float* px = args.image + size_t(__ldg(args.pix + row[s])) * 3;
-                        const float* th = args.thr + row[s] * 3;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) atomicAdd(px + c, __ldg(th + c) * qv[c]);
-                    }
-                }
-                layer[s] = 0;
-                TQ(2);
-                active[s] = start_tile(s);
-                TQK();
+            for (int L = 0; L < nh; ++L) {
+                mma_wait();
+                hidden_epilogue();
+                if (issuer_warp) issue_layer(L + 1);
             }
         }
-        any = active[0];
+        // output: q = max(0, y * (alpha + beta))
+        mma_wait();
+        uint32_t v[4];
+        tmem_ld4(t_d + lane_off, v);
+        tc_fence_before();
+        if (valid) {
+            float qv[3];
 #pragma unroll
-        for (int s = 1; s < S; ++s) any = any || active[s];
+            for (int c = 0; c < 3; ++c) {
+                qv[c] = __uint_as_float(v[c]) * fac[c];
+                if (args.flags & 2u) qv[c] = fmaxf(qv[c], 0.0f);
+            }
+            if (args.image == nullptr) {
+                float* o = args.out + row * 3;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) o[c] = qv[c];
+            } else {  // pixel += throughput * radiance
+                float* px = args.image + size_t(__ldg(args.pix + row)) * 3;
+                const float* th = args.thr + row * 3;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) atomicAdd(px + c, __ldg(th + c) * qv[c]);
+            }
+        }
     }
     tc_fence_before();
     block_count_add(args.degenerate, deg, deg_scratch);  // includes __syncthreads
     if (warp == 0) tmem_dealloc(tmem_base, 512);
-#undef TQ
-#undef TQI
-#undef TQK
 }
 
 }  // namespace nrc
