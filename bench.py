@@ -15,8 +15,10 @@ communication, training data-parallel: each rank takes l/N rows of every
 shuffled batch, one NCCL all-reduce of [gradient | loss sum] per step,
 identical Adam on every rank (--train-mode dp, the default).  Variants
 (SURVEY 8(f) N3): --train-mode replicated (one all-gather of the frame's
-records, then replicated training) and --train-mode allreduce-peer (the
-gradient all-reduce fused into the optimiser kernel over peer memory).
+records, then replicated training), --train-mode allreduce-peer (the
+gradient all-reduce fused into the optimiser kernel over peer memory) and
+--train-mode allreduce-nvls (the all-reduce in the NVSwitch: the optimiser
+reads every gradient entry with multimem.ld_reduce).
 Max-over-ranks device time.
 
 --impl reference: the fp64 CPU oracle (oracle/, as it stands) on the host
@@ -314,6 +316,11 @@ def run_nrc(args):
             # N3 (i): this rank's screen-region records, one all-gather, replicated training
             dpf.train_frame_replicated(d_rl, d_tl, TRAIN_S, TRAIN_L, seed, counts=t_counts)
             launches += dpf.last_launch_count
+        elif mode == "allreduce-nvls":
+            # SURVEY 8(e) mitigation 2 / N3 (ii): the gradient all-reduce done in the
+            # NVSwitch (multimem.ld_reduce read by the optimiser kernel; no NCCL call)
+            dpf.train_frame_allreduce_nvls(d_r, d_t, TRAIN_S, TRAIN_L, seed)
+            launches += dpf.last_launch_count
         elif mode == "allreduce-peer":
             # SURVEY 8(e) mitigation 2 / N3 (ii): the gradient all-reduce fused into
             # the optimiser over peer memory (no NCCL call)
@@ -464,11 +471,12 @@ def main():
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
-    ap.add_argument("--train-mode", choices=["dp", "replicated", "allreduce-peer"], default="dp",
+    ap.add_argument("--train-mode", choices=["dp", "replicated", "allreduce-peer", "allreduce-nvls"], default="dp",
                     help="N > 1 training: data-parallel with one NCCL all-reduce per step (dp, north_star's "
                          "partition, the default), one all-gather of the frame's records then replicated "
                          "training (replicated, SURVEY N3 (i)), or data-parallel with the gradient all-reduce "
-                         "fused into the optimiser over peer memory (allreduce-peer, N3 (ii))")
+                         "fused into the optimiser over peer memory (allreduce-peer, N3 (ii)) or done in the "
+                         "NVSwitch with multimem.ld_reduce feeding the optimiser (allreduce-nvls, N3 (ii))")
     args = ap.parse_args()
     if args.workload == "4k":
         global N_QUERY, METRIC, CONFIG_NAME

@@ -229,8 +229,47 @@ nrc_status nrc_train_frame_backward(nrc_handle* h, const nrc_record* d_rec, cons
 nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n_total,
                                    uint32_t s, uint32_t l, uint64_t shuffle_seed, uint32_t rank, uint32_t world,
                                    void* const* peer_state, float* d_losses, void* stream);
-/* Number of nrc_train_frame_dp_peer hand-offs that timed out (synchronous). */
+/* Number of nrc_train_frame_dp_peer / nrc_peer_barrier hand-offs that timed
+ * out (synchronous). */
 nrc_status nrc_dp_timeouts(nrc_handle* h, uint64_t* count);
+
+/* Data-parallel Adam + EMA step with the gradient all-reduce done in the
+ * NVSwitch (NVLink SHARP; SURVEY 8(e) mitigation 2 / 8(f) N3 (ii); the step
+ * of P:L896-902 on the batch of P:L491 split over the ranks).  mc_grad: the
+ * MULTICAST address (16-byte aligned) of a buffer that every rank holds in
+ * symmetric memory, laid out [logical gradient sum (nrc_param_count floats) |
+ * loss sum (1 float)] as written by nrc_train_backward /
+ * nrc_train_frame_backward.  The optimiser kernel reads every entry with
+ * multimem.ld_reduce.add.f32 (the sum over all ranks' copies, fp32 in the
+ * switch) and applies Adam + EMA on sum / n_global; d_loss (optional, 1
+ * float) receives loss sum / n_global.  The caller orders the call after
+ * every rank's gradient is written (nrc_peer_barrier) and keeps the buffer
+ * untouched until every rank's call has completed (e.g. two buffers used by
+ * step parity).  Not bitwise equal to single-GPU training (the switch's
+ * summation order).  Increments the step counter. */
+nrc_status nrc_train_apply_multimem(nrc_handle* h, const float* mc_grad, uint32_t n_global, float* d_loss,
+                                    void* stream);
+
+/* A single-process NVLS buffer on `device` (multicast object with this one
+ * device bound; driver multicast support required, else
+ * NRC_ERR_UNSUPPORTED): *d_uc = its ordinary (unicast) address, *d_mc = its
+ * multicast address, both >= bytes (rounded up to the multicast
+ * granularity), zero-filled.  For nrc_train_apply_multimem with one rank
+ * (the code path of the N-rank NVLS step on a one-GPU system; N ranks use
+ * symmetric memory from the framework, e.g. torch).  nrc_multicast_free
+ * takes the unicast address. */
+nrc_status nrc_multicast_alloc(int device, size_t bytes, void** d_uc, void** d_mc);
+nrc_status nrc_multicast_free(void* d_uc);
+
+/* Cross-rank barrier on the stream (one 32-thread kernel): adds 1 to every
+ * rank's counter (system-scope release; peer_counters: `world` device
+ * pointers, each rank's own u64 counter mapped into this process -- peer
+ * memory over NVLink, e.g. a symmetric-memory buffer -- in rank order,
+ * 8-byte aligned, zero before the first call) and waits until its own counter
+ * (peer_counters[rank]) reaches world x (number of calls so far).  All ranks
+ * must make the same sequence of calls; gives up after ~20 s (counted by
+ * nrc_dp_timeouts) instead of hanging. */
+nrc_status nrc_peer_barrier(nrc_handle* h, void* const* peer_counters, uint32_t rank, uint32_t world, void* stream);
 
 /* CUDA IPC for nrc_train_frame_dp_peer.  nrc_ipc_export: the 64-byte handle of
  * the device allocation that contains d_ptr and d_ptr's offset in it;

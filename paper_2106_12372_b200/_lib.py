@@ -37,7 +37,8 @@ SYMBOLS = [
     "nrc_set_params", "nrc_get_stats", "nrc_param_count", "nrc_status_string", "nrc_last_error",
     "nrc_frame_scratch_bytes", "nrc_frame_host", "nrc_selftest_umma", "nrc_last_launch_count",
     "nrc_assemble_targets", "nrc_query_accumulate", "nrc_train_frame_dp_peer",
-    "nrc_dp_timeouts", "nrc_ipc_export", "nrc_ipc_import", "nrc_ipc_close",
+    "nrc_dp_timeouts", "nrc_ipc_export", "nrc_ipc_import", "nrc_ipc_close", "nrc_train_apply_multimem",
+    "nrc_peer_barrier", "nrc_multicast_alloc", "nrc_multicast_free",
 ]
 
 
@@ -77,6 +78,10 @@ def load(build_if_missing: bool = True):
     L.nrc_train_frame_dp_peer.restype = st
     L.nrc_train_frame_dp_peer.argtypes = [vp, vp, vp, u32, u32, u32, u64, u32, u32, vp, vp, vp]
     L.nrc_dp_timeouts.restype = st; L.nrc_dp_timeouts.argtypes = [vp, P(u64)]
+    L.nrc_train_apply_multimem.restype = st; L.nrc_train_apply_multimem.argtypes = [vp, vp, u32, vp, vp]
+    L.nrc_peer_barrier.restype = st; L.nrc_peer_barrier.argtypes = [vp, vp, u32, u32, vp]
+    L.nrc_multicast_alloc.restype = st; L.nrc_multicast_alloc.argtypes = [ctypes.c_int, sz, P(vp), P(vp)]
+    L.nrc_multicast_free.restype = st; L.nrc_multicast_free.argtypes = [vp]
     L.nrc_ipc_export.restype = st; L.nrc_ipc_export.argtypes = [vp, vp, P(u64)]
     L.nrc_ipc_import.restype = st; L.nrc_ipc_import.argtypes = [vp, u64, P(vp)]
     L.nrc_ipc_close.restype = st; L.nrc_ipc_close.argtypes = [vp, u64]

@@ -143,6 +143,7 @@ struct nrc_handle {
     uint32_t launches;
     long long* dbg = nullptr;  // diagnostics only (nrc_debug_set_trace)
     unsigned long long dp_expect = 0;  // hand-off counter value after the last nrc_train_frame_dp_peer step
+    unsigned long long bar_expect = 0; // nrc_peer_barrier: this rank's counter value after the last barrier
     uint64_t dp_seq = 0;               // steps done by nrc_train_frame_dp_peer (partial-slot parity)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
@@ -858,6 +859,162 @@ nrc_status nrc_train_frame_dp_peer(nrc_handle* h, const nrc_record* d_rec, const
     }
     h->launches = launches;
     return NRC_OK;
+}
+
+nrc_status nrc_train_apply_multimem(nrc_handle* h, const float* mc_grad, uint32_t n_global, float* d_loss,
+                                    void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
+    h->launches = 0;
+    if (n_global == 0) return NRC_OK;
+    if (!mc_grad || !aligned(mc_grad, 16) || (d_loss && !aligned(d_loss, 4)))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply_multimem: NULL or misaligned pointer");
+    h->step += 1;
+    AdamWArgs aw = adam_w_args(h);
+    aw.grad_mc = mc_grad;
+    aw.apply = 1;
+    aw.inv_n = float(1.0 / double(n_global));
+    aw.loss_scale = aw.inv_n;
+    aw.loss_out = d_loss;
+    return launch_adam_w(h, aw, static_cast<cudaStream_t>(stream));
+}
+
+nrc_status nrc_peer_barrier(nrc_handle* h, void* const* peer_counters, uint32_t rank, uint32_t world, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    h->launches = 0;
+    if (!peer_counters || world == 0 || world > uint32_t(kMaxRanks) || rank >= world)
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_peer_barrier: 1..8 ranks, rank < world");
+    DpPeers peers{};
+    for (uint32_t p = 0; p < world; ++p) {
+        if (!peer_counters[p] || !aligned(peer_counters[p], 8))
+            return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_peer_barrier: NULL or misaligned counter");
+        peers.ctr[p] = static_cast<unsigned long long*>(peer_counters[p]);
+    }
+    h->bar_expect += world;
+    nrc_dp_exchange_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        peers, int(world), peers.ctr[rank], h->bar_expect, h->d_counters() + 5);
+    NRC_LAUNCHED(h, "nrc_dp_exchange_kernel");
+    return NRC_OK;
+}
+
+}  // extern "C"
+// ---- single-process NVLS multicast buffer (driver API through the runtime's
+// entry-point query: no link-time libcuda dependency)
+namespace {
+template <typename F>
+F driver_fn(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+    return reinterpret_cast<F>(fn);
+}
+struct McBuf {
+    CUmemGenericAllocationHandle mem = 0, mc = 0;
+    CUdeviceptr uc = 0, mcp = 0;
+    size_t size = 0;
+    int device = 0;
+};
+std::vector<McBuf> g_mc;  // live buffers (nrc_multicast_free releases)
+}  // namespace
+extern "C" {
+
+nrc_status nrc_multicast_alloc(int device, size_t bytes, void** d_uc, void** d_mc) {
+    if (!d_uc || !d_mc || bytes == 0) return NRC_ERR_INVALID_ARGUMENT;
+    *d_uc = *d_mc = nullptr;
+    using GetGran = CUresult (*)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+    using McCreate = CUresult (*)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+    using McAdd = CUresult (*)(CUmemGenericAllocationHandle, CUdevice);
+    using McBind = CUresult (*)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                                unsigned long long);
+    using MemCreate = CUresult (*)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    using Reserve = CUresult (*)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    using Map = CUresult (*)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    using Access = CUresult (*)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    using DevGet = CUresult (*)(CUdevice*, int);
+    using Attr = CUresult (*)(int*, CUdevice_attribute, CUdevice);
+    auto get_gran = driver_fn<GetGran>("cuMulticastGetGranularity");
+    auto mc_create = driver_fn<McCreate>("cuMulticastCreate");
+    auto mc_add = driver_fn<McAdd>("cuMulticastAddDevice");
+    auto mc_bind = driver_fn<McBind>("cuMulticastBindMem");
+    auto mem_create = driver_fn<MemCreate>("cuMemCreate");
+    auto reserve = driver_fn<Reserve>("cuMemAddressReserve");
+    auto map = driver_fn<Map>("cuMemMap");
+    auto access = driver_fn<Access>("cuMemSetAccess");
+    auto dev_get = driver_fn<DevGet>("cuDeviceGet");
+    auto attr = driver_fn<Attr>("cuDeviceGetAttribute");
+    if (!get_gran || !mc_create || !mc_add || !mc_bind || !mem_create || !reserve || !map || !access || !dev_get || !attr)
+        return NRC_ERR_UNSUPPORTED;
+    if (cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) return NRC_ERR_CUDA;
+    CUdevice dev;
+    if (dev_get(&dev, device) != CUDA_SUCCESS) return NRC_ERR_CUDA;
+    int mc_ok = 0;
+    if (attr(&mc_ok, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) != CUDA_SUCCESS || !mc_ok) return NRC_ERR_UNSUPPORTED;
+    CUmulticastObjectProp prop{};
+    prop.numDevices = 1;
+    prop.size = bytes;
+    size_t gran = 0;
+    if (get_gran(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || gran == 0) return NRC_ERR_CUDA;
+    McBuf b;
+    b.device = device;
+    b.size = (bytes + gran - 1) / gran * gran;
+    prop.size = b.size;
+    if (mc_create(&b.mc, &prop) != CUDA_SUCCESS) return NRC_ERR_UNSUPPORTED;
+    if (mc_add(b.mc, dev) != CUDA_SUCCESS) return NRC_ERR_CUDA;
+    CUmemAllocationProp mp{};
+    mp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    mp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    mp.location.id = device;
+    if (mem_create(&b.mem, b.size, &mp, 0) != CUDA_SUCCESS) return NRC_ERR_OUT_OF_MEMORY;
+    if (mc_bind(b.mc, 0, b.mem, 0, b.size, 0) != CUDA_SUCCESS) return NRC_ERR_CUDA;
+    CUmemAccessDesc ad{};
+    ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ad.location.id = device;
+    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (reserve(&b.uc, b.size, gran, 0, 0) != CUDA_SUCCESS || map(b.uc, b.size, 0, b.mem, 0) != CUDA_SUCCESS ||
+        access(b.uc, b.size, &ad, 1) != CUDA_SUCCESS)
+        return NRC_ERR_CUDA;
+    if (reserve(&b.mcp, b.size, gran, 0, 0) != CUDA_SUCCESS || map(b.mcp, b.size, 0, b.mc, 0) != CUDA_SUCCESS ||
+        access(b.mcp, b.size, &ad, 1) != CUDA_SUCCESS)
+        return NRC_ERR_CUDA;
+    if (cudaMemset(reinterpret_cast<void*>(b.uc), 0, b.size) != cudaSuccess) return NRC_ERR_CUDA;
+    *d_uc = reinterpret_cast<void*>(b.uc);
+    *d_mc = reinterpret_cast<void*>(b.mcp);
+    g_mc.push_back(b);
+    return NRC_OK;
+}
+
+nrc_status nrc_multicast_free(void* d_uc) {
+    using Unmap = CUresult (*)(CUdeviceptr, size_t);
+    using Free = CUresult (*)(CUdeviceptr, size_t);
+    using Release = CUresult (*)(CUmemGenericAllocationHandle);
+    using Unbind = CUresult (*)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+    using DevGet = CUresult (*)(CUdevice*, int);
+    auto unmap = driver_fn<Unmap>("cuMemUnmap");
+    auto afree = driver_fn<Free>("cuMemAddressFree");
+    auto release = driver_fn<Release>("cuMemRelease");
+    auto unbind = driver_fn<Unbind>("cuMulticastUnbind");
+    auto dev_get = driver_fn<DevGet>("cuDeviceGet");
+    for (size_t i = 0; i < g_mc.size(); ++i) {
+        McBuf& b = g_mc[i];
+        if (reinterpret_cast<void*>(b.uc) != d_uc) continue;
+        if (!unmap || !afree || !release || !unbind || !dev_get) return NRC_ERR_UNSUPPORTED;
+        cudaDeviceSynchronize();
+        CUdevice dev;
+        dev_get(&dev, b.device);
+        unmap(b.mcp, b.size);
+        afree(b.mcp, b.size);
+        unmap(b.uc, b.size);
+        afree(b.uc, b.size);
+        unbind(b.mc, dev, 0, b.size);
+        release(b.mc);
+        release(b.mem);
+        g_mc.erase(g_mc.begin() + long(i));
+        return NRC_OK;
+    }
+    return NRC_ERR_INVALID_ARGUMENT;
 }
 
 nrc_status nrc_dp_timeouts(nrc_handle* h, uint64_t* count) {

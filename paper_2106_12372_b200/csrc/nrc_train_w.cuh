@@ -481,6 +481,21 @@ __device__ __forceinline__ float4 ld_cg_v4(const float* p) {
                  : "memory");
     return v;
 }
+// NVLink SHARP (NVLS): the sum over every rank's copy of a multicast-mapped
+// buffer, reduced in the NVSwitch (fp32 accumulate) and returned to this SM
+__device__ __forceinline__ float4 multimem_ld_reduce_v4(const float* mc) {
+    float4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(mc)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ float multimem_ld_reduce_f32(const float* mc) {
+    float v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(mc) : "memory");
+    return v;
+}
 __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
     return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
@@ -508,6 +523,10 @@ struct AdamWArgs {
     // small: a 2 KB parameter block measurably slowed every launch.)
     const float* const* tile_part;
     const float* const* tile_loss;
+    // NVLS mode (nrc_train_apply_multimem), if grad_mc != nullptr: the
+    // multicast address of every rank's [logical gradient sum | loss sum];
+    // g = multimem.ld_reduce (the all-reduce done in the switch), loss likewise
+    const float* grad_mc;
 };
 
 template <int W>
@@ -560,6 +579,9 @@ __global__ void __launch_bounds__(kAdamThreads, 3) nrc_adam_w_kernel(AdamWArgs a
 #pragma unroll
             for (int q = 0; q < 8; ++q) g = f4_add(g, sred[q][lane]);
         }
+    } else if (wp == 0 && a.grad_mc != nullptr) {
+        // 4 consecutive logical entries (j0 % 4 == 0; W5's pad rows are beyond logical)
+        if (j0 < D.logical()) g = multimem_ld_reduce_v4(a.grad_mc + j0);
     } else if (wp == 0) {
         float gg[4];
 #pragma unroll
@@ -569,7 +591,12 @@ __global__ void __launch_bounds__(kAdamThreads, 3) nrc_adam_w_kernel(AdamWArgs a
     if (wp != 0) return;
     if (blockIdx.x == 0 && a.loss_out != nullptr) {
         float s = 0.0f;
-        for (int p = lane; p < a.nloss; p += 32) s += a.tile_part != nullptr ? ld_sys_f32(a.tile_loss[p]) : __ldcg(a.loss_part + p);
+        if (a.grad_mc != nullptr) {
+            if (lane == 0) s = multimem_ld_reduce_f32(a.grad_mc + D.logical());
+        } else {
+            for (int p = lane; p < a.nloss; p += 32)
+                s += a.tile_part != nullptr ? ld_sys_f32(a.tile_loss[p]) : __ldcg(a.loss_part + p);
+        }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane == 0) *a.loss_out = s * a.loss_scale;

@@ -157,6 +157,70 @@ class DataParallelFrame:
         self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
         return out
 
+    def _nvls_setup(self):
+        """Symmetric memory for train_frame_allreduce_nvls: two [gradient |
+        loss sum] buffers (step parity) + one barrier counter per rank, mapped
+        on every rank (torch symmetric memory over the process group) with a
+        multicast (NVLS) address."""
+        import torch.distributed._symmetric_memory as symm_mem
+        self._nvls_stride = (NPARAM + 1 + 63) // 64 * 64  # floats per buffer, 256-B aligned
+        n = 2 * self._nvls_stride + 64
+        esz = 4
+        buf = symm_mem.empty(n, dtype=torch.float32, device=self.device)
+        buf.zero_()
+        gname = (self.group or dist.group.WORLD).group_name
+        hdl = symm_mem.rendezvous(buf, gname)
+        if getattr(hdl, "multicast_ptr", 0):
+            self._nvls_hdl, self._nvls_buf = hdl, buf
+            mc, ctr = hdl.multicast_ptr, [int(p) + 2 * self._nvls_stride * esz for p in hdl.buffer_ptrs]
+        elif self.world == 1:
+            # one rank: a single-device multicast object from libnrc (torch exports
+            # multicast handles for sharing, which some systems refuse)
+            from .nrc import multicast_alloc
+            self._nvls_buf, mc = multicast_alloc(n, self.device)
+            ctr = [self._nvls_buf.data_ptr() + 2 * self._nvls_stride * esz]
+        else:
+            raise RuntimeError("NVLS multicast is not available on this system (symmetric memory without multicast)")
+        self._nvls_mc = [mc + k * self._nvls_stride * esz for k in range(2)]
+        self._nvls_ctr = ctr
+        self._nvls_seq = 0
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)  # zeroed everywhere before any rank signals
+
+    def train_frame_allreduce_nvls(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int,
+                                   shuffle_seed: int, losses: Optional[torch.Tensor] = None
+                                   ) -> Optional[torch.Tensor]:
+        """SURVEY 8(e) mitigation 2 / 8(f) N3 (ii): data-parallel training with
+        the gradient all-reduce done in the NVSwitch.  Per step: this rank's
+        rows of the shuffled batch -> its [gradient | loss sum] into a
+        symmetric buffer (by step parity), a cross-rank barrier kernel, then the
+        optimiser reads every entry as multimem.ld_reduce (the sum over the
+        ranks) and applies Adam + EMA -- no NCCL call.  Not bitwise equal to
+        single-GPU training (the switch's fp32 summation order)."""
+        if getattr(self, "_nvls_buf", None) is None:
+            self._nvls_setup()
+        n_total = int(records.shape[0])
+        s, l = frame_batches(n_total, s, l)
+        launches = 0
+        if s == 0:
+            self.last_launch_count = 0
+            return losses
+        lo, hi = shard(l, self.rank, self.world)
+        for j in range(s):
+            par = self._nvls_seq & 1
+            base = par * self._nvls_stride
+            grad = self._nvls_buf[base:base + NPARAM]
+            loss_sum = self._nvls_buf[base + NPARAM:base + NPARAM + 1]
+            self.cache.train_frame_backward(records, targets, l, shuffle_seed, j, lo, hi, grad, loss_sum)
+            launches += getattr(self.cache, "last_launch_count", 0)
+            self.cache.peer_barrier(self._nvls_ctr, self.rank, self.world)
+            launches += 1
+            self.cache.train_apply_multimem(self._nvls_mc[par], l, None if losses is None else losses[j:j + 1])
+            launches += getattr(self.cache, "last_launch_count", 0)
+            self._nvls_seq += 1
+        self.last_launch_count = launches
+        return losses
+
     def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
                     losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
         """All s steps of the frame's training on the full (replicated) record

@@ -295,6 +295,23 @@ class RadianceCache:
                                                    _ptr(losses), _stream(stream)), "nrc_train_frame_dp_peer")
         return losses
 
+    def train_apply_multimem(self, mc_ptr: int, n_global: int, loss: Optional[torch.Tensor] = None, stream=None):
+        """nrc_train_apply_multimem: Adam + EMA on the NVSwitch-reduced sum of
+        every rank's [gradient | loss sum] buffer (mc_ptr: its multicast
+        address), divided by n_global."""
+        if loss is not None:
+            self._f32(loss, tuple(loss.shape), "loss")
+        self._check(self.L.nrc_train_apply_multimem(self.h, ctypes.c_void_p(int(mc_ptr)), int(n_global), _ptr(loss),
+                                                    _stream(stream)), "nrc_train_apply_multimem")
+
+    def peer_barrier(self, counter_ptrs, rank: int, world: int, stream=None):
+        """nrc_peer_barrier: cross-rank barrier on the stream over peer-mapped
+        u64 counters (counter_ptrs: every rank's counter, own included)."""
+        if len(counter_ptrs) != world:
+            raise NRCError("one counter per rank required")
+        ps = (ctypes.c_void_p * world)(*[int(p) for p in counter_ptrs])
+        self._check(self.L.nrc_peer_barrier(self.h, ps, int(rank), int(world), _stream(stream)), "nrc_peer_barrier")
+
     def dp_timeouts(self) -> int:
         c = ctypes.c_uint64()
         self._check(self.L.nrc_dp_timeouts(self.h, ctypes.byref(c)), "nrc_dp_timeouts")
@@ -412,6 +429,49 @@ class RadianceCache:
             self.close()
         except Exception:
             pass
+
+
+class _McOwner:
+    """Releases a libnrc multicast buffer when the tensor view dies."""
+
+    def __init__(self, L, uc):
+        self.L, self.uc = L, uc
+
+    def __del__(self):
+        try:
+            self.L.nrc_multicast_free(ctypes.c_void_p(self.uc))
+        except Exception:
+            pass
+
+
+def multicast_alloc(n_floats: int, device=None):
+    """nrc_multicast_alloc: a zeroed fp32 buffer of n_floats on one GPU with a
+    multicast (NVLS) mapping.  Returns (tensor view of the unicast mapping,
+    multicast address)."""
+    L = _lib.load()
+    dev = torch.device(device if device is not None else "cuda")
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+    st = L.nrc_multicast_alloc(int(idx), int(n_floats) * 4, ctypes.byref(uc), ctypes.byref(mc))
+    if st != 0:
+        raise RuntimeError(f"NVLS multicast is not available: nrc_multicast_alloc {L.nrc_status_string(st).decode()}")
+    owner = _McOwner(L, uc.value)
+    # a tensor view of the unicast mapping; the owner frees it with the tensor
+    t = _tensor_from_ptr(uc.value, int(n_floats), dev, owner)
+    return t, int(mc.value)
+
+
+def _tensor_from_ptr(ptr: int, n: int, dev: torch.device, owner) -> torch.Tensor:
+    """A float32 tensor viewing n floats of device memory at ptr (kept alive by owner)."""
+    class _Cai:
+        def __init__(self):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                             "strides": None}
+            self._owner = owner
+    holder = _Cai()
+    t = torch.as_tensor(holder, device=dev)
+    t._nrc_owner = holder  # the tensor keeps the owner (and so the mapping) alive
+    return t
 
 
 def selftest_umma(mode: int, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:

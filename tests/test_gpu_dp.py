@@ -77,3 +77,35 @@ def test_replicated_frame_world1_equals_train_frame(group):
     np.testing.assert_array_equal(lb.cpu().numpy(), la)
     np.testing.assert_array_equal(b.get_params("train"), a.get_params("train"))
     np.testing.assert_array_equal(b.get_params("ema"), a.get_params("ema"))
+
+
+def test_nvls_frame_world1_equals_dp_frame(group):
+    """SURVEY N3 (ii), the all-reduce in the NVSwitch (multimem.ld_reduce into
+    the optimiser, nrc_train_apply_multimem + nrc_peer_barrier over torch
+    symmetric memory): with one rank the switch sum is the rank's own buffer,
+    so the frame equals the NCCL data-parallel frame bitwise; both match the
+    single-GPU frame's losses.  Skipped where the system has no multicast."""
+    import paper_2106_12372_b200 as nrc
+    n, s, l, seed = 8192 + 3, 4, 2048, 29
+    recs, tg = nrc_inputs.train_frame(4, n=n, noise=0.3)
+    d_r = torch.from_numpy(recs).cuda()
+    d_t = torch.from_numpy(tg).cuda()
+    a, b = nrc.RadianceCache(), nrc.RadianceCache()
+    fa = nrc.DataParallelFrame(a, device=torch.device("cuda", 0))
+    fb = nrc.DataParallelFrame(b, device=torch.device("cuda", 0))
+    la = torch.zeros(s, dtype=torch.float32, device="cuda")
+    lb = torch.zeros(s, dtype=torch.float32, device="cuda")
+    try:
+        fb.train_frame_allreduce_nvls(d_r, d_t, s, l, seed, lb)
+    except RuntimeError as e:
+        if "multicast" in str(e).lower():
+            pytest.skip(str(e))
+        raise
+    fa.train_frame(d_r, d_t, s, l, seed, la)
+    fb.train_frame_allreduce_nvls(d_r, d_t, s, l, seed + 1, lb)
+    fa.train_frame(d_r, d_t, s, l, seed + 1, la)  # a second frame: the other buffer parity
+    np.testing.assert_array_equal(lb.cpu().numpy(), la.cpu().numpy())
+    np.testing.assert_array_equal(b.get_params("train"), a.get_params("train"))
+    np.testing.assert_array_equal(b.get_params("ema"), a.get_params("ema"))
+    assert b.dp_timeouts() == 0
+    assert fb.last_launch_count == 4 * s  # partials + reduce, barrier, optimiser per step
