@@ -361,6 +361,44 @@ def run_nrc(args):
     replicas = None
     if world > 1:  # bitwise-identical replicas after the timed frames (outside the timing)
         replicas = "identical crc32 %08x" % dpf.verify_replicas()
+    # N3 comparison: the frame's training through every multi-GPU
+    # partition, each on a fresh cache, device time max over ranks
+    mode_ms = {}
+    if world > 1 and not args.no_mode_table:
+        for m in ["dp", "replicated", "allreduce-peer", "allreduce-nvls"]:
+            try:
+                c2 = nrc.RadianceCache(nrc.Config(max_batch=max(N_QUERY, N_TRAIN)), device=local)
+                f2 = nrc.DataParallelFrame(c2, device=dev)
+                d_r, d_t, _, _, d_rl, d_tl = frames[0]
+
+                def train(fi, m=m, c2=c2, f2=f2):
+                    d_r, d_t, _, _, d_rl, d_tl = frames[fi % 2]
+                    if m == "dp":
+                        f2.train_frame(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi)
+                    elif m == "replicated":
+                        f2.train_frame_replicated(d_rl, d_tl, TRAIN_S, TRAIN_L, 1000 + fi, counts=t_counts)
+                    elif m == "allreduce-peer":
+                        f2.train_frame_allreduce_peer(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi)
+                    else:
+                        f2.train_frame_allreduce_nvls(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi)
+                for i in range(3):
+                    train(i)
+                torch.cuda.synchronize()
+                barrier()
+                ts = []
+                for i in range(max(args.steps, 5)):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    train(i)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1))
+                t = torch.tensor([float(np.median(ts))], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                mode_ms[m] = {"train_ms": float(t[0]), "replicas": "identical crc32 %08x" % f2.verify_replicas()}
+            except Exception as e:  # e.g. no NVLS multicast on this system
+                mode_ms[m] = {"unavailable": str(e).splitlines()[0][:160]}
+            barrier()
     st = stats_ms(step_ms)
     ms, q_ms, t_ms = st["median"], float(np.median(q_list)), float(np.median(t_list))
     pct = [st["p10"], st["p50"], st["p90"]]
@@ -438,6 +476,8 @@ def run_nrc(args):
     }
     if replicas:
         line["replicas"] = replicas
+    if mode_ms:
+        line["train_modes"] = mode_ms
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -468,6 +508,8 @@ def main():
     ap.add_argument("--impl", choices=["nrc", "reference"], default="nrc")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer (e2e) leg (profiling runs)")
+    ap.add_argument("--no-mode-table", action="store_true",
+                    help="N > 1: skip the per-partition training comparison (train_modes)")
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")

@@ -30,6 +30,8 @@ def test_bench_two_ranks_shared_gpu(mode):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
            "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--train-mode", mode]
+    if mode != "dp":
+        cmd.append("--no-mode-table")
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -38,3 +40,8 @@ def test_bench_two_ranks_shared_gpu(mode):
     assert line["n_gpus"] == 2 and line["steps"] == 2 and line["config"]["parallelism"] == f"{mode}2"
     assert line["replicas"].startswith("identical")
     assert line["gpu_launches"] > 0 and line["value"] > 0
+    if mode == "dp":  # the N3 comparison: every partition trained the frame (NVLS where multicast exists)
+        tm = line["train_modes"]
+        assert set(tm) == {"dp", "replicated", "allreduce-peer", "allreduce-nvls"}
+        for m in ("dp", "replicated", "allreduce-peer"):
+            assert tm[m]["train_ms"] > 0 and tm[m]["replicas"].startswith("identical"), tm
