@@ -147,6 +147,7 @@ struct nrc_handle {
     uint64_t dp_seq = 0;               // steps done by nrc_train_frame_dp_peer (partial-slot parity)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
+    bool train_legacy = false;    // NRC_TRAIN_LEGACY=1: nrc_train_w_kernel for one-tile batches too
     int train_ctas = 0;           // cap on the train grid (0: one CTA per tile up to all SMs)
     // nrc_frame_host pipelining: host->device and device->host copy streams and events
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
@@ -381,6 +382,8 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     // diagnostics / probes only: cap the query or train grid
     if (const char* e = std::getenv("NRC_QUERY_CTAS")) h->query_ctas = std::atoi(e);
     if (const char* e = std::getenv("NRC_TRAIN_CTAS")) h->train_ctas = std::atoi(e);
+    // diagnostics / A-B only: the single-schedule partials kernel for every batch
+    if (const char* e = std::getenv("NRC_TRAIN_LEGACY")) h->train_legacy = std::atoi(e) != 0;
     if ((s = cuda_check(h, kQuery64.set_smem(), "cudaFuncSetAttribute(query)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW32.set_smem(), "cudaFuncSetAttribute(query w32)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW128.set_smem(), "cudaFuncSetAttribute(query w128)")) != NRC_OK) return bail(s);
@@ -396,7 +399,17 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
                         "cudaFuncSetAttribute(train w128)")) != NRC_OK ||
         (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_w_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 TrainW<64>::smem_bytes(TrainW<64>::kMaxNh)),
-                        "cudaFuncSetAttribute(train w64 exact)")) != NRC_OK)
+                        "cudaFuncSetAttribute(train w64 exact)")) != NRC_OK ||
+        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TrainWs<32>::smem_bytes(TrainWs<32>::kMaxNh)),
+                        "cudaFuncSetAttribute(train ws32)")) != NRC_OK ||
+        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_ws_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TrainWs<64>::smem_bytes(TrainWs<64>::kMaxNh)),
+                        "cudaFuncSetAttribute(train ws64)")) != NRC_OK ||
+        (s = cuda_check(h, cudaFuncSetAttribute(nrc_train_ws_kernel<64, true>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                TrainWs<64>::smem_bytes(TrainWs<64>::kMaxNh)),
+                        "cudaFuncSetAttribute(train ws64 exact)")) != NRC_OK)
         return bail(s);
 
     // Glorot-uniform init from the counter-based splitmix64 stream (R16):
@@ -557,6 +570,19 @@ static int train_grid(const nrc_handle* h, uint32_t n) {
 // The partials kernel for this handle's width / encoding, one tile per CTA up to `grid`.
 static cudaError_t launch_train_w_grid(nrc_handle* h, const TrainArgs& ta, int grid, cudaStream_t st) {
     const int nh = h->wi.nh;
+    // one tile per CTA at width <= 64, depth <= 6: the split schedule
+    // (nrc_train_ws_kernel, wgrads off the backward critical path)
+    const bool one_tile = uint64_t(grid) * kTile >= uint64_t(ta.n);
+    if (one_tile && nh <= TrainWs<64>::kMaxNh && h->wi.W <= 64 && !h->train_legacy) {
+        if (h->wi.W == 32)
+            return launch_pdl(nrc_train_ws_kernel<32>, dim3(grid), dim3(TrainWs<32>::kThreads),
+                              TrainWs<32>::smem_bytes(nh), st, ta);
+        if (h->ep.exact)
+            return launch_pdl(nrc_train_ws_kernel<64, true>, dim3(grid), dim3(TrainWs<64>::kThreads),
+                              TrainWs<64>::smem_bytes(nh), st, ta);
+        return launch_pdl(nrc_train_ws_kernel<64>, dim3(grid), dim3(TrainWs<64>::kThreads), TrainWs<64>::smem_bytes(nh),
+                          st, ta);
+    }
     if (h->wi.W == 32)
         return launch_pdl(nrc_train_w_kernel<32>, dim3(grid), dim3(128), TrainW<32>::smem_bytes(nh), st, ta);
     if (h->wi.W == 128)

@@ -16,6 +16,7 @@
 #include "nrc_common.cuh"
 #include "nrc_query_ts.cuh"
 #include "nrc_train_w.cuh"
+#include "nrc_train_ws.cuh"
 
 namespace nrc {
 

@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
     block_count_add(a.degenerate, deg, deg_scratch);
     if (warp == 0) tmem_dealloc(tmem_base, T::kTmemCols);
 }
-#undef NRC_WTRC
+
 
 // Reduce + Adam + EMA at width W.  Partials use the chunk-major layout
 // (part_index): thread t of block b owns float4 element e = 32 b + lane of
