@@ -47,8 +47,10 @@ def main(tag, d):
     print("\n".join(lines))
     tp = os.path.join(prof, f"{tag}_traffic.json")
     traffic = json.load(open(tp)) if os.path.exists(tp) else {}  # keep kernels not re-captured this time
+    traffic = {k: v for k, v in traffic.items() if k != "nrc_train_kernel"}  # (pruned in round 2)
     for name, rep in [("nrc_query_ts_kernel", "prof_query.ncu-rep"), ("nrc_train_w_kernel", "prof_train.ncu-rep"),
-                      ("nrc_train_w_kernel<64>", "prof_train_w.ncu-rep"), ("nrc_adam_w_kernel<64>", "prof_adam_w.ncu-rep")]:
+                      ("nrc_train_w_kernel<64>", "prof_train_w.ncu-rep"), ("nrc_adam_w_kernel<64>", "prof_adam_w.ncu-rep"),
+                      ("nrc_train_ws_kernel<64>", "prof_train_ws.ncu-rep")]:
         p = os.path.join(d, rep)
         if os.path.exists(p):
             m = raw(p, ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"])

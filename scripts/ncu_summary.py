@@ -32,15 +32,16 @@ def main(rep, top=30):
     for name, val in sorted(st, key=lambda x: -float(x[1] or 0))[:10]:
         print(f"  {name[34:-23]:30s} {val}")
     src = page(rep, "source", ["--print-source", "sass"])
-    hh = src[1]
-    data = src[2:]
+    hi = [i for i, r in enumerate(src) if "Warp Stall Sampling (All Samples)" in r][0]
+    hh = src[hi]
+    data = [r for r in src[hi + 1:] if len(r) == len(hh) and r[0].startswith("0x")]
     si, sti, exi = hh.index("Source"), hh.index("Warp Stall Sampling (All Samples)"), hh.index("Instructions Executed")
-    tot = sum(int(r[sti]) for r in data) or 1
+    tot = sum(int(r[sti] or 0) for r in data) or 1
     print(f"-- top stall instructions ({tot} samples, {len(data)} SASS)")
-    idx = sorted(range(len(data)), key=lambda i: -int(data[i][sti]))[:top]
+    idx = sorted(range(len(data)), key=lambda i: -int(data[i][sti] or 0))[:top]
     for i in sorted(idx):
         r = data[i]
-        print(f"{i:5d} {100 * int(r[sti]) / tot:5.1f}% exec={r[exi]:>9s} {r[si].strip()[:80]}")
+        print(f"{i:5d} {100 * int(r[sti] or 0) / tot:5.1f}% exec={r[exi]:>9s} {r[si].strip()[:80]}")
     c, s = Counter(), Counter()
     for r in data:
         toks = r[si].strip().split()
@@ -48,7 +49,7 @@ def main(rep, top=30):
             continue
         op = toks[1] if toks[0].startswith("@") else toks[0]
         op = op.split(".")[0]
-        c[op] += int(r[exi]); s[op] += int(r[sti])
+        c[op] += int(r[exi] or 0); s[op] += int(r[sti] or 0)
     print("-- opcode mix (executed warp-instructions)")
     print("  ", ", ".join(f"{op}:{n}" for op, n in c.most_common(25)))
 
