@@ -29,6 +29,8 @@ for hw, nh in ((32, 5), (128, 5), (64, 2), (32, 8)):  # width / depth variants (
     cw = nrc.RadianceCache(nrc.Config(hidden_width=hw, n_hidden_layers=nh))
     cw.train_frame(dev(tr), dev(tg), 2, 300, 5)
     cw.query(dev(recs))
+big = nrc_inputs.train_frame(1, n=40000)  # > 148 tiles: the single-schedule partials kernel
+c.train_step(dev(big[0]), dev(big[1]))
 cd = nrc.RadianceCache()  # fused peer all-reduce path at world 1 (hand-off kernel, table-driven optimiser)
 cd.train_frame_dp_peer(dev(tr), dev(tg), 2, 1024, 7, 0, 1, [cd.state_ptr])
 torch.cuda.synchronize()
