@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
 // (part_index): thread t of block b owns float4 element e = 32 b + lane of
 // that layout, i.e. parameters (o, 4 c4 .. 4 c4 + 3) of one layer.
 //   partials != nullptr: g = sum over p < np of partials[p][e] (ascending p
-//   within each of the 8 warps, p = w mod 8, then the 8 warp sums in warp
+//   within each of the kAdamWarps warps, p = w mod kAdamWarps, then the warp sums in warp
 //   order: deterministic for a given np);
 //   tile_part != nullptr: the same over the peer table;
 //   else g = grad_logical (logical layout = padded prefix; W5 pad rows 0).
@@ -457,7 +457,11 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
 //   apply: Adam (R11) + EMA (Eq. 2, R12) on g * inv_n, writing
 //   the fp32 state and both fp16 operand images.
 constexpr int kMaxDpTiles = 128;  // tiles per step in the fused peer all-reduce path
-constexpr int kAdamThreads = 256;  // 8 warps: 32 float4 elements (128 parameters) per block
+#ifndef NRC_ADAM_WARPS
+#define NRC_ADAM_WARPS 8
+#endif
+constexpr int kAdamWarps = NRC_ADAM_WARPS;     // warp w sums partials p = w mod kAdamWarps
+constexpr int kAdamThreads = 32 * kAdamWarps;  // 32 float4 elements (128 parameters) per block
 // a peer's (or our own) partial, read at system scope, not cached on this SM
 __device__ __forceinline__ float ld_sys_f32(const float* p) {
     float v;
@@ -530,9 +534,12 @@ struct AdamWArgs {
 };
 
 template <int W>
-__global__ void __launch_bounds__(kAdamThreads, 3) nrc_adam_w_kernel(AdamWArgs a) {
+#ifndef NRC_ADAM_MINB
+#define NRC_ADAM_MINB 1
+#endif
+__global__ void __launch_bounds__(kAdamThreads, NRC_ADAM_MINB) nrc_adam_w_kernel(AdamWArgs a) {
     const NetRt<W> D(a.nh);  // padded(nh) is a multiple of 128 for every width and depth
-    __shared__ float4 sred[8][32];
+    __shared__ float4 sred[kAdamWarps][32];
     const int lane = int(threadIdx.x & 31), wp = int(threadIdx.x >> 5);
     const int e = int(blockIdx.x) * 32 + lane;  // float4 element of the chunk-major layout
     const int k = 4 * e;
@@ -547,24 +554,25 @@ __global__ void __launch_bounds__(kAdamThreads, 3) nrc_adam_w_kernel(AdamWArgs a
     const int c4 = local / R, o = local - c4 * R;
     const int j0 = D.pad_off(i) + o * C + 4 * c4;  // row-major padded index of the 4 parameters
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    // warp 0's optimiser state, loaded under the partial loads (one L2 round trip)
-    float4 m = g, v = g, w = g, em = g;
-    if (wp == 0 && a.apply) {
-        m = ld_cg_v4(a.m + j0);
-        v = ld_cg_v4(a.v + j0);
-        w = ld_cg_v4(a.w + j0);
-        em = ld_cg_v4(a.ema + j0);
-    }
-    if (a.tile_part != nullptr || a.partials != nullptr) {
+    // the optimiser state (m, v, w, W-bar), one vector per warp 1..4, loaded
+    // under the partial loads (one L2 round trip) and handed to warp 0 through
+    // shared memory (4 registers per thread instead of 16: two optimiser
+    // blocks fit on an SM beside a partials CTA)
+    static_assert(kAdamWarps >= 5, "warps 1..4 load the optimiser state");
+    __shared__ float4 sstate[4][32];
+    float4 st = g;
+    if (a.apply && wp >= 1 && wp <= 4) st = ld_cg_v4((wp == 1 ? a.m : wp == 2 ? a.v : wp == 3 ? a.w : a.ema) + j0);
+    const bool from_partials = a.tile_part != nullptr || a.partials != nullptr;
+    if (from_partials) {
         float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
         const size_t stride = size_t(D.padded()) / 4;
         const float4* src = reinterpret_cast<const float4*>(a.partials) + e;
 #pragma unroll 1
-        for (int p0 = wp; p0 < a.np; p0 += 8 * 8) {
+        for (int p0 = wp; p0 < a.np; p0 += kAdamWarps * 8) {
             float4 x[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int p = p0 + 8 * u;
+                const int p = p0 + kAdamWarps * u;
                 x[u] = p >= a.np ? make_float4(0.f, 0.f, 0.f, 0.f)
                        : a.tile_part != nullptr ? ld_sys_v4(a.tile_part[p] + k)  // fused all-reduce: NVLink loads for peers
                                                 : __ldcg(src + size_t(p) * stride);
@@ -573,12 +581,6 @@ __global__ void __launch_bounds__(kAdamThreads, 3) nrc_adam_w_kernel(AdamWArgs a
             for (int u = 0; u < 8; ++u) s = f4_add(s, x[u]);
         }
         sred[wp][lane] = s;
-        __syncthreads();
-        if (trc) a.dbg[4084 + (blockIdx.x != 0)] = global_ns();
-        if (wp == 0) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) g = f4_add(g, sred[q][lane]);
-        }
     } else if (wp == 0 && a.grad_mc != nullptr) {
         // 4 consecutive logical entries (j0 % 4 == 0; W5's pad rows are beyond logical)
         if (j0 < D.logical()) g = multimem_ld_reduce_v4(a.grad_mc + j0);
@@ -588,7 +590,15 @@ __global__ void __launch_bounds__(kAdamThreads, 3) nrc_adam_w_kernel(AdamWArgs a
         for (int q = 0; q < 4; ++q) gg[q] = j0 + q < D.logical() ? a.grad_logical[j0 + q] : 0.0f;
         g = make_float4(gg[0], gg[1], gg[2], gg[3]);
     }
+    if (wp >= 1 && wp <= 4) sstate[wp - 1][lane] = st;
+    __syncthreads();
+    if (trc) a.dbg[4084 + (blockIdx.x != 0)] = global_ns();
+    if (wp == 0 && from_partials) {
+#pragma unroll
+        for (int q = 0; q < kAdamWarps; ++q) g = f4_add(g, sred[q][lane]);
+    }
     if (wp != 0) return;
+    const float4 m = sstate[0][lane], v = sstate[1][lane], w = sstate[2][lane], em = sstate[3][lane];
     if (blockIdx.x == 0 && a.loss_out != nullptr) {
         float s = 0.0f;
         if (a.grad_mc != nullptr) {

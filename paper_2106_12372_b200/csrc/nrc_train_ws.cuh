@@ -14,7 +14,12 @@
 //  * every layer has its own TMEM accumulator G_j (64 + 64 (nh + 1) <= 512
 //    columns) and four FLUSH warps (4..7, one per TMEM lane quadrant) drain
 //    G_j into the CTA's fp32 partial once bar_w[j] has completed -- the rows
-//    never touch the gradient accumulators.
+//    never touch the gradient accumulators;
+//  * a dedicated ISSUER warp (8) issues every MMA chain: tcgen05.mma issue
+//    blocks the issuing thread until the tensor pipe takes the instructions
+//    (a round's 12 MMAs hold it for most of the round), so the row warps only
+//    hand off (bar.arrive on named barrier 3; the issuer bar.syncs) and never
+//    stall behind the pipe.
 // One 128-row tile per CTA (batches of up to 128 x SMs rows, e.g. the
 // paper's 16,384); larger batches use nrc_train_w_kernel.
 #pragma once
@@ -26,7 +31,7 @@ template <int W>
 struct TrainWs {
     static_assert(W == 32 || W == 64, "the split schedule keeps one 64-column TMEM accumulator per layer");
     static constexpr int kMaxNh = 6;                 // 64 + 64 (nh + 1) <= 512 TMEM columns
-    static constexpr int kThreads = 256;             // 4 row warps + 4 flush warps
+    static constexpr int kThreads = 288;             // 4 row warps + 4 flush warps + the MMA issuer warp
     __host__ __device__ static constexpr int w_bytes(int nh) { return (NetRt<W>(nh).img() + 1023) / 1024 * 1024; }
     __host__ __device__ static constexpr int stash_bytes(int nh) { return kTileBytes + nh * kTileBytes; }
     // image + stash h0..h_nh + 2 g tiles + the dL/dy tile + barriers
@@ -100,63 +105,6 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
     auto wl = [&](int L) -> uint32_t { return sW_a + uint32_t(D.img_off(L)); };
     const uint32_t tile = blockIdx.x;  // grid = the batch's tiles
 
-    if (warp >= 4) {
-        // ------------------------------------------------ flush warps
-        // G_j (M = 64: out-neuron o = 16 q + lane in lanes 0..15 of quadrant q)
-        // -> this CTA's partial (chunk-major, part_index), undoing the tile's
-        // power-of-two dL/dy scale (exact in fp32); layers in the order their
-        // wgrads finish.  The partial belongs to the previous kernel until it
-        // has completed.
-        pdl_wait();
-        const uint32_t q = warp - 4u;
-        float* part = a.partials + size_t(blockIdx.x) * D.padded();
-        mbar_wait(scale_bar, 0);
-        const float inv_s = *inv_s_sh;
-        for (int j = nh; j >= 0; --j) {
-            mbar_wait(&bar_w[j], 0);
-            tc_fence_after();
-            const int o = int(q) * 16 + int(lane);
-            const bool valid = lane < 16 && o < D.rows(j);
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                if (32 * p >= D.cols(j)) break;
-                uint32_t v[32];
-                tmem_ld32(t_g(j) + lane_off + 32u * p, v);
-                if (valid) {
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        float4* dst = reinterpret_cast<float4*>(part + part_index(D, j, o, 32 * p + 4 * c));
-                        *dst = make_float4(__uint_as_float(v[4 * c]) * inv_s, __uint_as_float(v[4 * c + 1]) * inv_s,
-                                           __uint_as_float(v[4 * c + 2]) * inv_s, __uint_as_float(v[4 * c + 3]) * inv_s);
-                    }
-                }
-            }
-        }
-        tc_fence_before();
-        __syncthreads();  // (pairs with the rows' final barrier) before the TMEM is released
-        return;
-    }
-
-    // ------------------------------------------------ row warps (warp 0 issues)
-    uint32_t phase = 0, d_phase = 0;
-    auto copy = [&](uint32_t off, uint32_t bytes, uint64_t* bar) {
-        mbar_arrive_expect_tx(bar, bytes);
-        for (uint32_t o = 0; o < bytes; o += 8192u) {
-            const uint32_t b = bytes - o < 8192u ? bytes - o : 8192u;
-            bulk_g2s(smem + off + o, a.wimg + off + o, b, bar);
-        }
-    };
-    auto mma_wait = [&]() {
-        mbar_wait(mma_bar, phase);
-        phase ^= 1;
-        tc_fence_after();
-    };
-    auto sync_rows = [&]() {
-        tc_fence_before();
-        fence_async_smem();
-        named_bar_sync(1, 128);
-        tc_fence_after();
-    };
     auto issue_fwd = [&](int L) {
         const uint32_t idesc = warp_uniform(make_idesc(128, D.rows(L), 0, 0));
         const uint64_t a0 = warp_uniform(desc_kmajor(slot(L), 0));
@@ -203,161 +151,237 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
         }
         __syncwarp();
     };
-    // g_j = delta_j * 1[h_j > 0] -> gbuf[j & 1] (ReLU'(0) = 0, R17)
-    auto mask_epilogue = [&](int j) {
-#pragma unroll
-        for (int p = 0; p < W / 32; ++p) {
-            uint32_t v[32];
-            tmem_ld32(t_acc + lane_off + 32u * p, v);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t off = swz(r, uint32_t(p * 4 + q));
-                const uint4 hv = ld_shared_v4(slot(j) + off);
-                const float* f = reinterpret_cast<const float*>(v) + 8 * q;
-                st_shared_v4(gbuf(j) + off, pack_h2(f[0], f[1]) & relu_mask(hv.x), pack_h2(f[2], f[3]) & relu_mask(hv.y),
-                             pack_h2(f[4], f[5]) & relu_mask(hv.z), pack_h2(f[6], f[7]) & relu_mask(hv.w));
-            }
-        }
+    auto issuer_sync = [&]() {  // the rows' hand-off (their bar.arrive), then the MMAs may read
+        named_bar_sync(3, 160);
+        tc_fence_after();
     };
 
-    float loss_sum = 0.0f;
-    uint32_t bad = 0, deg = 0;
-    {
-        const uint32_t row = tile * kTile + r;
-        const bool valid = row < a.n;
-        float rec[16], tg[3];
-        train_gather_row(a, row, rec, tg);
-        {
-            uint32_t h[32];
-            const uint32_t dg = encode_record<EXACT>(rec, a.ep, h);
-            deg += valid ? dg : 0u;
-            store_row_swz(slot(0), r, h);
-        }
-        NRC_WTRC(1);
-        pdl_wait();  // the weights belong to the previous kernel until it completes
-        NRC_WTRC(2);
-        if (tid == 0) {
-            copy(0u, uint32_t(D.img_off(1)), wbar);
-            copy(uint32_t(D.img_off(1)), uint32_t(D.img() - D.img_off(1)), wbar1);
-        }
-        sync_rows();
-        // ---------------- forward: h_{L+1} = relu(W_L h_L), y = W_nh h_nh
+    if (warp == 8) {
+        // ------------------------------------------------ MMA issuer warp
+        issuer_sync();  // h0 encoded
+        mbar_wait(wbar, 0);
+        issue_fwd(0);
 #pragma unroll 1
-        for (int L = 0; L <= nh; ++L) {
-            if (warp == 0) {
-                if (L == 0) mbar_wait(wbar, 0);
-                if (L == 1) mbar_wait(wbar1, 0);
-                issue_fwd(L);
-            }
-            mma_wait();
-            if (nh == 5) NRC_WTRC(8 + L);
-            if (L == nh) break;
+        for (int L = 1; L <= nh; ++L) {
+            issuer_sync();  // h_L written
+            if (L == 1) mbar_wait(wbar1, 0);
+            issue_fwd(L);
+        }
+        issuer_sync();  // dL/dy written
+#pragma unroll 1
+        for (int j = nh; j >= 1; --j) {
+            issue_bwd(j);
+            issuer_sync();  // g_j written
+        }
+        issue_bwd(0);
+    } else if (warp >= 4) {
+        // ------------------------------------------------ flush warps
+        // G_j (M = 64: out-neuron o = 16 q + lane in lanes 0..15 of quadrant q)
+        // -> this CTA's partial (chunk-major, part_index), undoing the tile's
+        // power-of-two dL/dy scale (exact in fp32); layers in the order their
+        // wgrads finish.  The partial belongs to the previous kernel until it
+        // has completed.
+        pdl_wait();
+        const uint32_t q = warp - 4u;
+        float* part = a.partials + size_t(blockIdx.x) * D.padded();
+        mbar_wait(scale_bar, 0);
+        const float inv_s = *inv_s_sh;
+        for (int j = nh; j >= 0; --j) {
+            mbar_wait(&bar_w[j], 0);
+            tc_fence_after();
+#ifdef NRC_TRACE_FLUSH
+            // diagnostics: global time at which wgrad_j completed (flush warp 4)
+            if (a.dbg != nullptr && q == 0 && lane == 0 && blockIdx.x < 127)
+                a.dbg[16384 + 32 * blockIdx.x + j] = global_ns();
+#endif
+            const int o = int(q) * 16 + int(lane);
+            const bool valid = lane < 16 && o < D.rows(j);
 #pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (32 * p >= D.cols(j)) break;
+                uint32_t v[32];
+                tmem_ld32(t_g(j) + lane_off + 32u * p, v);
+                if (valid) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        float4* dst = reinterpret_cast<float4*>(part + part_index(D, j, o, 32 * p + 4 * c));
+                        *dst = make_float4(__uint_as_float(v[4 * c]) * inv_s, __uint_as_float(v[4 * c + 1]) * inv_s,
+                                           __uint_as_float(v[4 * c + 2]) * inv_s, __uint_as_float(v[4 * c + 3]) * inv_s);
+                    }
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ row warps
+        uint32_t phase = 0, d_phase = 0;
+        auto copy = [&](uint32_t off, uint32_t bytes, uint64_t* bar) {
+            mbar_arrive_expect_tx(bar, bytes);
+            for (uint32_t o = 0; o < bytes; o += 8192u) {
+                const uint32_t b = bytes - o < 8192u ? bytes - o : 8192u;
+                bulk_g2s(smem + off + o, a.wimg + off + o, b, bar);
+            }
+        };
+        auto mma_wait = [&]() {
+            mbar_wait(mma_bar, phase);
+            phase ^= 1;
+            tc_fence_after();
+        };
+        // this thread's smem / TMEM work for the next MMA chain is done
+        auto hand_off = [&]() {
+            tc_fence_before();
+            fence_async_smem();
+            asm volatile("bar.arrive 3, 160;" ::: "memory");
+        };
+        // g_j = delta_j * 1[h_j > 0] -> gbuf[j & 1] (ReLU'(0) = 0, R17)
+        auto mask_epilogue = [&](int j) {
+    #pragma unroll
             for (int p = 0; p < W / 32; ++p) {
                 uint32_t v[32];
                 tmem_ld32(t_acc + lane_off + 32u * p, v);
-#pragma unroll
+    #pragma unroll
                 for (int q = 0; q < 4; ++q) {
+                    const uint32_t off = swz(r, uint32_t(p * 4 + q));
+                    const uint4 hv = ld_shared_v4(slot(j) + off);
                     const float* f = reinterpret_cast<const float*>(v) + 8 * q;
-                    st_shared_v4(slot(L + 1) + swz(r, uint32_t(p * 4 + q)), pack_h2_relu(f[0], f[1]),
-                                 pack_h2_relu(f[2], f[3]), pack_h2_relu(f[4], f[5]), pack_h2_relu(f[6], f[7]));
+                    st_shared_v4(gbuf(j) + off, pack_h2(f[0], f[1]) & relu_mask(hv.x), pack_h2(f[2], f[3]) & relu_mask(hv.y),
+                                 pack_h2(f[4], f[5]) & relu_mask(hv.z), pack_h2(f[6], f[7]) & relu_mask(hv.w));
                 }
             }
-            sync_rows();
-        }
-        // ---------------- relative L2 loss, Eq.(5) (R8-R10, R13, R25)
+        };
+
+        float loss_sum = 0.0f;
+        uint32_t bad = 0, deg = 0;
         {
-            uint32_t v[4];
-            tmem_ld4(t_acc + lane_off, v);
-            const bool use = valid && isfinite(tg[0]) && isfinite(tg[1]) && isfinite(tg[2]);
-            if (valid && !use) ++bad;
-            float yh[3], f[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                f[c] = (a.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
-                yh[c] = __uint_as_float(v[c]) * f[c];
-            }
-            const float lam = 0.2126f * yh[0] + 0.7152f * yh[1] + 0.0722f * yh[2];
-            const float den = lam * lam + a.loss_eps;
-            const float inv3den = 1.0f / (3.0f * den);
-            float gy[3], l = 0.0f;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const float d = yh[c] - tg[c];
-                l += d * d;
-                gy[c] = use ? 2.0f * d * f[c] * inv3den : 0.0f;
-            }
-            if (use) loss_sum += l * inv3den;
-            if (a.pred != nullptr && valid) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) a.pred[size_t(row) * 3 + c] = yh[c];
-            }
-            // per-tile power-of-two scale of dL/dy (R13, R25): the tile's largest
-            // |dL/dy| maps into [2^7, 2^8); undone in fp32 by the flush warps
-            const uint32_t mx = __reduce_max_sync(
-                0xffffffffu, max(max(__float_as_uint(fabsf(gy[0])), __float_as_uint(fabsf(gy[1]))),
-                                 __float_as_uint(fabsf(gy[2]))));
-            if (lane == 0) gmax[warp] = mx;
-            named_bar_sync(2, 128);
+            const uint32_t row = tile * kTile + r;
+            const bool valid = row < a.n;
+            float rec[16], tg[3];
+            train_gather_row(a, row, rec, tg);
             {
-                const uint32_t tm = max(max(gmax[0], gmax[1]), max(gmax[2], gmax[3]));
-                const int ex = int(tm >> 23);
-                const int ks = min(max(134 - ex, -120), 120);
-                if (tid == 0) {
-                    *inv_s_sh = __uint_as_float(uint32_t(127 - ks) << 23);
-                    mbar_arrive(scale_bar);
-                }
-                const float sc = __uint_as_float(uint32_t(127 + ks) << 23);
-#pragma unroll
-                for (int c = 0; c < 3; ++c) gy[c] *= sc;
+                uint32_t h[32];
+                const uint32_t dg = encode_record<EXACT>(rec, a.ep, h);
+                deg += valid ? dg : 0u;
+                store_row_swz(slot(0), r, h);
             }
-            st_shared_v4(sG6_a + swz(r, 0), pack_h2(gy[0], gy[1]), pack_h2(gy[2], 0.0f), 0u, 0u);
+            NRC_WTRC(1);
+            pdl_wait();  // the weights belong to the previous kernel until it completes
+            NRC_WTRC(2);
+            if (tid == 0) {
+                copy(0u, uint32_t(D.img_off(1)), wbar);
+                copy(uint32_t(D.img_off(1)), uint32_t(D.img() - D.img_off(1)), wbar1);
+            }
+            hand_off();
+            // ---------------- forward: h_{L+1} = relu(W_L h_L), y = W_nh h_nh
+    #pragma unroll 1
+            for (int L = 0; L <= nh; ++L) {
+                mma_wait();
+                if (nh == 5) NRC_WTRC(8 + L);
+                if (L == nh) break;
+    #pragma unroll
+                for (int p = 0; p < W / 32; ++p) {
+                    uint32_t v[32];
+                    tmem_ld32(t_acc + lane_off + 32u * p, v);
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float* f = reinterpret_cast<const float*>(v) + 8 * q;
+                        st_shared_v4(slot(L + 1) + swz(r, uint32_t(p * 4 + q)), pack_h2_relu(f[0], f[1]),
+                                     pack_h2_relu(f[2], f[3]), pack_h2_relu(f[4], f[5]), pack_h2_relu(f[6], f[7]));
+                    }
+                }
+                hand_off();
+            }
+            // ---------------- relative L2 loss, Eq.(5) (R8-R10, R13, R25)
+            {
+                uint32_t v[4];
+                tmem_ld4(t_acc + lane_off, v);
+                const bool use = valid && isfinite(tg[0]) && isfinite(tg[1]) && isfinite(tg[2]);
+                if (valid && !use) ++bad;
+                float yh[3], f[3];
+    #pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    f[c] = (a.flags & 1u) ? rec[10 + c] + rec[13 + c] : 1.0f;
+                    yh[c] = __uint_as_float(v[c]) * f[c];
+                }
+                const float lam = 0.2126f * yh[0] + 0.7152f * yh[1] + 0.0722f * yh[2];
+                const float den = lam * lam + a.loss_eps;
+                const float inv3den = 1.0f / (3.0f * den);
+                float gy[3], l = 0.0f;
+    #pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float d = yh[c] - tg[c];
+                    l += d * d;
+                    gy[c] = use ? 2.0f * d * f[c] * inv3den : 0.0f;
+                }
+                if (use) loss_sum += l * inv3den;
+                if (a.pred != nullptr && valid) {
+    #pragma unroll
+                    for (int c = 0; c < 3; ++c) a.pred[size_t(row) * 3 + c] = yh[c];
+                }
+                // per-tile power-of-two scale of dL/dy (R13, R25): the tile's largest
+                // |dL/dy| maps into [2^7, 2^8); undone in fp32 by the flush warps
+                const uint32_t mx = __reduce_max_sync(
+                    0xffffffffu, max(max(__float_as_uint(fabsf(gy[0])), __float_as_uint(fabsf(gy[1]))),
+                                     __float_as_uint(fabsf(gy[2]))));
+                if (lane == 0) gmax[warp] = mx;
+                named_bar_sync(2, 128);
+                {
+                    const uint32_t tm = max(max(gmax[0], gmax[1]), max(gmax[2], gmax[3]));
+                    const int ex = int(tm >> 23);
+                    const int ks = min(max(134 - ex, -120), 120);
+                    if (tid == 0) {
+                        *inv_s_sh = __uint_as_float(uint32_t(127 - ks) << 23);
+                        mbar_arrive(scale_bar);
+                    }
+                    const float sc = __uint_as_float(uint32_t(127 + ks) << 23);
+    #pragma unroll
+                    for (int c = 0; c < 3; ++c) gy[c] *= sc;
+                }
+                st_shared_v4(sG6_a + swz(r, 0), pack_h2(gy[0], gy[1]), pack_h2(gy[2], 0.0f), 0u, 0u);
+            }
+            hand_off();
+            NRC_WTRC(3);
+            // ---------------- backward
+    #pragma unroll 1
+            for (int j = nh; j >= 1; --j) {
+                if (nh == 5) NRC_WTRC(14 + 2 * (5 - j));
+                mbar_wait(bar_d, d_phase);
+                d_phase ^= 1;
+                tc_fence_after();
+                if (nh == 5) NRC_WTRC(15 + 2 * (5 - j));
+                mask_epilogue(j);
+                if (nh == 5 && j >= 2) NRC_WTRC(24 + (5 - j));
+                hand_off();  // (wgrad_0 = g_1^T h_0 follows round 1 on the issuer: no gradient w.r.t. the encoding)
+                if (nh == 5 && j >= 2) NRC_WTRC(28 + (5 - j));
+            }
+            NRC_WTRC(4);
+            NRC_WTRC(5);
         }
-        sync_rows();
-        NRC_WTRC(3);
-        // ---------------- backward
-#pragma unroll 1
-        for (int j = nh; j >= 1; --j) {
-            if (warp == 0) issue_bwd(j);
-            if (nh == 5) NRC_WTRC(14 + 2 * (5 - j));
-            mbar_wait(bar_d, d_phase);
-            d_phase ^= 1;
-            tc_fence_after();
-            if (nh == 5) NRC_WTRC(15 + 2 * (5 - j));
-            mask_epilogue(j);
-            if (nh == 5 && j >= 2) NRC_WTRC(24 + (5 - j));
-            sync_rows();
-            if (nh == 5 && j >= 2) NRC_WTRC(28 + (5 - j));
+        // ---------------- this CTA's loss sum (fixed order over the 4 row warps)
+    #pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            loss_sum += __shfl_xor_sync(0xffffffffu, loss_sum, off);
+            bad += __shfl_xor_sync(0xffffffffu, bad, off);
         }
-        NRC_WTRC(4);
-        if (warp == 0) issue_bwd(0);  // G_0 = g_1^T h_0 (no gradient w.r.t. the encoding)
-        NRC_WTRC(5);
+        if (lane == 0) {
+            red[warp] = loss_sum;
+            reinterpret_cast<uint32_t*>(red + 4)[warp] = bad;
+        }
+        {
+            const uint32_t sdeg = __reduce_add_sync(0xffffffffu, deg);
+            if (lane == 0 && sdeg != 0) atomicAdd(deg_scratch, sdeg);
+        }
+        named_bar_sync(1, 128);
+        if (tid == 0) {
+            a.loss_part[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+            const uint32_t* b = reinterpret_cast<const uint32_t*>(red + 4);
+            const uint32_t nb = b[0] + b[1] + b[2] + b[3];
+            if (nb) atomicAdd(a.bad_targets, (unsigned long long)nb);
+            if (*deg_scratch != 0 && a.degenerate != nullptr) atomicAdd(a.degenerate, (unsigned long long)*deg_scratch);
+        }
+        NRC_WTRC(6);
     }
-    // ---------------- this CTA's loss sum (fixed order over the 4 row warps)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        loss_sum += __shfl_xor_sync(0xffffffffu, loss_sum, off);
-        bad += __shfl_xor_sync(0xffffffffu, bad, off);
-    }
-    if (lane == 0) {
-        red[warp] = loss_sum;
-        reinterpret_cast<uint32_t*>(red + 4)[warp] = bad;
-    }
-    {
-        const uint32_t sdeg = __reduce_add_sync(0xffffffffu, deg);
-        if (lane == 0 && sdeg != 0) atomicAdd(deg_scratch, sdeg);
-    }
-    named_bar_sync(1, 128);
-    if (tid == 0) {
-        a.loss_part[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
-        const uint32_t* b = reinterpret_cast<const uint32_t*>(red + 4);
-        const uint32_t nb = b[0] + b[1] + b[2] + b[3];
-        if (nb) atomicAdd(a.bad_targets, (unsigned long long)nb);
-        if (*deg_scratch != 0 && a.degenerate != nullptr) atomicAdd(a.degenerate, (unsigned long long)*deg_scratch);
-    }
-    NRC_WTRC(6);
+    // both roles meet here: the flush warps are done with the TMEM
     tc_fence_before();
-    __syncthreads();  // the flush warps are done with the TMEM
+    __syncthreads();
     tc_fence_after();
     if (warp == 0) tmem_dealloc(tmem_base, 512);
 }

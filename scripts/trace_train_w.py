@@ -23,13 +23,14 @@ tr, tg = torch.from_numpy(tr).cuda(), torch.from_numpy(tg).cuda()
 c = nrc.RadianceCache(nrc.Config(hidden_width=hw))
 for _ in range(5):
     c.train_frame(tr, tg, 4, 16384, 1)
-buf = torch.zeros(4 * 4096, dtype=torch.int64, device="cuda")
+buf = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
 c.L.nrc_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 c.L.nrc_debug_set_trace(c.h, ctypes.c_void_p(buf.data_ptr()))
 torch.cuda.synchronize()
 c.train_frame(tr, tg, 4, 16384, 1)
 torch.cuda.synchronize()
-d = buf.cpu().numpy().reshape(4, 4096)
+dall = buf.cpu().numpy()
+d = dall[:4 * 4096].reshape(4, 4096)
 step0 = c.stats()["step"] - 4
 t0 = None
 names = {0: "start", 1: "encoded", 2: "after wait", 8: "fwd L0 mma", 9: "fwd L1 mma", 10: "fwd L2 mma",
@@ -56,6 +57,11 @@ for k in range(4):
     for i, nm in names.items():
         col = g[:, i] - t0
         print(f"  {nm:14s} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}")
+    fl = dall[16384 + 4096 * ((step0 + k) % 4):16384 + 4096 * ((step0 + k) % 4) + 32 * 127].reshape(127, 32)
+    if fl[:, :8].any():  # NRC_TRACE_FLUSH builds: wgrad_j completion seen by the flush warps
+        for j in range(5, -1, -1):
+            col = fl[:, j] - t0
+            print(f"  wgrad {j} done     min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}")
     print(f"  adam blk0 {blk[4088] - t0:7d} -> sum {blk[4084] - t0:7d} -> {blk[4089] - t0:7d}   "
           f"last blk {blk[4090] - t0:7d} -> sum {blk[4085] - t0:7d} -> {blk[4091] - t0:7d}")
 c.L.nrc_debug_set_trace(c.h, None)
