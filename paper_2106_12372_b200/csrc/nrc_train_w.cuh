@@ -457,10 +457,13 @@ __global__ void __launch_bounds__(128, 1) nrc_train_w_kernel(TrainArgs a) {
 //   apply: Adam (R11) + EMA (Eq. 2, R12) on g * inv_n, writing
 //   the fp32 state and both fp16 operand images.
 constexpr int kMaxDpTiles = 128;  // tiles per step in the fused peer all-reduce path
-#ifndef NRC_ADAM_WARPS
-#define NRC_ADAM_WARPS 8
-#endif
-constexpr int kAdamWarps = NRC_ADAM_WARPS;     // warp w sums partials p = w mod kAdamWarps
+// 8 warps, 8 partial loads in flight per thread, ~84 registers: measured
+// best against 16 warps or 16 loads in flight (one load round instead of two,
+// but blocks that no longer fit beside the next step's partials CTAs) and
+// against a 64-register bound that keeps two blocks beside a partials CTA
+// (the next step's gather + encode then slows the reduction): 64.5 vs 72.7 /
+// 72.7 / 68.6 us per 4-step frame
+constexpr int kAdamWarps = 8;                  // warp w sums partials p = w mod kAdamWarps
 constexpr int kAdamThreads = 32 * kAdamWarps;  // 32 float4 elements (128 parameters) per block
 // a peer's (or our own) partial, read at system scope, not cached on this SM
 __device__ __forceinline__ float ld_sys_f32(const float* p) {
@@ -534,10 +537,7 @@ struct AdamWArgs {
 };
 
 template <int W>
-#ifndef NRC_ADAM_MINB
-#define NRC_ADAM_MINB 1
-#endif
-__global__ void __launch_bounds__(kAdamThreads, NRC_ADAM_MINB) nrc_adam_w_kernel(AdamWArgs a) {
+__global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a) {
     const NetRt<W> D(a.nh);  // padded(nh) is a multiple of 128 for every width and depth
     __shared__ float4 sred[kAdamWarps][32];
     const int lane = int(threadIdx.x & 31), wp = int(threadIdx.x >> 5);
@@ -567,18 +567,19 @@ __global__ void __launch_bounds__(kAdamThreads, NRC_ADAM_MINB) nrc_adam_w_kernel
         float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
         const size_t stride = size_t(D.padded()) / 4;
         const float4* src = reinterpret_cast<const float4*>(a.partials) + e;
+        constexpr int kIn = 8;  // partial loads in flight per thread
 #pragma unroll 1
-        for (int p0 = wp; p0 < a.np; p0 += kAdamWarps * 8) {
-            float4 x[8];
+        for (int p0 = wp; p0 < a.np; p0 += kAdamWarps * kIn) {
+            float4 x[kIn];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kIn; ++u) {
                 const int p = p0 + kAdamWarps * u;
                 x[u] = p >= a.np ? make_float4(0.f, 0.f, 0.f, 0.f)
                        : a.tile_part != nullptr ? ld_sys_v4(a.tile_part[p] + k)  // fused all-reduce: NVLink loads for peers
                                                 : __ldcg(src + size_t(p) * stride);
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) s = f4_add(s, x[u]);
+            for (int u = 0; u < kIn; ++u) s = f4_add(s, x[u]);
         }
         sred[wp][lane] = s;
     } else if (wp == 0 && a.grad_mc != nullptr) {
