@@ -479,6 +479,25 @@ __device__ __forceinline__ float4 ld_sys_v4(const float* p) {
                  : "memory");
     return v;
 }
+// Adam (R11) + EMA (Eq. 2, R12) of one parameter on the batch-mean
+// gradient g; shared by the optimiser kernel and the fused optimiser stage
+// so that both compile to the same arithmetic.  Returns 1 if g was
+// non-finite (zeroed and counted).
+struct AdamCoef {
+    float lr, b1, b2, eps, inv_bc1, inv_bc2, ema_c1, ema_c2;
+};
+__device__ __forceinline__ uint32_t adam_ema(float g, const AdamCoef& k, float& m, float& v, float& w, float& e) {
+    uint32_t bad = 0;
+    if (!isfinite(g)) {
+        g = 0.0f;
+        bad = 1;
+    }
+    m = k.b1 * m + (1.0f - k.b1) * g;
+    v = k.b2 * v + (1.0f - k.b2) * g * g;
+    w = w - k.lr * (m * k.inv_bc1) / (sqrtf(v * k.inv_bc2) + k.eps);
+    e = k.ema_c1 * w + k.ema_c2 * e;
+    return bad;
+}
 // L2 load kept in program order (not sunk below the partial loads)
 __device__ __forceinline__ float4 ld_cg_v4(const float* p) {
     float4 v;
@@ -621,19 +640,10 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
     if (!a.apply) return;
     float mq[4] = {m.x, m.y, m.z, m.w}, vq[4] = {v.x, v.y, v.z, v.w}, wq[4] = {w.x, w.y, w.z, w.w},
           eq[4] = {em.x, em.y, em.z, em.w};
+    const AdamCoef kc{a.lr, a.b1, a.b2, a.eps, a.inv_bc1, a.inv_bc2, a.ema_c1, a.ema_c2};
     uint32_t nbad = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        float gg = gq[q] * a.inv_n;
-        if (!isfinite(gg)) {  // non-finite gradient entries are zeroed and counted
-            gg = 0.0f;
-            ++nbad;
-        }
-        mq[q] = a.b1 * mq[q] + (1.0f - a.b1) * gg;
-        vq[q] = a.b2 * vq[q] + (1.0f - a.b2) * gg * gg;
-        wq[q] = wq[q] - a.lr * (mq[q] * a.inv_bc1) / (sqrtf(vq[q] * a.inv_bc2) + a.eps);
-        eq[q] = a.ema_c1 * wq[q] + a.ema_c2 * eq[q];
-    }
+    for (int q = 0; q < 4; ++q) nbad += adam_ema(gq[q] * a.inv_n, kc, mq[q], vq[q], wq[q], eq[q]);
     if (nbad) atomicAdd(a.bad_grads, (unsigned long long)nbad);
     *reinterpret_cast<float4*>(a.m + j0) = make_float4(mq[0], mq[1], mq[2], mq[3]);
     *reinterpret_cast<float4*>(a.v + j0) = make_float4(vq[0], vq[1], vq[2], vq[3]);
