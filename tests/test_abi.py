@@ -129,3 +129,19 @@ def test_state_bytes_depth_and_width(libnrc, hw, nh, ok):
     if nh > 1:
         c.n_hidden_layers = nh - 1
         assert libnrc.nrc_state_bytes(ctypes.byref(c)) < nb
+
+
+def test_nvls_entry_points_validate_arguments(libnrc):
+    """nrc_train_apply_multimem / nrc_peer_barrier / nrc_multicast_alloc reject
+    bad arguments without touching a GPU, and the multimem.ld_reduce load of
+    the NVLS optimiser is in the binary (LDGMC)."""
+    from paper_2106_12372_b200 import _lib
+    STATE, INVALID = 6, 1
+    assert libnrc.nrc_train_apply_multimem(None, None, 1, None, None) == STATE
+    assert libnrc.nrc_peer_barrier(None, None, 0, 1, None) == STATE
+    uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+    assert libnrc.nrc_multicast_alloc(0, 0, ctypes.byref(uc), ctypes.byref(mc)) == INVALID
+    assert libnrc.nrc_multicast_alloc(0, 1024, None, ctypes.byref(mc)) == INVALID
+    assert libnrc.nrc_multicast_free(None) == INVALID
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.lib_path()], capture_output=True, text=True).stdout
+    assert "LDGMC" in sass  # multimem.ld_reduce (NVLS all-reduce read by the optimiser)
