@@ -148,11 +148,25 @@ struct nrc_handle {
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
     bool train_legacy = false;    // NRC_TRAIN_LEGACY=1: nrc_train_w_kernel for one-tile batches too
+    // nrc_train_frame as one CUDA graph (2 s kernel nodes with programmatic
+    // edges), captured once per (rows per step, steps) and replayed with the
+    // per-call arguments; NRC_TRAIN_GRAPH=0 launches on the stream instead
+    bool train_graph = true;
+    struct TrainGraph {
+        uint32_t n = 0, nsteps = 0;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<cudaGraphNode_t> nodes;  // P_0, A_0, P_1, A_1, ...
+    } tgraph;
+    cudaStream_t capture = nullptr;
     int train_ctas = 0;           // cap on the train grid (0: one CTA per tile up to all SMs)
     // nrc_frame_host pipelining: host->device and device->host copy streams and events
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> events;
     ~nrc_handle() {
+        if (tgraph.exec) cudaGraphExecDestroy(tgraph.exec);
+        if (tgraph.graph) cudaGraphDestroy(tgraph.graph);
+        if (capture) cudaStreamDestroy(capture);
         for (cudaEvent_t e : events) cudaEventDestroy(e);
         if (copy_in) cudaStreamDestroy(copy_in);
         if (copy_out) cudaStreamDestroy(copy_out);
@@ -384,6 +398,7 @@ nrc_status nrc_init(const nrc_config* cfg, void* d_state, size_t state_bytes, nr
     if (const char* e = std::getenv("NRC_TRAIN_CTAS")) h->train_ctas = std::atoi(e);
     // diagnostics / A-B only: the single-schedule partials kernel for every batch
     if (const char* e = std::getenv("NRC_TRAIN_LEGACY")) h->train_legacy = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NRC_TRAIN_GRAPH")) h->train_graph = std::atoi(e) != 0;
     if ((s = cuda_check(h, kQuery64.set_smem(), "cudaFuncSetAttribute(query)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW32.set_smem(), "cudaFuncSetAttribute(query w32)")) != NRC_OK) return bail(s);
     if ((s = cuda_check(h, kQueryW128.set_smem(), "cudaFuncSetAttribute(query w128)")) != NRC_OK) return bail(s);
@@ -641,8 +656,11 @@ static nrc_status launch_adam_w(nrc_handle* h, const AdamWArgs& aa, cudaStream_t
 
 // nsteps optimisation steps of n rows each (step k gathers rows offset + k n
 // when gathering): per step the partials kernel, then reduce + Adam + EMA.
+static nrc_status train_steps_graph(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                                    const Gather& gth, float* d_losses, uint32_t nsteps, cudaStream_t st);
 static nrc_status train_steps(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
                               const Gather& gth, float* d_losses, uint32_t nsteps, cudaStream_t st) {
+    if (nsteps >= 2 && h->train_graph && !h->dbg) return train_steps_graph(h, d_rec, d_tgt, n, gth, d_losses, nsteps, st);
     uint32_t launches = 0;
     for (uint32_t k = 0; k < nsteps; ++k) {
         Gather g = gth;
@@ -665,6 +683,92 @@ static nrc_status train_steps(nrc_handle* h, const nrc_record* d_rec, const floa
     h->launches = launches;
     return NRC_OK;
 }
+// The same launches as one CUDA graph: the graph of (n, nsteps) is captured
+// once on a private stream (programmatic edges between the kernels, as on the
+// stream) and replayed with this call's kernel arguments
+// (cudaGraphExecKernelNodeSetParams); saves the per-launch gaps of the chain.
+static nrc_status train_steps_graph(nrc_handle* h, const nrc_record* d_rec, const float* d_tgt, uint32_t n,
+                                    const Gather& gth, float* d_losses, uint32_t nsteps, cudaStream_t st) {
+    const int grid = train_grid(h, n);
+    std::vector<TrainArgs> pa(nsteps);
+    std::vector<AdamWArgs> aa(nsteps);
+    for (uint32_t k = 0; k < nsteps; ++k) {
+        Gather g = gth;
+        g.offset = gth.offset + uint64_t(k) * n;
+        pa[k] = train_args(h, d_rec, d_tgt, n, g);
+        h->step += 1;
+        aa[k] = adam_w_args(h);
+        aa[k].partials = h->d_partials();
+        aa[k].np = grid;
+        aa[k].apply = 1;
+        aa[k].inv_n = float(1.0 / double(n));
+        aa[k].nloss = grid;
+        aa[k].loss_scale = aa[k].inv_n;
+        aa[k].loss_out = d_losses ? d_losses + k : nullptr;
+    }
+    auto& tg = h->tgraph;
+    if (tg.exec == nullptr || tg.n != n || tg.nsteps != nsteps) {
+        if (tg.exec) cudaGraphExecDestroy(tg.exec);
+        if (tg.graph) cudaGraphDestroy(tg.graph);
+        tg = nrc_handle::TrainGraph{};
+        if (!h->capture) NRC_CUDA(h, cudaStreamCreateWithFlags(&h->capture, cudaStreamNonBlocking));
+        NRC_CUDA(h, cudaStreamBeginCapture(h->capture, cudaStreamCaptureModeThreadLocal));
+        for (uint32_t k = 0; k < nsteps; ++k) {
+            cudaError_t e = launch_train_w_grid(h, pa[k], grid, h->capture);
+            if (e == cudaSuccess) {
+                const uint64_t saved = h->launches;
+                nrc_status st2 = launch_adam_w(h, aa[k], h->capture);
+                h->launches = uint32_t(saved);
+                if (st2 != NRC_OK) e = cudaErrorUnknown;
+            }
+            if (e != cudaSuccess) {
+                cudaGraph_t dead = nullptr;
+                cudaStreamEndCapture(h->capture, &dead);
+                if (dead) cudaGraphDestroy(dead);
+                return fail(h, NRC_ERR_CUDA, "nrc_train_frame: graph capture failed");
+            }
+        }
+        NRC_CUDA(h, cudaStreamEndCapture(h->capture, &tg.graph));
+        // the captured chain in launch order: from the root along its single
+        // dependent each time (the programmatic edges are graph edges too)
+        size_t count = 0;
+        NRC_CUDA(h, cudaGraphGetRootNodes(tg.graph, nullptr, &count));
+        if (count != 1) return fail(h, NRC_ERR_CUDA, "nrc_train_frame: unexpected graph shape");
+        cudaGraphNode_t node = nullptr;
+        NRC_CUDA(h, cudaGraphGetRootNodes(tg.graph, &node, &count));
+        while (node != nullptr) {
+            cudaGraphNodeType t;
+            NRC_CUDA(h, cudaGraphNodeGetType(node, &t));
+            if (t != cudaGraphNodeTypeKernel) return fail(h, NRC_ERR_CUDA, "nrc_train_frame: unexpected graph node");
+            tg.nodes.push_back(node);
+            size_t nd = 0;
+            NRC_CUDA(h, cudaGraphNodeGetDependentNodes_v2(node, nullptr, nullptr, &nd));
+            if (nd > 1) return fail(h, NRC_ERR_CUDA, "nrc_train_frame: unexpected graph shape");
+            cudaGraphNode_t next = nullptr;
+            cudaGraphEdgeData edge{};
+            if (nd == 1) NRC_CUDA(h, cudaGraphNodeGetDependentNodes_v2(node, &next, &edge, &nd));
+            node = next;
+        }
+        if (tg.nodes.size() != size_t(2) * nsteps)
+            return fail(h, NRC_ERR_CUDA, "nrc_train_frame: unexpected graph shape");
+        NRC_CUDA(h, cudaGraphInstantiate(&tg.exec, tg.graph, 0));
+        tg.n = n;
+        tg.nsteps = nsteps;
+    } else {
+        for (uint32_t i = 0; i < 2 * nsteps; ++i) {
+            cudaKernelNodeParams p{};
+            NRC_CUDA(h, cudaGraphKernelNodeGetParams(tg.nodes[i], &p));
+            void* args[1] = {(i & 1) ? static_cast<void*>(&aa[i / 2]) : static_cast<void*>(&pa[i / 2])};
+            p.kernelParams = args;
+            p.extra = nullptr;
+            NRC_CUDA(h, cudaGraphExecKernelNodeSetParams(tg.exec, tg.nodes[i], &p));
+        }
+    }
+    NRC_CUDA(h, cudaGraphLaunch(tg.exec, st));
+    h->launches = 2 * nsteps;
+    return NRC_OK;
+}
+
 // partials -> logical gradient sum + loss sum (multi-GPU backward)
 static nrc_status reduce_partials(nrc_handle* h, int np, float* d_grad, float* d_loss_sum, cudaStream_t st) {
     AdamWArgs aa = adam_w_args(h);
