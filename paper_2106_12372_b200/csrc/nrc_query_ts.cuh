@@ -125,13 +125,16 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     const uint32_t lane_off = (wq * 32u) << 16;
     const uint32_t t_d = tmem_base + uint32_t(W) * g;               // fp32 accumulator
     const uint32_t t_a = tmem_base + uint32_t(W * G) + kACols * g;  // fp16 A operand
+    const uint32_t t_dl = t_d + lane_off, t_al = t_a + lane_off;      // this warp's lane quadrant
     // called by the whole issuer warp (converged)
     auto issue_layer = [&](int L) {
-        const uint32_t wl = sW_a + uint32_t(D.img_off(L));
+        // the weight tile's address made warp-uniform first: the descriptor
+        // arithmetic then stays inside the issuer warp (not hoisted into all)
+        const uint32_t wl = warp_uniform(sW_a + uint32_t(D.img_off(L)));
         const uint32_t idesc = make_idesc(128, D.rows(L), 0, 0);
         const uint32_t d = warp_uniform(t_d), a = warp_uniform(t_a);
-        const uint64_t b0 = warp_uniform(desc_kmajor(wl, 0));
-        const uint64_t b1 = warp_uniform(desc_kmajor(wl + uint32_t(D.rows(L)) * 128u, 0));
+        const uint64_t b0 = desc_kmajor(wl, 0);
+        const uint64_t b1 = desc_kmajor(wl + uint32_t(D.rows(L)) * 128u, 0);
         tc_fence_after();
         if (elect_one()) {
             if (D.cols(L) == 32)
@@ -154,11 +157,11 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
 #pragma unroll
         for (int part = 0; part < W / 32; ++part) {
             uint32_t v[32];
-            tmem_ld32(t_d + lane_off + 32 * part, v);
+            tmem_ld32(t_dl + 32 * part, v);
             uint32_t hp[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q) hp[q] = pack_h2_relu(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
-            tmem_st16_nowait(t_a + lane_off + 16 * part, hp);
+            tmem_st16_nowait(t_al + 16 * part, hp);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
             uint32_t h[32];
             const uint32_t dg = encode_record<EXACT>(rec, args.ep, h);
             deg += valid ? dg : 0u;
-            tmem_st32(t_a + lane_off, h);  // includes tcgen05.wait::st
+            tmem_st32(t_al, h);  // includes tcgen05.wait::st
         }
         fence_async_smem();  // record reads before the next TMA overwrite
         tc_fence_before();
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
         // output: q = max(0, y * (alpha + beta))
         mma_wait();
         uint32_t v[4];
-        tmem_ld4(t_d + lane_off, v);
+        tmem_ld4(t_dl, v);
         tc_fence_before();
         if (valid) {
             float qv[3];
