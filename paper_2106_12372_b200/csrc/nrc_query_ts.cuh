@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(128 * G, 1) nrc_query_ts_kernel(QueryArgs args
     const uint32_t lane_off = (wq * 32u) << 16;
     const uint32_t t_d = tmem_base + uint32_t(W) * g;               // fp32 accumulator
     const uint32_t t_a = tmem_base + uint32_t(W * G) + kACols * g;  // fp16 A operand
-    const uint32_t t_dl = t_d + lane_off, t_al = t_a + lane_off;      // this warp's lane quadrant
+    // this warp's lane quadrant, warp-uniform (kept in uniform registers for tcgen05.ld / st)
+    const uint32_t t_dl = warp_uniform(t_d + lane_off), t_al = warp_uniform(t_a + lane_off);
     // called by the whole issuer warp (converged)
     auto issue_layer = [&](int L) {
         // the weight tile's address made warp-uniform first: the descriptor
