@@ -96,8 +96,9 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
     tc_fence_after();
     pdl_trigger();  // the optimiser kernel may launch (its griddepcontrol.wait covers this grid)
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t lane_off = ((warp & 3u) * 32u) << 16;
+    const uint32_t lane_off = warp_uniform(((warp & 3u) * 32u) << 16);  // (uniform register for tcgen05.ld)
     const uint32_t t_acc = tmem_base;
+    const uint32_t t_accl = warp_uniform(t_acc + lane_off);  // this warp's lane quadrant of the accumulator
     auto t_g = [&](int j) -> uint32_t { return tmem_base + uint32_t(kNW) * (1u + uint32_t(j)); };
     auto slot = [&](int i) -> uint32_t { return sH_a + uint32_t(i) * kTileBytes; };
     auto gbuf = [&](int j) -> uint32_t { return sGb_a + uint32_t(j & 1) * kTileBytes; };
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
     #pragma unroll
             for (int p = 0; p < W / 32; ++p) {
                 uint32_t v[32];
-                tmem_ld32(t_acc + lane_off + 32u * p, v);
+                tmem_ld32(t_accl + 32u * p, v);
     #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t off = swz(r, uint32_t(p * 4 + q));
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
     #pragma unroll
                 for (int p = 0; p < W / 32; ++p) {
                     uint32_t v[32];
-                    tmem_ld32(t_acc + lane_off + 32u * p, v);
+                    tmem_ld32(t_accl + 32u * p, v);
     #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const float* f = reinterpret_cast<const float*>(v) + 8 * q;
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
             // ---------------- relative L2 loss, Eq.(5) (R8-R10, R13, R25)
             {
                 uint32_t v[4];
-                tmem_ld4(t_acc + lane_off, v);
+                tmem_ld4(t_accl, v);
                 const bool use = valid && isfinite(tg[0]) && isfinite(tg[1]) && isfinite(tg[2]);
                 if (valid && !use) ++bad;
                 float yh[3], f[3];
