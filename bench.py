@@ -316,6 +316,11 @@ def run_nrc(args):
             # N3 (i): this rank's screen-region records, one all-gather, replicated training
             dpf.train_frame_replicated(d_rl, d_tl, TRAIN_S, TRAIN_L, seed, counts=t_counts)
             launches += dpf.last_launch_count
+        elif mode == "allreduce-sym":
+            # the per-step all-reduce folded into the optimiser's loads over peer
+            # memory (symmetric buffers of the reduced [gradient | loss], no NCCL call)
+            dpf.train_frame_allreduce_sym(d_r, d_t, TRAIN_S, TRAIN_L, seed)
+            launches += dpf.last_launch_count
         elif mode == "allreduce-nvls":
             # SURVEY 8(e) mitigation 2 / N3 (ii): the gradient all-reduce done in the
             # NVSwitch (multimem.ld_reduce read by the optimiser kernel; no NCCL call)
@@ -365,7 +370,7 @@ def run_nrc(args):
     # partition, each on a fresh cache, device time max over ranks
     mode_ms = {}
     if world > 1 and not args.no_mode_table:
-        for m in ["dp", "replicated", "allreduce-peer", "allreduce-nvls"]:
+        for m in ["dp", "replicated", "allreduce-peer", "allreduce-sym", "allreduce-nvls"]:
             try:
                 c2 = nrc.RadianceCache(nrc.Config(max_batch=max(N_QUERY, N_TRAIN)), device=local)
                 f2 = nrc.DataParallelFrame(c2, device=dev)
@@ -379,6 +384,8 @@ def run_nrc(args):
                         f2.train_frame_replicated(d_rl, d_tl, TRAIN_S, TRAIN_L, 1000 + fi, counts=t_counts)
                     elif m == "allreduce-peer":
                         f2.train_frame_allreduce_peer(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi)
+                    elif m == "allreduce-sym":
+                        f2.train_frame_allreduce_sym(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi)
                     else:
                         f2.train_frame_allreduce_nvls(d_r, d_t, TRAIN_S, TRAIN_L, 1000 + fi)
                 for i in range(3):
@@ -513,12 +520,14 @@ def main():
     ap.add_argument("--workload", choices=["1080p", "4k"], default="1080p",
                     help="1080p: BASELINE.json configs[1] (the metric's workload); 4k: configs[4] (C5), "
                          "8,294,400 queries + 4x16384 train, for the multi-GPU scaling runs")
-    ap.add_argument("--train-mode", choices=["dp", "replicated", "allreduce-peer", "allreduce-nvls"], default="dp",
+    ap.add_argument("--train-mode", choices=["dp", "replicated", "allreduce-peer", "allreduce-sym", "allreduce-nvls"],
+                    default="dp",
                     help="N > 1 training: data-parallel with one NCCL all-reduce per step (dp, north_star's "
                          "partition, the default), one all-gather of the frame's records then replicated "
                          "training (replicated, SURVEY N3 (i)), or data-parallel with the gradient all-reduce "
-                         "fused into the optimiser over peer memory (allreduce-peer, N3 (ii)) or done in the "
-                         "NVSwitch with multimem.ld_reduce feeding the optimiser (allreduce-nvls, N3 (ii))")
+                         "fused into the optimiser over peer memory (allreduce-peer: every tile partial; "
+                         "allreduce-sym: each rank's reduced gradient), or done in the NVSwitch with "
+                         "multimem.ld_reduce feeding the optimiser (allreduce-nvls, N3 (ii))")
     args = ap.parse_args()
     if args.workload == "4k":
         global N_QUERY, METRIC, CONFIG_NAME

@@ -250,6 +250,23 @@ nrc_status nrc_dp_timeouts(nrc_handle* h, uint64_t* count);
 nrc_status nrc_train_apply_multimem(nrc_handle* h, const float* mc_grad, uint32_t n_global, float* d_loss,
                                     void* stream);
 
+/* Data-parallel Adam + EMA step with the all-reduce folded into the
+ * optimiser's loads over peer memory (SURVEY 8(e) mitigation 2 without NVLS;
+ * P:L896-902 on the batch of P:L491 split over the ranks).  peer_bufs: host
+ * array of `world` device pointers (16-byte aligned), rank order, each rank's
+ * [logical gradient sum (nrc_param_count floats) | loss sum] as written by
+ * nrc_train_frame_backward -- this rank's own buffer and its peers' (mapped
+ * over NVLink, e.g. a symmetric-memory buffer).  Every gradient entry is
+ * summed over the ranks in rank order, so every rank applies the same
+ * gradient (replicas stay bitwise identical; not bitwise equal to one GPU,
+ * the per-rank sums add in another order).  The caller orders the call after
+ * every rank's buffer is written (nrc_peer_barrier) and keeps the buffers
+ * untouched until every rank's call has completed (two buffer sets by step
+ * parity).  d_loss (optional) receives the loss sum / n_global.  Increments
+ * the step counter. */
+nrc_status nrc_train_apply_peers(nrc_handle* h, const float* const* peer_bufs, uint32_t world, uint32_t n_global,
+                                 float* d_loss, void* stream);
+
 /* A single-process NVLS buffer on `device` (multicast object with this one
  * device bound; driver multicast support required, else
  * NRC_ERR_UNSUPPORTED): *d_uc = its ordinary (unicast) address, *d_mc = its

@@ -38,7 +38,7 @@ SYMBOLS = [
     "nrc_frame_scratch_bytes", "nrc_frame_host", "nrc_selftest_umma", "nrc_last_launch_count",
     "nrc_assemble_targets", "nrc_query_accumulate", "nrc_train_frame_dp_peer",
     "nrc_dp_timeouts", "nrc_ipc_export", "nrc_ipc_import", "nrc_ipc_close", "nrc_train_apply_multimem",
-    "nrc_peer_barrier", "nrc_multicast_alloc", "nrc_multicast_free",
+    "nrc_peer_barrier", "nrc_multicast_alloc", "nrc_multicast_free", "nrc_train_apply_peers",
 ]
 
 
@@ -80,6 +80,7 @@ def load(build_if_missing: bool = True):
     L.nrc_dp_timeouts.restype = st; L.nrc_dp_timeouts.argtypes = [vp, P(u64)]
     L.nrc_train_apply_multimem.restype = st; L.nrc_train_apply_multimem.argtypes = [vp, vp, u32, vp, vp]
     L.nrc_peer_barrier.restype = st; L.nrc_peer_barrier.argtypes = [vp, vp, u32, u32, vp]
+    L.nrc_train_apply_peers.restype = st; L.nrc_train_apply_peers.argtypes = [vp, vp, u32, u32, vp, vp]
     L.nrc_multicast_alloc.restype = st; L.nrc_multicast_alloc.argtypes = [ctypes.c_int, sz, P(vp), P(vp)]
     L.nrc_multicast_free.restype = st; L.nrc_multicast_free.argtypes = [vp]
     L.nrc_ipc_export.restype = st; L.nrc_ipc_export.argtypes = [vp, vp, P(u64)]

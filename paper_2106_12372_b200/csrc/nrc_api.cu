@@ -90,7 +90,7 @@ WidthInfo width_info(int W, int nh) {
 }
 
 struct StateLayout {
-    size_t w, m, v, ema, wimg, eimg, partials, loss_part, counters, dp_tables, total;
+    size_t w, m, v, ema, wimg, eimg, partials, loss_part, counters, dp_tables, peer_tab, total;
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -119,6 +119,8 @@ StateLayout layout(int W, int nh) {
     L.counters = take(sizeof(unsigned long long) * 8);
     // nrc_train_frame_dp_peer: per step parity, kMaxDpTiles partial + loss pointers
     L.dp_tables = take(sizeof(const float*) * 2 * 2 * kMaxDpTiles);
+    // nrc_train_apply_peers: two tables of kMaxRanks peer-buffer pointers
+    L.peer_tab = take(sizeof(const float*) * 2 * kMaxRanks);
     L.total = o;
     return L;
 }
@@ -144,6 +146,10 @@ struct nrc_handle {
     long long* dbg = nullptr;  // diagnostics only (nrc_debug_set_trace)
     unsigned long long dp_expect = 0;  // hand-off counter value after the last nrc_train_frame_dp_peer step
     unsigned long long bar_expect = 0; // nrc_peer_barrier: this rank's counter value after the last barrier
+    // nrc_train_apply_peers: host copies of the two device pointer tables
+    const float* peer_tab_host[2][kMaxRanks] = {};
+    uint32_t peer_tab_world[2] = {0, 0};
+    int peer_tab_next = 0;
     uint64_t dp_seq = 0;               // steps done by nrc_train_frame_dp_peer (partial-slot parity)
     WidthInfo wi;                 // hidden width (64 unless the C4 width ablation)
     int query_ctas = 0;           // cap on the query grid (0: all SMs)
@@ -1008,6 +1014,48 @@ nrc_status nrc_train_apply_multimem(nrc_handle* h, const float* mc_grad, uint32_
     aw.loss_scale = aw.inv_n;
     aw.loss_out = d_loss;
     return launch_adam_w(h, aw, static_cast<cudaStream_t>(stream));
+}
+
+nrc_status nrc_train_apply_peers(nrc_handle* h, const float* const* peer_bufs, uint32_t world, uint32_t n_global,
+                                 float* d_loss, void* stream) {
+    nrc_status s = check_handle(h);
+    if (s != NRC_OK) return s;
+    if ((s = check_train_width(h)) != NRC_OK) return s;
+    h->launches = 0;
+    if (!peer_bufs || world == 0 || world > uint32_t(kMaxRanks))
+        return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply_peers: 1..8 peer buffers");
+    for (uint32_t p = 0; p < world; ++p)
+        if (!peer_bufs[p] || !aligned(peer_bufs[p], 16))
+            return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply_peers: NULL or misaligned peer buffer");
+    if (d_loss && !aligned(d_loss, 4)) return fail(h, NRC_ERR_INVALID_ARGUMENT, "nrc_train_apply_peers: misaligned d_loss");
+    if (n_global == 0) return NRC_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // the pointer table in device memory: reuse one of two slots when it holds
+    // the same pointers (buffers alternate by step parity), else refill one
+    const float** d_tab = reinterpret_cast<const float**>(h->state + h->L.peer_tab);
+    int slot = -1;
+    for (int q = 0; q < 2 && slot < 0; ++q)
+        if (h->peer_tab_world[q] == world &&
+            std::equal(peer_bufs, peer_bufs + world, static_cast<const float* const*>(h->peer_tab_host[q])))
+            slot = q;
+    if (slot < 0) {
+        slot = h->peer_tab_next;
+        h->peer_tab_next ^= 1;
+        std::copy(peer_bufs, peer_bufs + world, h->peer_tab_host[slot]);
+        h->peer_tab_world[slot] = world;
+        // pageable source: staged before the call returns
+        NRC_CUDA(h, cudaMemcpyAsync(d_tab + slot * kMaxRanks, h->peer_tab_host[slot], sizeof(const float*) * world,
+                                    cudaMemcpyHostToDevice, st));
+    }
+    h->step += 1;
+    AdamWArgs aw = adam_w_args(h);
+    aw.peer_grad = d_tab + slot * kMaxRanks;
+    aw.npeer = int(world);
+    aw.apply = 1;
+    aw.inv_n = float(1.0 / double(n_global));
+    aw.loss_scale = aw.inv_n;
+    aw.loss_out = d_loss;
+    return launch_adam_w(h, aw, st);
 }
 
 nrc_status nrc_peer_barrier(nrc_handle* h, void* const* peer_counters, uint32_t rank, uint32_t world, void* stream) {

@@ -553,6 +553,12 @@ struct AdamWArgs {
     // multicast address of every rank's [logical gradient sum | loss sum];
     // g = multimem.ld_reduce (the all-reduce done in the switch), loss likewise
     const float* grad_mc;
+    // peer mode (nrc_train_apply_peers), if peer_grad != nullptr: a device
+    // table of npeer pointers to every rank's [logical gradient sum | loss
+    // sum] (peer memory over NVLink); g = their sum in rank order, identical
+    // on every rank
+    const float* const* peer_grad;
+    int npeer;
 };
 
 template <int W>
@@ -601,6 +607,15 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
             for (int u = 0; u < kIn; ++u) s = f4_add(s, x[u]);
         }
         sred[wp][lane] = s;
+    } else if (wp == 0 && a.peer_grad != nullptr) {
+        if (j0 < D.logical()) {  // 4 consecutive logical entries; all ranks' loads in flight, then the sum in rank order
+            float4 x[kMaxRanks];
+#pragma unroll
+            for (int p = 0; p < kMaxRanks; ++p) x[p] = p < a.npeer ? ld_sys_v4(a.peer_grad[p] + j0) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int p = 0; p < kMaxRanks; ++p)
+                if (p < a.npeer) g = f4_add(g, x[p]);
+        }
     } else if (wp == 0 && a.grad_mc != nullptr) {
         // 4 consecutive logical entries (j0 % 4 == 0; W5's pad rows are beyond logical)
         if (j0 < D.logical()) g = multimem_ld_reduce_v4(a.grad_mc + j0);
@@ -621,7 +636,10 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
     const float4 m = sstate[0][lane], v = sstate[1][lane], w = sstate[2][lane], em = sstate[3][lane];
     if (blockIdx.x == 0 && a.loss_out != nullptr) {
         float s = 0.0f;
-        if (a.grad_mc != nullptr) {
+        if (a.peer_grad != nullptr) {
+            if (lane == 0)
+                for (int p = 0; p < a.npeer; ++p) s += ld_sys_f32(a.peer_grad[p] + D.logical());
+        } else if (a.grad_mc != nullptr) {
             if (lane == 0) s = multimem_ld_reduce_f32(a.grad_mc + D.logical());
         } else {
             for (int p = lane; p < a.nloss; p += 32)

@@ -157,48 +157,56 @@ class DataParallelFrame:
         self.last_launch_count = getattr(self.cache, "last_launch_count", 0)
         return out
 
-    def _nvls_setup(self):
-        """Symmetric memory for train_frame_allreduce_nvls: two [gradient |
+    def _sym_setup(self, multicast: bool):
+        """Peer-mapped buffers for the in-kernel all-reduce modes: two [gradient |
         loss sum] buffers (step parity) + one barrier counter per rank, mapped
-        on every rank (torch symmetric memory over the process group) with a
+        on every rank -- CUDA IPC handles exchanged over the process group, or
+        (multicast=True) torch symmetric memory, which also gives the buffer's
         multicast (NVLS) address."""
-        import torch.distributed._symmetric_memory as symm_mem
-        self._nvls_stride = (NPARAM + 1 + 63) // 64 * 64  # floats per buffer, 256-B aligned
-        n = 2 * self._nvls_stride + 64
+        self._sym_stride = (NPARAM + 1 + 63) // 64 * 64  # floats per buffer, 256-B aligned
+        n = 2 * self._sym_stride + 64
         esz = 4
-        buf = symm_mem.empty(n, dtype=torch.float32, device=self.device)
-        buf.zero_()
-        gname = (self.group or dist.group.WORLD).group_name
-        hdl = symm_mem.rendezvous(buf, gname)
-        if getattr(hdl, "multicast_ptr", 0):
-            self._nvls_hdl, self._nvls_buf = hdl, buf
-            mc, ctr = hdl.multicast_ptr, [int(p) + 2 * self._nvls_stride * esz for p in hdl.buffer_ptrs]
-        elif self.world == 1:
+        mc = 0
+        if not multicast:
+            # peer mappings through CUDA IPC (also two ranks on one GPU, where
+            # torch's symmetric memory refuses overlapping devices)
+            from .nrc import ipc_export_ptr, ipc_import
+            buf = torch.zeros(n, dtype=torch.float32, device=self.device)
+            mine = ipc_export_ptr(buf.data_ptr())
+            everyone = [None] * self.world
+            dist.all_gather_object(everyone, mine, group=self.group)
+            self._sym_buf = buf
+            ptrs = [buf.data_ptr() if r == self.rank else ipc_import(*everyone[r]) for r in range(self.world)]
+            self._sym_multicast = False
+        else:
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(n, dtype=torch.float32, device=self.device)
+            buf.zero_()
+            gname = (self.group or dist.group.WORLD).group_name
+            hdl = symm_mem.rendezvous(buf, gname)
+            mc = getattr(hdl, "multicast_ptr", 0)
+        if multicast and mc:
+            self._sym_hdl, self._sym_buf = hdl, buf
+            ptrs = [int(p) for p in hdl.buffer_ptrs]
+        elif multicast and self.world == 1:
             # one rank: a single-device multicast object from libnrc (torch exports
             # multicast handles for sharing, which some systems refuse)
             from .nrc import multicast_alloc
-            self._nvls_buf, mc = multicast_alloc(n, self.device)
-            ctr = [self._nvls_buf.data_ptr() + 2 * self._nvls_stride * esz]
-        else:
+            self._sym_buf, mc = multicast_alloc(n, self.device)
+            ptrs = [self._sym_buf.data_ptr()]
+        elif multicast:
             raise RuntimeError("NVLS multicast is not available on this system (symmetric memory without multicast)")
-        self._nvls_mc = [mc + k * self._nvls_stride * esz for k in range(2)]
-        self._nvls_ctr = ctr
-        self._nvls_seq = 0
+        self._sym_mc = [mc + k * self._sym_stride * esz for k in range(2)] if mc else None
+        self._sym_peers = [[p + k * self._sym_stride * esz for p in ptrs] for k in range(2)]
+        self._sym_ctr = [p + 2 * self._sym_stride * esz for p in ptrs]
+        self._sym_seq = 0
+        self._sym_multicast = bool(mc)
         torch.cuda.current_stream().synchronize()
         dist.barrier(group=self.group)  # zeroed everywhere before any rank signals
 
-    def train_frame_allreduce_nvls(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int,
-                                   shuffle_seed: int, losses: Optional[torch.Tensor] = None
-                                   ) -> Optional[torch.Tensor]:
-        """SURVEY 8(e) mitigation 2 / 8(f) N3 (ii): data-parallel training with
-        the gradient all-reduce done in the NVSwitch.  Per step: this rank's
-        rows of the shuffled batch -> its [gradient | loss sum] into a
-        symmetric buffer (by step parity), a cross-rank barrier kernel, then the
-        optimiser reads every entry as multimem.ld_reduce (the sum over the
-        ranks) and applies Adam + EMA -- no NCCL call.  Not bitwise equal to
-        single-GPU training (the switch's fp32 summation order)."""
-        if getattr(self, "_nvls_buf", None) is None:
-            self._nvls_setup()
+    def _train_frame_sym(self, records, targets, s, l, shuffle_seed, losses, multicast: bool):
+        if getattr(self, "_sym_buf", None) is None or (multicast and not self._sym_multicast):
+            self._sym_setup(multicast)
         n_total = int(records.shape[0])
         s, l = frame_batches(n_total, s, l)
         launches = 0
@@ -207,19 +215,44 @@ class DataParallelFrame:
             return losses
         lo, hi = shard(l, self.rank, self.world)
         for j in range(s):
-            par = self._nvls_seq & 1
-            base = par * self._nvls_stride
-            grad = self._nvls_buf[base:base + NPARAM]
-            loss_sum = self._nvls_buf[base + NPARAM:base + NPARAM + 1]
+            par = self._sym_seq & 1
+            base = par * self._sym_stride
+            grad = self._sym_buf[base:base + NPARAM]
+            loss_sum = self._sym_buf[base + NPARAM:base + NPARAM + 1]
             self.cache.train_frame_backward(records, targets, l, shuffle_seed, j, lo, hi, grad, loss_sum)
             launches += getattr(self.cache, "last_launch_count", 0)
-            self.cache.peer_barrier(self._nvls_ctr, self.rank, self.world)
+            self.cache.peer_barrier(self._sym_ctr, self.rank, self.world)
             launches += 1
-            self.cache.train_apply_multimem(self._nvls_mc[par], l, None if losses is None else losses[j:j + 1])
+            out = None if losses is None else losses[j:j + 1]
+            if multicast:
+                self.cache.train_apply_multimem(self._sym_mc[par], l, out)
+            else:
+                self.cache.train_apply_peers(self._sym_peers[par], l, out)
             launches += getattr(self.cache, "last_launch_count", 0)
-            self._nvls_seq += 1
+            self._sym_seq += 1
         self.last_launch_count = launches
         return losses
+
+    def train_frame_allreduce_sym(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int,
+                                  shuffle_seed: int, losses: Optional[torch.Tensor] = None
+                                  ) -> Optional[torch.Tensor]:
+        """Data-parallel training with the per-step all-reduce folded into the
+        optimiser over peer memory: this rank's rows of the shuffled batch ->
+        its [gradient | loss sum] into a peer-mapped buffer (by step parity), a
+        cross-rank barrier kernel, then the optimiser loads every rank's
+        buffer over NVLink and sums them in rank order (nrc_train_apply_peers)
+        -- no NCCL call, identical replicas, 86 KB per peer per step."""
+        return self._train_frame_sym(records, targets, s, l, shuffle_seed, losses, multicast=False)
+
+    def train_frame_allreduce_nvls(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int,
+                                   shuffle_seed: int, losses: Optional[torch.Tensor] = None
+                                   ) -> Optional[torch.Tensor]:
+        """SURVEY 8(e) mitigation 2 / 8(f) N3 (ii): as train_frame_allreduce_sym,
+        but the optimiser reads every gradient entry with multimem.ld_reduce on
+        the buffer's multicast address -- the all-reduce done in the NVSwitch.
+        Not bitwise equal to single-GPU training (the switch's fp32 summation
+        order); every rank reads the same switch result."""
+        return self._train_frame_sym(records, targets, s, l, shuffle_seed, losses, multicast=True)
 
     def train_frame(self, records: torch.Tensor, targets: torch.Tensor, s: int, l: int, shuffle_seed: int,
                     losses: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:

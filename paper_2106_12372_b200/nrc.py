@@ -304,6 +304,16 @@ class RadianceCache:
         self._check(self.L.nrc_train_apply_multimem(self.h, ctypes.c_void_p(int(mc_ptr)), int(n_global), _ptr(loss),
                                                     _stream(stream)), "nrc_train_apply_multimem")
 
+    def train_apply_peers(self, buf_ptrs, n_global: int, loss: Optional[torch.Tensor] = None, stream=None):
+        """nrc_train_apply_peers: Adam + EMA on the rank-order sum of every
+        rank's [gradient | loss sum] buffer (buf_ptrs: device addresses, own
+        included, peers' mapped over NVLink), divided by n_global."""
+        if loss is not None:
+            self._f32(loss, tuple(loss.shape), "loss")
+        ps = (ctypes.c_void_p * len(buf_ptrs))(*[int(p) for p in buf_ptrs])
+        self._check(self.L.nrc_train_apply_peers(self.h, ps, len(buf_ptrs), int(n_global), _ptr(loss), _stream(stream)),
+                    "nrc_train_apply_peers")
+
     def peer_barrier(self, counter_ptrs, rank: int, world: int, stream=None):
         """nrc_peer_barrier: cross-rank barrier on the stream over peer-mapped
         u64 counters (counter_ptrs: every rank's counter, own included)."""

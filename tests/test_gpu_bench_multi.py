@@ -22,7 +22,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode", ["dp", "replicated", "allreduce-peer"])
+@pytest.mark.parametrize("mode", ["dp", "replicated", "allreduce-peer", "allreduce-sym"])
 def test_bench_two_ranks_shared_gpu(mode):
     if not torch.cuda.is_available():
         pytest.skip("needs a B200")
@@ -42,6 +42,6 @@ def test_bench_two_ranks_shared_gpu(mode):
     assert line["gpu_launches"] > 0 and line["value"] > 0
     if mode == "dp":  # the N3 comparison: every partition trained the frame (NVLS where multicast exists)
         tm = line["train_modes"]
-        assert set(tm) == {"dp", "replicated", "allreduce-peer", "allreduce-nvls"}
+        assert set(tm) == {"dp", "replicated", "allreduce-peer", "allreduce-sym", "allreduce-nvls"}
         for m in ("dp", "replicated", "allreduce-peer"):
             assert tm[m]["train_ms"] > 0 and tm[m]["replicas"].startswith("identical"), tm

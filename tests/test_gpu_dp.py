@@ -109,3 +109,29 @@ def test_nvls_frame_world1_equals_dp_frame(group):
     np.testing.assert_array_equal(b.get_params("ema"), a.get_params("ema"))
     assert b.dp_timeouts() == 0
     assert fb.last_launch_count == 4 * s  # partials + reduce, barrier, optimiser per step
+
+
+def test_sym_frame_world1_equals_dp_frame(group):
+    """The all-reduce folded into the optimiser over peer memory
+    (nrc_train_apply_peers + nrc_peer_barrier over torch symmetric memory):
+    with one rank the rank-order sum is the rank's own reduced gradient, so the
+    frame equals the NCCL data-parallel frame bitwise (two frames: both buffer
+    parities)."""
+    import paper_2106_12372_b200 as nrc
+    n, s, l, seed = 8192 + 3, 4, 2048, 31
+    recs, tg = nrc_inputs.train_frame(5, n=n, noise=0.3)
+    d_r = torch.from_numpy(recs).cuda()
+    d_t = torch.from_numpy(tg).cuda()
+    a, b = nrc.RadianceCache(), nrc.RadianceCache()
+    fa = nrc.DataParallelFrame(a, device=torch.device("cuda", 0))
+    fb = nrc.DataParallelFrame(b, device=torch.device("cuda", 0))
+    la = torch.zeros(s, dtype=torch.float32, device="cuda")
+    lb = torch.zeros(s, dtype=torch.float32, device="cuda")
+    for f in range(2):
+        fa.train_frame(d_r, d_t, s, l, seed + f, la)
+        fb.train_frame_allreduce_sym(d_r, d_t, s, l, seed + f, lb)
+    np.testing.assert_array_equal(lb.cpu().numpy(), la.cpu().numpy())
+    np.testing.assert_array_equal(b.get_params("train"), a.get_params("train"))
+    np.testing.assert_array_equal(b.get_params("ema"), a.get_params("ema"))
+    assert b.dp_timeouts() == 0
+    assert fb.last_launch_count == 4 * s  # partials + reduce, barrier, optimiser per step
