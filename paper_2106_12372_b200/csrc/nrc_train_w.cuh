@@ -494,7 +494,10 @@ __device__ __forceinline__ uint32_t adam_ema(float g, const AdamCoef& k, float& 
     }
     m = k.b1 * m + (1.0f - k.b1) * g;
     v = k.b2 * v + (1.0f - k.b2) * g * g;
-    w = w - k.lr * (m * k.inv_bc1) / (sqrtf(v * k.inv_bc2) + k.eps);
+    // sqrt.approx and the fast reciprocal-multiply division (relative error
+    // <= 2 ulp on the update; the IEEE sqrtf / division slow paths, taken for
+    // v = 0 entries, cost ~1.3 us on the step's critical path, DESIGN 5)
+    w = w - __fdividef(k.lr * (m * k.inv_bc1), sqrt_approx(v * k.inv_bc2) + k.eps);
     e = k.ema_c1 * w + k.ema_c2 * e;
     return bad;
 }
@@ -569,8 +572,10 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
     const int e = int(blockIdx.x) * 32 + lane;  // float4 element of the chunk-major layout
     const int k = 4 * e;
     const int i = D.layer_of(k);  // one layer per block (layer sizes are multiples of 128)
-    pdl_wait();     // launched as a programmatic dependent of the partials kernel
+    pdl_wait();  // launched as a programmatic dependent of the partials kernel
+#ifndef NRC_ADAM_LATE_TRIGGER
     pdl_trigger();  // the next step's partials kernel may become resident (its griddepcontrol.wait covers this grid)
+#endif
     const bool trc = a.dbg != nullptr && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x + 1 == gridDim.x);
     if (trc) a.dbg[4088 + 2 * (blockIdx.x != 0)] = global_ns();
 
@@ -592,7 +597,10 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
         float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
         const size_t stride = size_t(D.padded()) / 4;
         const float4* src = reinterpret_cast<const float4*>(a.partials) + e;
-        constexpr int kIn = 8;  // partial loads in flight per thread
+#ifndef NRC_ADAM_KIN
+#define NRC_ADAM_KIN 8
+#endif
+        constexpr int kIn = NRC_ADAM_KIN;  // partial loads in flight per thread
 #pragma unroll 1
         for (int p0 = wp; p0 < a.np; p0 += kAdamWarps * kIn) {
             float4 x[kIn];
@@ -606,6 +614,7 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
 #pragma unroll
             for (int u = 0; u < kIn; ++u) s = f4_add(s, x[u]);
         }
+        if (trc) a.dbg[4086 + (blockIdx.x != 0)] = global_ns();
         sred[wp][lane] = s;
     } else if (wp == 0 && a.peer_grad != nullptr) {
         if (j0 < D.logical()) {  // 4 consecutive logical entries; all ranks' loads in flight, then the sum in rank order
@@ -632,9 +641,9 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
 #pragma unroll
         for (int q = 0; q < kAdamWarps; ++q) g = f4_add(g, sred[q][lane]);
     }
-    if (wp != 0) return;
-    const float4 m = sstate[0][lane], v = sstate[1][lane], w = sstate[2][lane], em = sstate[3][lane];
-    if (blockIdx.x == 0 && a.loss_out != nullptr) {
+    if (wp == 1 && blockIdx.x == 0 && a.loss_out != nullptr) {
+        // the batch loss, off warp 0's critical path: all loads in flight,
+        // then each lane's sum in partial order and a butterfly
         float s = 0.0f;
         if (a.peer_grad != nullptr) {
             if (lane == 0)
@@ -642,13 +651,26 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
         } else if (a.grad_mc != nullptr) {
             if (lane == 0) s = multimem_ld_reduce_f32(a.grad_mc + D.logical());
         } else {
-            for (int p = lane; p < a.nloss; p += 32)
-                s += a.tile_part != nullptr ? ld_sys_f32(a.tile_loss[p]) : __ldcg(a.loss_part + p);
+#pragma unroll 1
+            for (int p0 = lane; p0 < a.nloss; p0 += 4 * 32) {
+                float x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int p = p0 + 32 * u;
+                    x[u] = p >= a.nloss ? 0.0f : a.tile_part != nullptr ? ld_sys_f32(a.tile_loss[p]) : __ldcg(a.loss_part + p);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (p0 + 32 * u < a.nloss) s += x[u];
+            }
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane == 0) *a.loss_out = s * a.loss_scale;
+        return;
     }
+    if (wp != 0) return;
+    const float4 m = sstate[0][lane], v = sstate[1][lane], w = sstate[2][lane], em = sstate[3][lane];
     float gq[4] = {g.x, g.y, g.z, g.w};
     if (a.grad_out != nullptr) {
 #pragma unroll
@@ -663,6 +685,7 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
 #pragma unroll
     for (int q = 0; q < 4; ++q) nbad += adam_ema(gq[q] * a.inv_n, kc, mq[q], vq[q], wq[q], eq[q]);
     if (nbad) atomicAdd(a.bad_grads, (unsigned long long)nbad);
+    if (trc) a.dbg[4092 + (blockIdx.x != 0)] = global_ns();
     *reinterpret_cast<float4*>(a.m + j0) = make_float4(mq[0], mq[1], mq[2], mq[3]);
     *reinterpret_cast<float4*>(a.v + j0) = make_float4(vq[0], vq[1], vq[2], vq[3]);
     *reinterpret_cast<float4*>(a.w + j0) = make_float4(wq[0], wq[1], wq[2], wq[3]);

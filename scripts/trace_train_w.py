@@ -62,6 +62,7 @@ for k in range(4):
         for j in range(5, -1, -1):
             col = fl[:, j] - t0
             print(f"  wgrad {j} done     min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}")
-    print(f"  adam blk0 {blk[4088] - t0:7d} -> sum {blk[4084] - t0:7d} -> {blk[4089] - t0:7d}   "
-          f"last blk {blk[4090] - t0:7d} -> sum {blk[4085] - t0:7d} -> {blk[4091] - t0:7d}")
+    print(f"  adam blk0 {blk[4088] - t0:7d} -> w0 loads {blk[4086] - t0:7d} -> sum {blk[4084] - t0:7d} -> math "
+          f"{blk[4092] - t0:7d} -> {blk[4089] - t0:7d}   last blk {blk[4090] - t0:7d} -> w0 loads {blk[4087] - t0:7d} -> sum "
+          f"{blk[4085] - t0:7d} -> math {blk[4093] - t0:7d} -> {blk[4091] - t0:7d}")
 c.L.nrc_debug_set_trace(c.h, None)
