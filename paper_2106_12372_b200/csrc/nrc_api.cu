@@ -47,7 +47,10 @@ struct QueryLauncherW {
             nrc_query_ts_kernel<G, W, 0, EXACT><<<grid, 128 * G, smem, st>>>(qa);
     }
 };
-const QueryEntry kQuery64 = {&QueryLauncherW<5, 64>::set_smem, &QueryLauncherW<5, 64>::launch, 5};
+#ifndef NRC_Q64_G
+#define NRC_Q64_G 5
+#endif
+const QueryEntry kQuery64 = {&QueryLauncherW<NRC_Q64_G, 64>::set_smem, &QueryLauncherW<NRC_Q64_G, 64>::launch, NRC_Q64_G};
 const QueryEntry kQueryExact = {&QueryLauncherW<5, 64, true>::set_smem, &QueryLauncherW<5, 64, true>::launch, 5};
 #ifndef NRC_W32_G
 #define NRC_W32_G 7  // 7 groups: 82 us vs 90 us with 5 at 1080p (round 1, 5 / 7 groups at width 32)
