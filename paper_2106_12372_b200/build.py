@@ -10,7 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnrc.so")
 SOURCES = ["nrc_api.cu"]
-DEPS = ["nrc_api.cu", "nrc_kernels.cuh", "nrc_common.cuh", "nrc_query_ts.cuh", "nrc_train_w.cuh", "nrc_device.cuh"]
+DEPS = ["nrc_api.cu", "nrc_kernels.cuh", "nrc_common.cuh", "nrc_query_ts.cuh", "nrc_train_w.cuh", "nrc_train_ws.cuh",
+        "nrc_device.cuh"]
 
 
 def nvcc() -> str:

@@ -23,7 +23,7 @@ tr, tg = torch.from_numpy(tr).cuda(), torch.from_numpy(tg).cuda()
 c = nrc.RadianceCache(nrc.Config(hidden_width=hw))
 for _ in range(5):
     c.train_frame(tr, tg, 4, 16384, 1)
-buf = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16 * 4096, dtype=torch.int64, device="cuda")  # adam SM ids at 32768 + 4096 step + block
 c.L.nrc_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 c.L.nrc_debug_set_trace(c.h, ctypes.c_void_p(buf.data_ptr()))
 torch.cuda.synchronize()
@@ -50,14 +50,33 @@ names = {k: names[k] for k in order}
 for k in range(4):
     blk = d[(step0 + k) % 4]
     g = blk[:32 * 127].reshape(127, 32)
-    g = g[g[:, 0] != 0]
+    g = g[g[:, 8] != 0]  # (the frame kernel writes mark 0 at its start only)
     if t0 is None:
-        t0 = g[:, 0].min()
+        t0 = g[:, 0].min() if g[:, 0].min() > 0 else g[:, 8].min()
     print(f"--- step {k} ({len(g)} CTAs), ns from the frame's first CTA start")
     for i, nm in names.items():
         col = g[:, i] - t0
         print(f"  {nm:14s} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}")
+    st = g[:, 0] - t0
+    late = np.nonzero(st > np.median(st) + 1000)[0]
+    if len(late) and g[:, 7].max() > 0:  # CTAs starting > 1 us after the median: block index, SM, start
+        print("  late CTAs (block, sm, start):", [(int(b), int(g[b, 7]), int(st[b])) for b in late])
+        prev = dall[32768 + 4096 * ((step0 + k - 1) % 4):32768 + 4096 * ((step0 + k - 1) % 4) + 4096]
+        nblk = int((prev != 0).sum()) + 1
+        ad = np.bincount(prev[:nblk], minlength=160)
+        early = [int(ad[int(g[b, 7])]) for b in range(len(g)) if b not in set(late)]
+        lat = [int(ad[int(g[b, 7])]) for b in late]
+        print(f"  previous optimiser blocks on the SM of each early CTA: {np.bincount(early).tolist()}, late CTA: {np.bincount(lat).tolist()}")
+        print(f"  optimiser blocks per SM histogram: {np.bincount(ad[:148]).tolist()}")
+        res = dall[49152 + 4096 * ((step0 + k - 1) % 4):49152 + 4096 * ((step0 + k - 1) % 4) + nblk] - t0
+        print(f"  previous optimiser blocks resident at (ns): min {res.min()} p25 {int(np.percentile(res, 25))} med {int(np.median(res))} p75 {int(np.percentile(res, 75))} max {res.max()}")
     fl = dall[16384 + 4096 * ((step0 + k) % 4):16384 + 4096 * ((step0 + k) % 4) + 32 * 127].reshape(127, 32)
+    if fl[:, 8:13].any():  # frame kernel: exchange marks of thread 0
+        for m, nm in enumerate(["exchange entry", "barrier A passed", "slice loads done", "adam done", "barrier B passed"]):
+            col = fl[:, 8 + m]
+            col = col[col != 0] - t0
+            if len(col):
+                print(f"  {nm:16s} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}")
     if fl[:, :8].any():  # NRC_TRACE_FLUSH builds: wgrad_j completion seen by the flush warps
         for j in range(5, -1, -1):
             col = fl[:, j] - t0

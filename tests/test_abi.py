@@ -47,6 +47,33 @@ def test_library_is_sm100a_tcgen05(libnrc):
     assert "HMMA" not in re.sub(r"UTCHMMA", "", sass)  # no legacy mma.sync path
 
 
+def _res_usage():
+    """{kernel: registers}, {kernel: local-memory bytes} from cuobjdump -res-usage."""
+    from paper_2106_12372_b200 import _lib
+    out = subprocess.run(["cuobjdump", "-res-usage", _lib.lib_path()], capture_output=True, text=True).stdout
+    rows = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) .*?LOCAL:(\d+)", out)
+    return {f: int(r) for f, r, _ in rows}, {f: int(l) for f, _, l in rows}
+
+
+def test_partials_kernel_fits_beside_an_optimiser_block(libnrc):
+    """Co-residency budget (DESIGN 5.2): the next step's partials CTA becomes
+    resident beside one optimiser block and gathers + encodes while the
+    reduction runs.  Register files are split per SM sub-partition (16,384
+    registers each); the partials CTA's 9 warps put 3 on one of them and an
+    8-warp optimiser block 2, so 3 R_p + 2 R_a <= 512 (registers rounded up to
+    8 per thread).  A partials kernel at 138 registers broke this and cost
+    ~2 us per frame.  No hot kernel spills to local memory."""
+    regs, local = _res_usage()
+    up8 = lambda r: (int(r) + 7) // 8 * 8
+    ra = up8(regs["_ZN3nrc17nrc_adam_w_kernelILi64EEEvNS_9AdamWArgsE"])
+    for w in (32, 64):
+        rp = up8(regs[f"_ZN3nrc19nrc_train_ws_kernelILi{w}ELb0EEEvNS_9TrainArgsE"])
+        assert 3 * rp + 2 * ra <= 512, (w, rp, ra)
+    for f, l in local.items():
+        if "query_ts_kernel" in f or "train_ws_kernel" in f or "adam_w_kernel" in f:
+            assert l == 0, f
+
+
 def test_default_config_and_state_bytes(libnrc):
     from paper_2106_12372_b200 import _lib
     c = _lib.NrcConfig()
