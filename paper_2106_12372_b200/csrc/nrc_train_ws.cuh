@@ -27,6 +27,9 @@
 
 namespace nrc {
 
+#ifndef NRC_WS_MAXNREG
+#define NRC_WS_MAXNREG __maxnreg__(112)
+#endif
 template <int W>
 struct TrainWs {
     static_assert(W == 32 || W == 64, "the split schedule keeps one 64-column TMEM accumulator per layer");
@@ -42,7 +45,7 @@ struct TrainWs {
 static_assert(TrainWs<64>::smem_bytes(TrainWs<64>::kMaxNh) <= 232448, "227 KB of SMEM per CTA");
 
 template <int W, bool EXACT = false>
-__global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(TrainArgs a) {
+__global__ void NRC_WS_MAXNREG nrc_train_ws_kernel(TrainArgs a) {
     const NetRt<W> D(int(a.nh));
     const int nh = D.nh;
     using T = TrainWs<W>;
@@ -233,21 +236,26 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
             fence_async_smem();
             asm volatile("bar.arrive 3, 160;" ::: "memory");
         };
-        // g_j = delta_j * 1[h_j > 0] -> gbuf[j & 1] (ReLU'(0) = 0, R17)
-        auto mask_epilogue = [&](int j) {
+        // g_j = delta_j * 1[h_j > 0] -> gbuf[j & 1] (ReLU'(0) = 0, R17).  The
+        // row's h_j chunks are loaded before the dgrad wait (mask_prefetch), so
+        // no shared-memory round trip sits between the accumulator and the
+        // hand-off; both accumulator halves are read before the first store.
+        constexpr int kChunks = W / 8;  // 16-B chunks of a row
+        auto mask_prefetch = [&](int j, uint4 (&hv)[kChunks]) {
     #pragma unroll
-            for (int p = 0; p < W / 32; ++p) {
-                uint32_t v[32];
-                tmem_ld32(t_accl + 32u * p, v);
+            for (int c = 0; c < kChunks; ++c) hv[c] = ld_shared_v4(slot(j) + swz(r, uint32_t(c)));
+        };
+        auto mask_epilogue = [&](int j, const uint4 (&hv)[kChunks]) {
+            uint32_t v[W];
+            tmem_ld32(t_accl, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+            if (W == 64) tmem_ld32(t_accl + 32u, *reinterpret_cast<uint32_t(*)[32]>(&v[W == 64 ? 32 : 0]));
+            const float* f = reinterpret_cast<const float*>(v);
     #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t off = swz(r, uint32_t(p * 4 + q));
-                    const uint4 hv = ld_shared_v4(slot(j) + off);
-                    const float* f = reinterpret_cast<const float*>(v) + 8 * q;
-                    st_shared_v4(gbuf(j) + off, pack_h2(f[0], f[1]) & relu_mask(hv.x), pack_h2(f[2], f[3]) & relu_mask(hv.y),
-                                 pack_h2(f[4], f[5]) & relu_mask(hv.z), pack_h2(f[6], f[7]) & relu_mask(hv.w));
-                }
-            }
+            for (int c = 0; c < kChunks; ++c)
+                st_shared_v4(gbuf(j) + swz(r, uint32_t(c)), pack_h2(f[8 * c], f[8 * c + 1]) & relu_mask(hv[c].x),
+                             pack_h2(f[8 * c + 2], f[8 * c + 3]) & relu_mask(hv[c].y),
+                             pack_h2(f[8 * c + 4], f[8 * c + 5]) & relu_mask(hv[c].z),
+                             pack_h2(f[8 * c + 6], f[8 * c + 7]) & relu_mask(hv[c].w));
         };
 
         float loss_sum = 0.0f;
@@ -344,11 +352,13 @@ __global__ void __launch_bounds__(TrainWs<W>::kThreads, 1) nrc_train_ws_kernel(T
     #pragma unroll 1
             for (int j = nh; j >= 1; --j) {
                 if (nh == 5) NRC_WTRC(14 + 2 * (5 - j));
+                uint4 hv[kChunks];
+                mask_prefetch(j, hv);
                 mbar_wait(bar_d, d_phase);
                 d_phase ^= 1;
                 tc_fence_after();
                 if (nh == 5) NRC_WTRC(15 + 2 * (5 - j));
-                mask_epilogue(j);
+                mask_epilogue(j, hv);
                 if (nh == 5 && j >= 2) NRC_WTRC(24 + (5 - j));
                 hand_off();  // (wgrad_0 = g_1^T h_0 follows round 1 on the issuer: no gradient w.r.t. the encoding)
                 if (nh == 5 && j >= 2) NRC_WTRC(28 + (5 - j));
