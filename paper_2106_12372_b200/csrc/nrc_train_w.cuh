@@ -564,8 +564,11 @@ struct AdamWArgs {
     int npeer;
 };
 
+#ifndef NRC_ADAM_BOUNDS
+#define NRC_ADAM_BOUNDS __launch_bounds__(kAdamThreads, 1)
+#endif
 template <int W>
-__global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a) {
+__global__ void NRC_ADAM_BOUNDS nrc_adam_w_kernel(AdamWArgs a) {
     const NetRt<W> D(a.nh);  // padded(nh) is a multiple of 128 for every width and depth
     __shared__ float4 sred[kAdamWarps][32];
     const int lane = int(threadIdx.x & 31), wp = int(threadIdx.x >> 5);
@@ -601,18 +604,30 @@ __global__ void __launch_bounds__(kAdamThreads, 1) nrc_adam_w_kernel(AdamWArgs a
 #define NRC_ADAM_KIN 8
 #endif
         constexpr int kIn = NRC_ADAM_KIN;  // partial loads in flight per thread
+        if (a.tile_part != nullptr) {  // fused all-reduce: NVLink loads for peers
 #pragma unroll 1
-        for (int p0 = wp; p0 < a.np; p0 += kAdamWarps * kIn) {
-            float4 x[kIn];
+            for (int p0 = wp; p0 < a.np; p0 += kAdamWarps * kIn) {
+                float4 x[kIn];
 #pragma unroll
-            for (int u = 0; u < kIn; ++u) {
-                const int p = p0 + kAdamWarps * u;
-                x[u] = p >= a.np ? make_float4(0.f, 0.f, 0.f, 0.f)
-                       : a.tile_part != nullptr ? ld_sys_v4(a.tile_part[p] + k)  // fused all-reduce: NVLink loads for peers
-                                                : __ldcg(src + size_t(p) * stride);
+                for (int u = 0; u < kIn; ++u) {
+                    const int p = p0 + kAdamWarps * u;
+                    x[u] = p >= a.np ? make_float4(0.f, 0.f, 0.f, 0.f) : ld_sys_v4(a.tile_part[p] + k);
+                }
+#pragma unroll
+                for (int u = 0; u < kIn; ++u) s = f4_add(s, x[u]);
             }
+        } else {
+#pragma unroll 1
+            for (int p0 = wp; p0 < a.np; p0 += kAdamWarps * kIn) {
+                float4 x[kIn];
+                const float4* sp = src + size_t(p0) * stride;
 #pragma unroll
-            for (int u = 0; u < kIn; ++u) s = f4_add(s, x[u]);
+                for (int u = 0; u < kIn; ++u)
+                    x[u] = p0 + kAdamWarps * u >= a.np ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                       : __ldcg(sp + size_t(kAdamWarps * u) * stride);
+#pragma unroll
+                for (int u = 0; u < kIn; ++u) s = f4_add(s, x[u]);
+            }
         }
         if (trc) a.dbg[4086 + (blockIdx.x != 0)] = global_ns();
         sred[wp][lane] = s;
